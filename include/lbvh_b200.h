@@ -1,0 +1,193 @@
+/*
+ * lbvh_b200.h -- C ABI of the B200-native LBVH hot path.
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures.
+ * All array arguments are DEVICE pointers unless marked "host".  `stream` is
+ * a cudaStream_t passed as void*.  The library never allocates, frees or
+ * throws: callers own every buffer, including the workspace whose size the
+ * matching *_workspace_bytes() function reports.  Calls are stream-ordered
+ * and asynchronous; per-element failures are reported through a device
+ * status word (LBVH_FLAG_* bits, OR-ed by the kernels) that the caller reads
+ * back, mirroring the reference's per-query err/overflow arrays
+ * (pkg/src/lbvh/_kernels.py:3-5, traversal.py:168-170).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference checkout).
+ */
+#ifndef LBVH_B200_H
+#define LBVH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes (host side). */
+enum {
+    LBVH_OK = 0,
+    LBVH_ERR_INVALID_ARG = 1,  /* bad sizes / null pointers                */
+    LBVH_ERR_WORKSPACE = 2,    /* workspace smaller than *_workspace_bytes */
+    LBVH_ERR_CUDA = 3,         /* a CUDA launch or runtime call failed     */
+    LBVH_ERR_EMPTY_SCENE = 4,  /* n == 0 (tree.py:186-188)                 */
+    LBVH_ERR_TOO_LARGE = 5     /* n or nq beyond the supported 2^30 - 1    */
+};
+
+/* Device status-word bits. */
+#define LBVH_FLAG_STACK_EXHAUSTED 0x01u /* _kernels.py:220-223,274-277,397-400 */
+#define LBVH_FLAG_BUFFER_OVERFLOW 0x02u /* _kernels.py:267-270 (1P)          */
+#define LBVH_FLAG_NONFINITE 0x04u       /* validation.py:18-22               */
+#define LBVH_FLAG_INVERTED_BOX 0x08u    /* validation.py:75-77               */
+#define LBVH_FLAG_BAD_RADIUS 0x10u      /* validation.py:88-89               */
+#define LBVH_FLAG_BAD_K 0x20u           /* validation.py:100-101             */
+#define LBVH_FLAG_BAD_TREE 0x40u        /* child / leaf ordinal out of range */
+
+#define LBVH_STACK_CAPACITY 64 /* _kernels.py:15 */
+#define LBVH_MAX_ITEMS ((int64_t)1 << 30)
+
+/*
+ * Immutable tree view (pkg/src/lbvh/tree.py:122-174).  The reference arrays
+ * (node_mins/node_maxs (2n-1)x3 f32, left/right (n-1) i32, leaf_obj n i32)
+ * keep the reference's Karras ordinals: internal nodes 0..n-2 (root 0),
+ * leaf p at (n-1)+p.  `nodes` is the traversal layout: one 64-byte record
+ * per internal node holding both child boxes and both child links (a leaf
+ * child is stored as its object ordinal with bit 31 set).  `root_box` points
+ * to 6 floats (min xyz, max xyz) of node 0.
+ */
+typedef struct lbvh_tree {
+    int64_t n;
+    const float *node_mins;
+    const float *node_maxs;
+    const int32_t *left;
+    const int32_t *right;
+    const int32_t *leaf_obj;
+    const void *nodes;
+    const float *root_box;
+} lbvh_tree;
+
+#define LBVH_NODE_BYTES 64
+
+const char *lbvh_strerror(int code);
+/* Last CUDA error string seen by this thread (for LBVH_ERR_CUDA). */
+const char *lbvh_last_cuda_error(void);
+int lbvh_abi_version(void);
+
+/* ---------------------------------------------------------------- build */
+
+/* Workspace for lbvh_build / lbvh_sort_pairs / lbvh_query_order. */
+size_t lbvh_build_workspace_bytes(int64_t n);
+size_t lbvh_sort_workspace_bytes(int64_t n);
+
+/*
+ * build(boxes) -> Bvh          replaces tree.py:177-209
+ *   (check_boxes value checks validation.py:43-78, scene reduce tree.py:189-190,
+ *    f64 centroids tree.py:191-192, morton_codes morton.py:68-91, stable argsort
+ *    tree.py:194, leaf gather tree.py:196-199, generate_topology tree.py:85-105,
+ *    refit_bounds tree.py:108-119)
+ * mins, maxs: n x 3 f32 (maxs may equal mins for point input).
+ * Outputs: node_mins/node_maxs (2n-1)x3, left/right (n-1), leaf_obj n,
+ * root_box 6 floats (== scene box), nodes (n-1) x 64 B, status word.
+ * sorted_codes (optional, may be NULL): n u32 Morton codes in leaf order.
+ */
+int lbvh_build(const float *mins, const float *maxs, int64_t n, void *workspace,
+               size_t workspace_bytes, float *node_mins, float *node_maxs, int32_t *left,
+               int32_t *right, int32_t *leaf_obj, float *root_box, void *nodes,
+               uint32_t *sorted_codes, uint32_t *status, void *stream);
+
+/* morton_codes(points, scene_min, scene_max)   replaces morton.py:68-91
+ * points n x 3 f64 (device); scene bounds host doubles (smin[3], smax[3]). */
+int lbvh_morton_codes(const double *points, int64_t n, const double *scene_min_host,
+                      const double *scene_max_host, uint32_t *codes, void *stream);
+
+/* Stable LSD radix sort of (key, value) pairs, in place; sorts the low
+ * key_bits bits.  Replaces np.argsort(kind="stable") (tree.py:194) when
+ * values are the identity. */
+int lbvh_sort_pairs(uint32_t *keys, uint32_t *values, int64_t n, int key_bits,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* generate_topology(sorted_codes)   replaces tree.py:85-105 / _kernels.py:61-115
+ * left/right (n-1) i32, parent (2n-1) i32 (parent[0] = -1).  Workspace:
+ * lbvh_topology_workspace_bytes(n). */
+size_t lbvh_topology_workspace_bytes(int64_t n);
+int lbvh_generate_topology(const uint32_t *sorted_codes, int64_t n, int32_t *left,
+                           int32_t *right, int32_t *parent, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
+/* refit_bounds(node_mins, node_maxs, topology)   replaces tree.py:108-119 /
+ * _kernels.py:118-138: fills internal boxes from leaf boxes in place. */
+int lbvh_refit(float *node_mins, float *node_maxs, const int32_t *left,
+               const int32_t *right, const int32_t *parent, int64_t n, void *workspace,
+               size_t workspace_bytes, void *stream);
+
+/* Pack a reference-layout tree (e.g. a user-constructed Bvh) into the
+ * traversal layout.  Sets LBVH_FLAG_BAD_TREE on out-of-range links. */
+int lbvh_pack(const lbvh_tree *tree, void *nodes, float *root_box, uint32_t *status,
+              void *stream);
+
+/* Unpack: traversal layout + root box -> reference node_mins/node_maxs. */
+int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
+                      void *stream);
+
+/* ---------------------------------------------------------------- query */
+
+/* query_sort_order(centers, scene)   replaces traversal.py:146-165.
+ * order: nq u32 permutation.  scene_box: 6 floats DEVICE (tree root box). */
+size_t lbvh_query_workspace_bytes(int64_t nq);
+int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box,
+                     uint32_t *order, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
+/* Finite check of nq x 3 query centers and (optional) radii >= 0. */
+int lbvh_check_queries(const float *centers, int64_t nq, const float *radii,
+                       uint32_t *status, void *stream);
+
+/* spatial_pass(store=False)  replaces _kernels.py:179-228 (count pass of
+ * query_spatial_2p, traversal.py:197-201).  radii may be NULL -> radius.
+ * order may be NULL -> identity.  counts: nq i32. */
+int lbvh_spatial_count(const lbvh_tree *tree, const float *centers, const float *radii,
+                       float radius, const uint32_t *order, int64_t nq, int32_t *counts,
+                       uint32_t *status, void *stream);
+
+/* spatial_pass(store=True)  replaces _kernels.py:179-228 (fill pass,
+ * traversal.py:205-209); writes out[offsets[q] ...]. */
+int lbvh_spatial_fill(const lbvh_tree *tree, const float *centers, const float *radii,
+                      float radius, const uint32_t *order, int64_t nq,
+                      const int64_t *offsets, int32_t *out, uint32_t *status,
+                      void *stream);
+
+/* _exclusive_scan   replaces traversal.py:173-176: offsets[0]=0,
+ * offsets[i+1] = sum(counts[0..i]); offsets is nq+1 i64.  Also copies the
+ * total to *total_out (device, may be NULL). */
+size_t lbvh_scan_workspace_bytes(int64_t nq);
+int lbvh_exclusive_scan(const int32_t *counts, int64_t nq, int64_t *offsets,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* spatial_pass_buffered  replaces _kernels.py:231-282 (query_spatial_1p,
+ * traversal.py:214-248): buf nq x buffer_size i32, counts nq i32. */
+int lbvh_spatial_1p(const lbvh_tree *tree, const float *centers, const float *radii,
+                    float radius, const uint32_t *order, int64_t nq, int32_t *buf,
+                    int64_t buffer_size, int32_t *counts, uint32_t *status, void *stream);
+
+/* compact_rows  replaces _kernels.py:285-290. */
+int lbvh_compact(const int32_t *buf, int64_t buffer_size, const int32_t *counts,
+                 const int64_t *offsets, int64_t nq, int32_t *out, void *stream);
+
+/* kNN spans  replaces traversal.py:261-262: spans = min(k_q, n), offsets =
+ * scan(spans).  ks may be NULL -> k.  Sets LBVH_FLAG_BAD_K for k < 1 and
+ * writes max span to *max_span (device i32). */
+int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_t *offsets,
+                     int32_t *max_span, uint32_t *status, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
+/* knn_pass  replaces _kernels.py:328-414 (query_knn, traversal.py:251-272).
+ * max_span: host upper bound of min(k_q, n) (selects the kernel variant). */
+int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
+             int64_t nq, const int64_t *offsets, int64_t max_span, int32_t *out_idx,
+             float *out_dist, uint32_t *status, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LBVH_B200_H */

@@ -1,0 +1,90 @@
+"""Device plumbing: tensors, streams, workspaces, host<->device transfers.
+
+PyTorch is used only as the allocator / stream provider; all compute goes
+through the C ABI.  Host outputs are staged in pinned memory (torch's caching
+host allocator) and handed back as numpy views, so D2H runs at full PCIe
+speed and no extra host copy is made.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_NP2T = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+         np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
+         np.dtype(np.uint8): torch.uint8, np.dtype(np.uint32): torch.uint32}
+
+
+def device() -> torch.device:
+    _lib.lib()  # asserts CUDA + library
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def empty(shape, dtype, dev=None) -> torch.Tensor:
+    return torch.empty(shape, dtype=dtype, device=dev or device())
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device())
+
+
+def is_cuda_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def h2d(arr: np.ndarray) -> torch.Tensor:
+    """Host numpy -> device tensor (async from pinned memory, else staged)."""
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.to(device(), non_blocking=True)
+
+
+def pinned(shape, dtype) -> torch.Tensor:
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def d2h(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy view of a pinned host buffer (sync)."""
+    host = pinned(tuple(t.shape), t.dtype)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy()
+
+
+def d2h_many(*ts) -> list:
+    hosts = []
+    for t in ts:
+        if t is None:
+            hosts.append(None)
+            continue
+        h = pinned(tuple(t.shape), t.dtype)
+        h.copy_(t, non_blocking=True)
+        hosts.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [None if h is None else h.numpy() for h in hosts]
+
+
+class Status:
+    """A device status word plus a pinned readback slot."""
+
+    def __init__(self):
+        self.dev = torch.zeros(1, dtype=torch.int32, device=device())
+
+    @property
+    def ptr(self) -> int:
+        return self.dev.data_ptr()
+
+    def read(self) -> int:
+        return int(d2h(self.dev)[0]) & 0xFFFFFFFF

@@ -1,0 +1,134 @@
+"""ctypes binding of the C-ABI library ``_lib/liblbvh_b200.so``.
+
+This is the only route to the compute path: there is no CPU fallback.  If
+the library is missing or no CUDA device is visible, every batch operation
+raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "liblbvh_b200.so")
+
+STACK_CAPACITY = 64
+FLAG_STACK_EXHAUSTED = 0x01
+FLAG_BUFFER_OVERFLOW = 0x02
+FLAG_NONFINITE = 0x04
+FLAG_INVERTED_BOX = 0x08
+FLAG_BAD_RADIUS = 0x10
+FLAG_BAD_K = 0x20
+FLAG_BAD_TREE = 0x40
+NODE_BYTES = 64
+MAX_ITEMS = (1 << 30) - 1
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LbvhError(RuntimeError):
+    """A non-OK return code from the C ABI."""
+
+
+class CTree(ctypes.Structure):
+    """Mirror of ``struct lbvh_tree`` (include/lbvh_b200.h)."""
+
+    _fields_ = [("n", ctypes.c_int64),
+                ("node_mins", ctypes.c_void_p), ("node_maxs", ctypes.c_void_p),
+                ("left", ctypes.c_void_p), ("right", ctypes.c_void_p),
+                ("leaf_obj", ctypes.c_void_p), ("nodes", ctypes.c_void_p),
+                ("root_box", ctypes.c_void_p)]
+
+
+_SIGS = {
+    "lbvh_strerror": ([ctypes.c_int], ctypes.c_char_p),
+    "lbvh_last_cuda_error": ([], ctypes.c_char_p),
+    "lbvh_abi_version": ([], ctypes.c_int),
+    "lbvh_build_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_sort_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_topology_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_query_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_scan_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_build": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                    ctypes.c_size_t] + [ctypes.c_void_p] * 10, ctypes.c_int),
+    "lbvh_morton_codes": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_sort_pairs": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_generate_topology": ([ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 4 +
+                               [ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_refit": ([ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
+                                            ctypes.c_void_p], ctypes.c_int),
+    "lbvh_pack": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 4, ctypes.c_int),
+    "lbvh_unpack_boxes": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 3, ctypes.c_int),
+    "lbvh_query_order": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                          ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_check_queries": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_void_p], ctypes.c_int),
+    "lbvh_spatial_count": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                            ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_spatial_fill": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_exclusive_scan": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_spatial_1p": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
+                         ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+                        ctypes.c_int),
+    "lbvh_compact": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_knn_offsets": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                          ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_knn": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                  ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+}
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the library (no CUDA needed; used by the CPU tests)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"CUDA extension {path} is missing -- build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'`; "
+                "there is no CPU fallback")
+        lib = ctypes.CDLL(path)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def lib():
+    """The library, after asserting a CUDA device is present."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1908_11807_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return load_library()
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        l = load_library()
+        msg = l.lbvh_strerror(rc).decode()
+        if rc == 3:
+            msg += f" ({l.lbvh_last_cuda_error().decode()})"
+        raise LbvhError(f"liblbvh_b200: {msg}")
+
+
+def exported_symbols():
+    return sorted(_SIGS)

@@ -1,0 +1,504 @@
+// build.cu -- LBVH construction on sm_100a.
+//
+// Pipeline (reference tree.py:177-209):
+//   K1 scene_reduce_kernel   scene box + value checks       tree.py:189-190, validation.py:43-78
+//   K2 morton_kernel         f64 centroid + 30-bit code     tree.py:191-193, morton.py:68-91
+//   K3 sort_pairs            stable (code, index) sort      tree.py:194
+//   K4+K5 hierarchy_kernel   leaf gather + single-pass bottom-up hierarchy
+//                            emitting Karras ordinals + atomic-flag refit +
+//                            packed node records            tree.py:85-119, 196-199
+//
+// The hierarchy kernel is Apetrei's bottom-up construction: one thread per
+// leaf climbs; at every node it decides whether it is a left or right child
+// from the two boundary prefix lengths, meets its sibling at the split slot
+// through an atomic exchange, and the second arrival builds the parent.  The
+// node it builds gets exactly the Karras ordinal of the reference's
+// top-down generate_topology: a node [l, r] that is a left child has id r, a
+// right child has id l, the root id 0, leaf p id (n-1)+p.  So left/right,
+// node boxes and leaf order are byte-identical to the reference.
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace lbvh {
+namespace {
+
+constexpr int kReduceThreads = 256;
+
+__device__ __forceinline__ void warp_minmax(float v[6]) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float lo = __shfl_xor_sync(0xFFFFFFFFu, v[a], o);
+            float hi = __shfl_xor_sync(0xFFFFFFFFu, v[3 + a], o);
+            v[a] = fminf(v[a], lo);
+            v[3 + a] = fmaxf(v[3 + a], hi);
+        }
+    }
+}
+
+// K1: scene box (exact min/max) and the check_boxes value checks.  The last
+// CTA to finish folds the per-CTA partials (threadfence reduction).
+__global__ void __launch_bounds__(kReduceThreads)
+scene_reduce_kernel(const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
+                    float *__restrict__ partials, uint32_t *counter, float *__restrict__ scene,
+                    uint32_t *status) {
+    float v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    uint32_t bad = 0;
+    const bool same = (mins == maxs);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float lo = __ldcs(mins + 3 * i + a);
+            float hi = same ? lo : __ldcs(maxs + 3 * i + a);
+            if (!isfinite(lo) || !isfinite(hi)) bad |= LBVH_FLAG_NONFINITE;
+            if (lo > hi) bad |= LBVH_FLAG_INVERTED_BOX;
+            v[a] = fminf(v[a], lo);
+            v[3 + a] = fmaxf(v[3 + a], hi);
+        }
+    }
+    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (bad && lane_id() == 0) atomicOr(status, bad);
+    warp_minmax(v);
+    __shared__ float s_part[kReduceThreads / 32][6];
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5;
+    if (lane_id() == 0)
+        for (int a = 0; a < 6; ++a) s_part[warp][a] = v[a];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        int a = threadIdx.x;
+        float r = s_part[0][a];
+        for (int w = 1; w < kReduceThreads / 32; ++w)
+            r = a < 3 ? fminf(r, s_part[w][a]) : fmaxf(r, s_part[w][a]);
+        partials[blockIdx.x * 6 + a] = r;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < 6) {
+        int a = threadIdx.x;
+        float r = __ldcg(partials + a);
+        for (unsigned b = 1; b < gridDim.x; ++b) {
+            float x = __ldcg(partials + b * 6 + a);
+            r = a < 3 ? fminf(r, x) : fmaxf(r, x);
+        }
+        scene[a] = r;
+    }
+}
+
+// K2: codes of the f64 box centroids on the scene grid, plus iota values.
+__global__ void __launch_bounds__(256)
+morton_kernel(const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
+              const float *__restrict__ scene, uint32_t *__restrict__ codes,
+              uint32_t *__restrict__ iota) {
+    double lo[3], ext[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = (double)scene[a];
+        ext[a] = __dsub_rn((double)scene[3 + a], lo[a]);
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double c[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            // (f64(min) + max) * 0.5 -- tree.py:191-192
+            c[a] = __dmul_rn(__dadd_rn((double)__ldg(mins + 3 * i + a),
+                                       (double)__ldg(maxs + 3 * i + a)),
+                             0.5);
+        }
+        codes[i] = morton3(c[0], c[1], c[2], lo, ext);
+        if (iota) iota[i] = (uint32_t)i;
+    }
+}
+
+// Common-prefix length of augmented keys i, i+1 (code << 32 | position),
+// _kernels.py:50-58.  Keys are distinct, so the xor is never 0.
+__device__ __forceinline__ int delta(const uint32_t *__restrict__ codes, int64_t i) {
+    uint32_t a = __ldg(codes + i), b = __ldg(codes + i + 1);
+    if (a != b) return __clz(a ^ b);
+    return 32 + __clz((uint32_t)i ^ (uint32_t)(i + 1));
+}
+
+// Is [l, r] the left child of its parent?  Boundary prefixes are never equal.
+__device__ __forceinline__ bool is_left_child(const uint32_t *__restrict__ codes, int64_t n,
+                                              int64_t l, int64_t r) {
+    if (l == 0) return true;
+    if (r == n - 1) return false;
+    return delta(codes, r) > delta(codes, l - 1);
+}
+
+__device__ __forceinline__ void load_box_cg(const float *mins, const float *maxs, int64_t id,
+                                            Box &b) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        b.lo[a] = __ldcg(mins + 3 * id + a);
+        b.hi[a] = __ldcg(maxs + 3 * id + a);
+    }
+}
+
+__device__ __forceinline__ void store_box(float *mins, float *maxs, int64_t id, const Box &b) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        mins[3 * id + a] = b.lo[a];
+        maxs[3 * id + a] = b.hi[a];
+    }
+}
+
+__device__ __forceinline__ void store_packed(PackedNode *nodes, int64_t id, const Box &L,
+                                             const Box &R, int32_t lc, int32_t rc) {
+    PackedNode *p = nodes + id;
+    __stcg(&p->a, make_float4(L.lo[0], L.lo[1], L.lo[2], L.hi[0]));
+    __stcg(&p->b, make_float4(L.hi[1], L.hi[2], R.lo[0], R.lo[1]));
+    __stcg(&p->c, make_float4(R.lo[2], R.hi[0], R.hi[1], R.hi[2]));
+    __stcg(&p->d, make_int4(lc, rc, 0, 0));
+}
+
+// K4 + K5.  WITH_BOXES=false is the topology-only variant behind
+// lbvh_generate_topology (sorted codes in, left/right/parent out).
+template <bool WITH_BOXES>
+__global__ void __launch_bounds__(256)
+hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict__ perm,
+                 const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
+                 uint32_t *slots, float *node_mins, float *node_maxs, int32_t *__restrict__ left,
+                 int32_t *__restrict__ right, int32_t *__restrict__ parent,
+                 int32_t *__restrict__ leaf_obj, PackedNode *__restrict__ nodes,
+                 float *__restrict__ root_box) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t internal = n - 1;
+    Box mine;
+    int32_t my_link = 0;  // packed-layout link of the current node
+    if (WITH_BOXES) {
+        const uint32_t obj = __ldg(perm + p);
+        leaf_obj[p] = (int32_t)obj;
+        const bool same = (mins == maxs);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mine.lo[a] = __ldg(mins + 3 * (int64_t)obj + a);
+            mine.hi[a] = same ? mine.lo[a] : __ldg(maxs + 3 * (int64_t)obj + a);
+        }
+        store_box(node_mins, node_maxs, internal + p, mine);
+        my_link = (int32_t)(obj | kLeafTag);
+        if (n == 1) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                root_box[a] = mine.lo[a];
+                root_box[3 + a] = mine.hi[a];
+            }
+            return;
+        }
+    } else if (n == 1) {
+        if (parent) parent[0] = -1;
+        return;
+    }
+    int64_t l = p, r = p;
+    bool left_side = is_left_child(codes, n, l, r);
+    while (true) {
+        const int64_t g = left_side ? r : l - 1;
+        const uint32_t known = (uint32_t)(left_side ? l : r);
+        __threadfence();  // release this subtree's boxes before the handshake
+        const uint32_t other = atomicExch(slots + g, known + 1u);
+        if (other == 0) return;  // first arrival: sibling subtree not done
+        __threadfence();         // acquire the sibling's boxes
+        const int64_t pl = left_side ? l : (int64_t)(other - 1u);
+        const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
+        const int64_t lc = (pl == g) ? internal + g : g;
+        const int64_t rc = (g + 1 == pr) ? internal + g + 1 : g + 1;
+        const bool root = (pl == 0 && pr == n - 1);
+        const bool parent_left = root ? false : is_left_child(codes, n, pl, pr);
+        const int64_t pid = root ? 0 : (parent_left ? pr : pl);
+        left[pid] = (int32_t)lc;
+        right[pid] = (int32_t)rc;
+        if (parent) {
+            parent[lc] = (int32_t)pid;
+            parent[rc] = (int32_t)pid;
+            if (root) parent[0] = -1;
+        }
+        if (WITH_BOXES) {
+            const int64_t sib = left_side ? rc : lc;
+            Box sb;
+            load_box_cg(node_mins, node_maxs, sib, sb);
+            int32_t sib_link;
+            if (sib >= internal)
+                sib_link = (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
+            else
+                sib_link = (int32_t)sib;
+            const Box &L = left_side ? mine : sb;
+            const Box &R = left_side ? sb : mine;
+            Box P;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                P.lo[a] = min_left(L.lo[a], R.lo[a]);
+                P.hi[a] = max_left(L.hi[a], R.hi[a]);
+            }
+            store_packed(nodes, pid, L, R, left_side ? my_link : sib_link,
+                         left_side ? sib_link : my_link);
+            store_box(node_mins, node_maxs, pid, P);
+            mine = P;
+            my_link = (int32_t)pid;
+            if (root) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    root_box[a] = P.lo[a];
+                    root_box[3 + a] = P.hi[a];
+                }
+            }
+        }
+        if (root) return;
+        l = pl;
+        r = pr;
+        left_side = parent_left;
+    }
+}
+
+// Atomic-flag refit over an arbitrary (left, right, parent) topology --
+// refit_bounds (tree.py:108-119): leaf boxes in place, internal boxes filled.
+__global__ void __launch_bounds__(256)
+refit_kernel(float *node_mins, float *node_maxs, const int32_t *__restrict__ left,
+             const int32_t *__restrict__ right, const int32_t *__restrict__ parent, int64_t n,
+             uint32_t *visits) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int64_t node = (n - 1) + p;
+    while (true) {
+        const int64_t par = __ldg(parent + node);
+        if (par < 0) return;
+        __threadfence();
+        if (atomicAdd(visits + par, 1u) == 0) return;
+        __threadfence();
+        const int64_t lc = __ldg(left + par), rc = __ldg(right + par);
+        Box L, R, P;
+        load_box_cg(node_mins, node_maxs, lc, L);
+        load_box_cg(node_mins, node_maxs, rc, R);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            P.lo[a] = min_left(L.lo[a], R.lo[a]);
+            P.hi[a] = max_left(L.hi[a], R.hi[a]);
+        }
+        store_box(node_mins, node_maxs, par, P);
+        node = par;
+    }
+}
+
+__device__ __forceinline__ bool load_child(const lbvh_tree t, int64_t c, Box &b,
+                                           int32_t &link) {
+    const int64_t internal = t.n - 1;
+    if (c < 0 || c >= 2 * t.n - 1) return false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        b.lo[a] = __ldg(t.node_mins + 3 * c + a);
+        b.hi[a] = __ldg(t.node_maxs + 3 * c + a);
+    }
+    if (c >= internal) {
+        int32_t obj = __ldg(t.leaf_obj + (c - internal));
+        if (obj < 0) return false;
+        link = (int32_t)((uint32_t)obj | kLeafTag);
+    } else {
+        link = (int32_t)c;
+    }
+    return true;
+}
+
+// Reference layout -> traversal layout (user-built or modified trees).
+__global__ void __launch_bounds__(256)
+pack_kernel(const lbvh_tree t, PackedNode *__restrict__ nodes, float *__restrict__ root_box,
+            uint32_t *status) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            root_box[a] = __ldg(t.node_mins + a);
+            root_box[3 + a] = __ldg(t.node_maxs + a);
+        }
+    }
+    if (i >= t.n - 1) return;
+    Box L, R;
+    int32_t ll = 0, rl = 0;
+    bool ok = load_child(t, __ldg(t.left + i), L, ll);
+    ok = load_child(t, __ldg(t.right + i), R, rl) && ok;
+    if (!ok) {
+        flag(status, LBVH_FLAG_BAD_TREE);
+        L = Box{{0, 0, 0}, {0, 0, 0}};
+        R = L;
+        ll = rl = (int32_t)kLeafTag;
+    }
+    store_packed(nodes, i, L, R, ll, rl);
+}
+
+__global__ void __launch_bounds__(256)
+unpack_kernel(const lbvh_tree t, float *__restrict__ node_mins, float *__restrict__ node_maxs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            node_mins[a] = t.root_box[a];
+            node_maxs[a] = t.root_box[3 + a];
+        }
+    }
+    if (i >= t.n - 1) return;
+    const PackedNode *pn = reinterpret_cast<const PackedNode *>(t.nodes) + i;
+    float4 a = pn->a, b = pn->b, c = pn->c;
+    int64_t lc = t.left[i], rc = t.right[i];
+    node_mins[3 * lc] = a.x; node_mins[3 * lc + 1] = a.y; node_mins[3 * lc + 2] = a.z;
+    node_maxs[3 * lc] = a.w; node_maxs[3 * lc + 1] = b.x; node_maxs[3 * lc + 2] = b.y;
+    node_mins[3 * rc] = b.z; node_mins[3 * rc + 1] = b.w; node_mins[3 * rc + 2] = c.x;
+    node_maxs[3 * rc] = c.y; node_maxs[3 * rc + 1] = c.z; node_maxs[3 * rc + 2] = c.w;
+}
+
+__global__ void morton_f64_kernel(const double *__restrict__ pts, int64_t n, double lo0,
+                                  double lo1, double lo2, double hi0, double hi1, double hi2,
+                                  uint32_t *__restrict__ codes) {
+    double lo[3] = {lo0, lo1, lo2};
+    double ext[3] = {__dsub_rn(hi0, lo0), __dsub_rn(hi1, lo1), __dsub_rn(hi2, lo2)};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        codes[i] = morton3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], lo, ext);
+}
+
+unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
+    unsigned g = div_up(n, threads);
+    unsigned cap = kNumSMs * per_sm;
+    return g < cap ? (g ? g : 1) : cap;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- host API
+
+size_t build_workspace_bytes(int64_t n) {
+    size_t b = 0;
+    b += align_up(sizeof(uint32_t) * (size_t)n) * 2;             // codes + perm
+    b += align_up(sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1));  // handshake slots
+    b += align_up(sizeof(float) * 6 * kNumSMs * 8);              // reduce partials
+    b += align_up(sizeof(uint32_t) * 4);                         // reduce counter
+    b += sort_workspace_bytes(n);
+    return b + 1024;
+}
+
+int build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
+          float *node_mins, float *node_maxs, int32_t *left, int32_t *right, int32_t *leaf_obj,
+          float *root_box, void *nodes, uint32_t *sorted_codes, uint32_t *status,
+          cudaStream_t stream) {
+    if (n == 0) return LBVH_ERR_EMPTY_SCENE;
+    if (n < 0 || !mins || !maxs || !node_mins || !node_maxs || !leaf_obj || !root_box ||
+        !status)
+        return LBVH_ERR_INVALID_ARG;
+    if (n > 1 && (!left || !right || !nodes)) return LBVH_ERR_INVALID_ARG;
+    if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    if (ws_bytes < build_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+    Carve c(ws, ws_bytes);
+    uint32_t *codes = c.take<uint32_t>(n);
+    uint32_t *perm = c.take<uint32_t>(n);
+    size_t zero_begin = align_up(c.off);
+    uint32_t *slots = c.take<uint32_t>(n > 1 ? n - 1 : 1);
+    uint32_t *counter = c.take<uint32_t>(4);
+    size_t zero_end = c.off;
+    float *partials = c.take<float>(6 * kNumSMs * 8);
+    void *sort_ws = c.take<char>(sort_workspace_bytes(n));
+    if (!c.ok()) return LBVH_ERR_WORKSPACE;
+    cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
+
+    unsigned rg = grid_for(n, kReduceThreads, 4);
+    scene_reduce_kernel<<<rg, kReduceThreads, 0, stream>>>(mins, maxs, n, partials, counter,
+                                                           root_box, status);
+    unsigned mg = grid_for(n, 256, 16);
+    morton_kernel<<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm);
+    int rc = sort_pairs(codes, perm, n, 30, sort_ws, sort_workspace_bytes(n), stream);
+    if (rc != LBVH_OK) return rc;
+    hierarchy_kernel<true><<<div_up(n, 256), 256, 0, stream>>>(
+        codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
+        leaf_obj, (PackedNode *)nodes, root_box);
+    if (sorted_codes)
+        cudaMemcpyAsync(sorted_codes, codes, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
+                        stream);
+    return check_launch();
+}
+
+size_t topology_workspace_bytes(int64_t n) {
+    return align_up(sizeof(uint32_t) * (size_t)(n > 1 ? n : 1)) + 256;
+}
+
+int generate_topology(const uint32_t *codes, int64_t n, int32_t *left, int32_t *right,
+                      int32_t *parent, void *ws, size_t ws_bytes, cudaStream_t stream) {
+    if (n == 0) return LBVH_ERR_EMPTY_SCENE;
+    if (n < 0 || !codes || !parent || (n > 1 && (!left || !right))) return LBVH_ERR_INVALID_ARG;
+    if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    if (ws_bytes < topology_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+    uint32_t *slots = (uint32_t *)ws;
+    cudaMemsetAsync(slots, 0, sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1), stream);
+    hierarchy_kernel<false><<<div_up(n, 256), 256, 0, stream>>>(
+        codes, nullptr, nullptr, nullptr, n, slots, nullptr, nullptr, left, right, parent,
+        nullptr, nullptr, nullptr);
+    return check_launch();
+}
+
+int refit(float *node_mins, float *node_maxs, const int32_t *left, const int32_t *right,
+          const int32_t *parent, int64_t n, void *ws, size_t ws_bytes, cudaStream_t stream) {
+    if (n < 0 || !node_mins || !node_maxs) return LBVH_ERR_INVALID_ARG;
+    if (n <= 1) return LBVH_OK;
+    if (!left || !right || !parent) return LBVH_ERR_INVALID_ARG;
+    if (ws_bytes < topology_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+    uint32_t *visits = (uint32_t *)ws;
+    cudaMemsetAsync(visits, 0, sizeof(uint32_t) * (size_t)(n - 1), stream);
+    refit_kernel<<<div_up(n, 256), 256, 0, stream>>>(node_mins, node_maxs, left, right,
+                                                      parent, n, visits);
+    return check_launch();
+}
+
+int pack(const lbvh_tree *t, void *nodes, float *root_box, uint32_t *status,
+         cudaStream_t stream) {
+    if (!t || t->n < 1 || !t->node_mins || !t->node_maxs || !t->leaf_obj || !root_box)
+        return LBVH_ERR_INVALID_ARG;
+    if (t->n > 1 && (!t->left || !t->right || !nodes)) return LBVH_ERR_INVALID_ARG;
+    int64_t work = t->n > 1 ? t->n - 1 : 1;
+    pack_kernel<<<div_up(work, 256), 256, 0, stream>>>(*t, (PackedNode *)nodes, root_box,
+                                                       status);
+    return check_launch();
+}
+
+int unpack_boxes(const lbvh_tree *t, float *node_mins, float *node_maxs, cudaStream_t stream) {
+    if (!t || t->n < 1 || !t->root_box || !node_mins || !node_maxs) return LBVH_ERR_INVALID_ARG;
+    if (t->n > 1 && (!t->left || !t->right || !t->nodes)) return LBVH_ERR_INVALID_ARG;
+    int64_t work = t->n > 1 ? t->n - 1 : 1;
+    unpack_kernel<<<div_up(work, 256), 256, 0, stream>>>(*t, node_mins, node_maxs);
+    return check_launch();
+}
+
+int morton_codes_f64(const double *pts, int64_t n, const double *lo, const double *hi,
+                     uint32_t *codes, cudaStream_t stream) {
+    if (n < 0 || (n > 0 && (!pts || !codes)) || !lo || !hi) return LBVH_ERR_INVALID_ARG;
+    if (n == 0) return LBVH_OK;
+    morton_f64_kernel<<<grid_for(n, 256, 16), 256, 0, stream>>>(pts, n, lo[0], lo[1], lo[2],
+                                                               hi[0], hi[1], hi[2], codes);
+    return check_launch();
+}
+
+// Query Morton codes on the tree's scene box + stable sort -> order.
+size_t query_workspace_bytes(int64_t nq) {
+    return align_up(sizeof(uint32_t) * (size_t)nq) + sort_workspace_bytes(nq) + 512;
+}
+
+int query_order(const float *centers, int64_t nq, const float *scene, uint32_t *order,
+                void *ws, size_t ws_bytes, cudaStream_t stream) {
+    if (nq < 0 || (nq > 0 && (!centers || !order)) || !scene) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0) return LBVH_OK;
+    if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    if (ws_bytes < query_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
+    Carve c(ws, ws_bytes);
+    uint32_t *codes = c.take<uint32_t>(nq);
+    void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
+    morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq, scene, codes,
+                                                             order);
+    int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream);
+    if (rc != LBVH_OK) return rc;
+    return check_launch();
+}
+
+}  // namespace lbvh

@@ -1,0 +1,178 @@
+// capi.cu -- extern "C" entry points (include/lbvh_b200.h).
+
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace lbvh {
+
+static thread_local char g_cuda_err[256] = "";
+
+void set_cuda_error(cudaError_t e) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e),
+             cudaGetErrorString(e));
+}
+
+int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_cuda_error(e);
+        return LBVH_ERR_CUDA;
+    }
+    return LBVH_OK;
+}
+
+// defined in build.cu / traverse.cu / scan.cu
+size_t build_workspace_bytes(int64_t n);
+int build(const float *, const float *, int64_t, void *, size_t, float *, float *, int32_t *,
+          int32_t *, int32_t *, float *, void *, uint32_t *, uint32_t *, cudaStream_t);
+size_t topology_workspace_bytes(int64_t n);
+int generate_topology(const uint32_t *, int64_t, int32_t *, int32_t *, int32_t *, void *, size_t,
+                      cudaStream_t);
+int refit(float *, float *, const int32_t *, const int32_t *, const int32_t *, int64_t, void *,
+          size_t, cudaStream_t);
+int pack(const lbvh_tree *, void *, float *, uint32_t *, cudaStream_t);
+int unpack_boxes(const lbvh_tree *, float *, float *, cudaStream_t);
+int morton_codes_f64(const double *, int64_t, const double *, const double *, uint32_t *,
+                     cudaStream_t);
+size_t query_workspace_bytes(int64_t nq);
+int query_order(const float *, int64_t, const float *, uint32_t *, void *, size_t, cudaStream_t);
+int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
+                  int64_t, int32_t *, uint32_t *, cudaStream_t);
+int spatial_fill(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
+                 int64_t, const int64_t *, int32_t *, uint32_t *, cudaStream_t);
+int spatial_1p(const lbvh_tree *, const float *, const float *, float, const uint32_t *, int64_t,
+               int32_t *, int64_t, int32_t *, uint32_t *, cudaStream_t);
+int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t, int32_t *,
+            cudaStream_t);
+int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
+                void *, size_t, cudaStream_t);
+int knn(const lbvh_tree *, const float *, const uint32_t *, int64_t, const int64_t *, int64_t,
+        int32_t *, float *, uint32_t *, cudaStream_t);
+int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
+
+}  // namespace lbvh
+
+using namespace lbvh;
+
+#define S(x) ((cudaStream_t)(x))
+
+extern "C" {
+
+const char *lbvh_strerror(int code) {
+    switch (code) {
+    case LBVH_OK: return "ok";
+    case LBVH_ERR_INVALID_ARG: return "invalid argument";
+    case LBVH_ERR_WORKSPACE: return "workspace too small";
+    case LBVH_ERR_CUDA: return "CUDA error";
+    case LBVH_ERR_EMPTY_SCENE: return "empty scene";
+    case LBVH_ERR_TOO_LARGE: return "too many items (limit 2^30 - 1)";
+    default: return "unknown error";
+    }
+}
+
+const char *lbvh_last_cuda_error(void) { return g_cuda_err; }
+
+int lbvh_abi_version(void) { return 1; }
+
+size_t lbvh_build_workspace_bytes(int64_t n) { return build_workspace_bytes(n); }
+size_t lbvh_sort_workspace_bytes(int64_t n) { return sort_workspace_bytes(n); }
+size_t lbvh_topology_workspace_bytes(int64_t n) { return topology_workspace_bytes(n); }
+size_t lbvh_query_workspace_bytes(int64_t nq) { return query_workspace_bytes(nq); }
+size_t lbvh_scan_workspace_bytes(int64_t nq) { return scan_workspace_bytes(nq); }
+
+int lbvh_build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
+               float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
+               int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
+               uint32_t *status, void *stream) {
+    return build(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left, right, leaf_obj,
+                 root_box, nodes, sorted_codes, status, S(stream));
+}
+
+int lbvh_morton_codes(const double *pts, int64_t n, const double *lo, const double *hi,
+                      uint32_t *codes, void *stream) {
+    return morton_codes_f64(pts, n, lo, hi, codes, S(stream));
+}
+
+int lbvh_sort_pairs(uint32_t *keys, uint32_t *values, int64_t n, int key_bits, void *ws,
+                    size_t ws_bytes, void *stream) {
+    if (n < 0 || (n > 0 && (!keys || !values))) return LBVH_ERR_INVALID_ARG;
+    return sort_pairs(keys, values, n, key_bits, ws, ws_bytes, S(stream));
+}
+
+int lbvh_generate_topology(const uint32_t *codes, int64_t n, int32_t *left, int32_t *right,
+                           int32_t *parent, void *ws, size_t ws_bytes, void *stream) {
+    return generate_topology(codes, n, left, right, parent, ws, ws_bytes, S(stream));
+}
+
+int lbvh_refit(float *node_mins, float *node_maxs, const int32_t *left, const int32_t *right,
+               const int32_t *parent, int64_t n, void *ws, size_t ws_bytes, void *stream) {
+    return refit(node_mins, node_maxs, left, right, parent, n, ws, ws_bytes, S(stream));
+}
+
+int lbvh_pack(const lbvh_tree *tree, void *nodes, float *root_box, uint32_t *status,
+              void *stream) {
+    return pack(tree, nodes, root_box, status, S(stream));
+}
+
+int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
+                      void *stream) {
+    return unpack_boxes(tree, node_mins, node_maxs, S(stream));
+}
+
+int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box, uint32_t *order,
+                     void *ws, size_t ws_bytes, void *stream) {
+    return query_order(centers, nq, scene_box, order, ws, ws_bytes, S(stream));
+}
+
+int lbvh_check_queries(const float *centers, int64_t nq, const float *radii, uint32_t *status,
+                       void *stream) {
+    return check_queries(centers, nq, radii, status, S(stream));
+}
+
+int lbvh_spatial_count(const lbvh_tree *tree, const float *centers, const float *radii,
+                       float radius, const uint32_t *order, int64_t nq, int32_t *counts,
+                       uint32_t *status, void *stream) {
+    return spatial_count(tree, centers, radii, radius, order, nq, counts, status, S(stream));
+}
+
+int lbvh_spatial_fill(const lbvh_tree *tree, const float *centers, const float *radii,
+                      float radius, const uint32_t *order, int64_t nq, const int64_t *offsets,
+                      int32_t *out, uint32_t *status, void *stream) {
+    return spatial_fill(tree, centers, radii, radius, order, nq, offsets, out, status,
+                        S(stream));
+}
+
+int lbvh_exclusive_scan(const int32_t *counts, int64_t nq, int64_t *offsets, void *ws,
+                        size_t ws_bytes, void *stream) {
+    return scan_counts(counts, nq, offsets, ws, ws_bytes, S(stream));
+}
+
+int lbvh_spatial_1p(const lbvh_tree *tree, const float *centers, const float *radii,
+                    float radius, const uint32_t *order, int64_t nq, int32_t *buf,
+                    int64_t buffer_size, int32_t *counts, uint32_t *status, void *stream) {
+    return spatial_1p(tree, centers, radii, radius, order, nq, buf, buffer_size, counts, status,
+                      S(stream));
+}
+
+int lbvh_compact(const int32_t *buf, int64_t buffer_size, const int32_t *counts,
+                 const int64_t *offsets, int64_t nq, int32_t *out, void *stream) {
+    return compact(buf, buffer_size, counts, offsets, nq, out, S(stream));
+}
+
+int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_t *offsets,
+                     int32_t *max_span, uint32_t *status, void *ws, size_t ws_bytes,
+                     void *stream) {
+    return knn_offsets(ks, k, n, nq, offsets, max_span, status, ws, ws_bytes, S(stream));
+}
+
+int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order, int64_t nq,
+             const int64_t *offsets, int64_t max_span, int32_t *out_idx, float *out_dist,
+             uint32_t *status, void *stream) {
+    return knn(tree, centers, order, nq, offsets, max_span, out_idx, out_dist, status,
+               S(stream));
+}
+
+}  // extern "C"

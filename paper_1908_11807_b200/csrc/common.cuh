@@ -1,0 +1,110 @@
+// common.cuh -- shared device helpers for the sm_100a LBVH kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lbvh_b200.h"
+
+namespace lbvh {
+
+constexpr int kStack = LBVH_STACK_CAPACITY;
+constexpr uint32_t kLeafTag = 0x80000000u;
+constexpr int kNumSMs = 148;  // B200
+
+// Traversal layout of one internal node: both child boxes + both links,
+// 64 bytes = four 128-bit loads, 64-byte aligned (half an L2 line).
+//   a = {L.min.x, L.min.y, L.min.z, L.max.x}
+//   b = {L.max.y, L.max.z, R.min.x, R.min.y}
+//   c = {R.min.z, R.max.x, R.max.y, R.max.z}
+//   d = {left link, right link, 0, 0}; a leaf link is obj | kLeafTag.
+struct __align__(64) PackedNode {
+    float4 a, b, c;
+    int4 d;
+};
+static_assert(sizeof(PackedNode) == LBVH_NODE_BYTES, "packed node must be 64 B");
+
+struct Box {
+    float lo[3], hi[3];
+};
+
+// Reference box distance (_kernels.py:146-176): per axis the clamp gap,
+// squared and accumulated x -> y -> z in fp32, every op round-to-nearest and
+// unfused.  max(lo - v, v - hi, 0) equals the reference's branch: when v < lo
+// the first term is the (positive, exactly rounded) gap, when v > hi the
+// second is, otherwise both are <= 0; adding a +0 gap term is the identity,
+// matching the reference's "skip axis".
+__device__ __forceinline__ float gap(float v, float lo, float hi) {
+    return fmaxf(fmaxf(__fsub_rn(lo, v), __fsub_rn(v, hi)), 0.0f);
+}
+
+__device__ __forceinline__ float box_dist_sq(float px, float py, float pz, float lx,
+                                             float ly, float lz, float hx, float hy,
+                                             float hz) {
+    float tx = gap(px, lx, hx), ty = gap(py, ly, hy), tz = gap(pz, lz, hz);
+    float d = __fmul_rn(tx, tx);
+    d = __fadd_rn(d, __fmul_rn(ty, ty));
+    d = __fadd_rn(d, __fmul_rn(tz, tz));
+    return d;
+}
+
+// Refit tie rules of numba's min/max (first argument wins ties,
+// _kernels.py:136-137): matters only for signed zeros.
+__device__ __forceinline__ float min_left(float l, float r) { return (r < l) ? r : l; }
+__device__ __forceinline__ float max_left(float l, float r) { return (r > l) ? r : l; }
+
+__device__ __forceinline__ void flag(uint32_t *status, uint32_t bits) {
+    if (status) atomicOr(status, bits);
+}
+
+// Morton (morton.py:52-58, 68-91): f64 normalisation, correctly rounded.
+__device__ __forceinline__ uint32_t spread_bits(uint32_t v) {
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__device__ __forceinline__ uint32_t grid_cell(double c, double lo, double ext) {
+    double t = 0.0;
+    if (ext > 0.0) t = __ddiv_rn(__dsub_rn(c, lo), ext);
+    t = t < 0.0 ? 0.0 : t;
+    t = t > 1.0 ? 1.0 : t;
+    uint32_t g = (uint32_t)__double2uint_rz(__dmul_rn(t, 1024.0));
+    return g < 1023u ? g : 1023u;
+}
+
+__device__ __forceinline__ uint32_t morton3(double x, double y, double z, const double *lo,
+                                            const double *ext) {
+    return (spread_bits(grid_cell(x, lo[0], ext[0])) << 2) |
+           (spread_bits(grid_cell(y, lo[1], ext[1])) << 1) |
+           spread_bits(grid_cell(z, lo[2], ext[2]));
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+template <typename T>
+__device__ __forceinline__ T ld_volatile(const T *p) {
+    return *reinterpret_cast<const volatile T *>(p);
+}
+
+inline unsigned int div_up(int64_t a, int64_t b) { return (unsigned int)((a + b - 1) / b); }
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller-owned workspace.
+struct Carve {
+    char *base;
+    size_t off, cap;
+    __host__ Carve(void *p, size_t c) : base((char *)p), off(0), cap(c) {}
+    template <typename T>
+    __host__ T *take(size_t count) {
+        size_t o = align_up(off);
+        off = o + sizeof(T) * count;
+        return (T *)(base + o);
+    }
+    __host__ bool ok() const { return off <= cap; }
+};
+
+}  // namespace lbvh

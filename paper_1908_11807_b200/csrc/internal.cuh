@@ -1,0 +1,24 @@
+// internal.cuh -- host-side declarations shared between translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lbvh {
+
+// Records the CUDA error string for lbvh_last_cuda_error(); returns
+// LBVH_ERR_CUDA on a pending launch error, LBVH_OK otherwise.
+int check_launch();
+void set_cuda_error(cudaError_t e);
+
+size_t sort_workspace_bytes(int64_t n);
+int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+               size_t ws_bytes, cudaStream_t stream);
+
+size_t scan_workspace_bytes(int64_t n);
+// offsets[0] = 0, offsets[i+1] = offsets[i] + f(i); f reads counts (i32) or
+// the per-query kNN span min(k_q, n).
+int scan_counts(const int32_t *counts, int64_t n, int64_t *offsets, void *ws,
+                size_t ws_bytes, cudaStream_t stream);
+
+}  // namespace lbvh

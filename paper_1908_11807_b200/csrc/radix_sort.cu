@@ -1,0 +1,264 @@
+// radix_sort.cu -- stable LSD radix sort of (u32 key, u32 value) pairs.
+//
+// Replaces np.argsort(codes, kind="stable") (reference tree.py:194,
+// traversal.py:159): sorting (code, index) pairs with a stable LSD sort gives
+// exactly the stable argsort.  One-sweep design (Adinets & Merrill): one
+// upfront pass builds the digit histograms of every digit position, then each
+// digit pass is a single kernel that ranks a 4096-key tile in shared memory,
+// resolves its global offsets with a decoupled look-back over preceding tiles
+// and scatters.  8-bit digits; the 30-bit Morton keys take 4 passes.
+//
+// HBM traffic per pass: 8 B read + 8 B written per pair; histogram pass 4 B.
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace lbvh {
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kItems = 16;
+constexpr int kTile = kSortThreads * kItems;  // 4096
+constexpr int kMaxPasses = 4;
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagPrefix = 2u << 30;
+constexpr uint32_t kCountMask = (1u << 30) - 1;
+
+constexpr int kHistThreads = 512;
+constexpr int kHistItems = 16;
+
+// Digit histograms of every pass in one read of the keys.
+__global__ void __launch_bounds__(kHistThreads)
+histogram_kernel(const uint32_t *__restrict__ keys, int64_t n, int passes,
+                 uint32_t *__restrict__ hist) {
+    __shared__ uint32_t s_hist[kMaxPasses][kRadix];
+    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x)
+        (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * kHistThreads * kHistItems;
+    for (int j = 0; j < kHistItems; ++j) {
+        int64_t i = base + (int64_t)j * kHistThreads + threadIdx.x;
+        if (i < n) {
+            uint32_t k = __ldcs(keys + i);
+            for (int p = 0; p < passes; ++p)
+                atomicAdd(&s_hist[p][(k >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
+        uint32_t c = (&s_hist[0][0])[i];
+        if (c) atomicAdd(hist + i, c);
+    }
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// One digit pass.  Tiles are claimed in order through `tile_counter`, so a
+// tile only ever waits on tiles already owned by running CTAs.
+__global__ void __launch_bounds__(kSortThreads)
+onesweep_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t n,
+                int shift, const uint32_t *__restrict__ hist, uint32_t *lookback,
+                uint32_t *tile_counter) {
+    __shared__ uint32_t s_keys[kTile];
+    __shared__ uint32_t s_vals[kTile];
+    __shared__ uint32_t s_warp[kSortWarps][kRadix];  // counts -> warp exclusive offsets
+    __shared__ uint32_t s_local[kRadix];             // digit start within the tile
+    __shared__ int64_t s_global[kRadix];             // global dest of tile position 0 of digit
+    __shared__ uint32_t s_scan[kSortWarps];
+    __shared__ uint32_t s_tile;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&s_warp[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t tile_base = (int64_t)tile * kTile;
+    const int64_t warp_base = tile_base + (int64_t)warp * 32 * kItems;
+
+    // Warp-striped load: item j of a lane sits at warp_base + j*32 + lane, so
+    // (j, lane) order is position order and the ranking below is stable.
+    uint32_t key[kItems], val[kItems], rank[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        int64_t i = warp_base + j * 32 + lane;
+        bool ok = i < n;
+        key[j] = ok ? __ldcs(keys_in + i) : 0xFFFFFFFFu;  // pads sort last
+        val[j] = ok ? __ldcs(vals_in + i) : 0u;
+    }
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        uint32_t d = (key[j] >> shift) & (kRadix - 1);
+        uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        int leader = __ffs(peers) - 1;
+        uint32_t before = 0;
+        if (lane == leader) {
+            before = s_warp[warp][d];
+            s_warp[warp][d] = before + __popc(peers);
+        }
+        before = __shfl_sync(0xFFFFFFFFu, before, leader);
+        rank[j] = before + __popc(peers & lt);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // Thread tid owns digit tid: exclusive scan over warps, tile total.
+    const uint32_t d = tid;
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+        uint32_t c = s_warp[w][d];
+        s_warp[w][d] = total;
+        total += c;
+    }
+    // Publish the tile aggregate (tile 0 publishes its inclusive prefix).
+    uint32_t *my_slot = lookback + (size_t)tile * kRadix + d;
+    if (tile == 0)
+        atomicExch(my_slot, kFlagPrefix | total);
+    else
+        atomicExch(my_slot, kFlagAgg | total);
+
+    // Block-wide exclusive scan of digit totals -> tile-local digit starts.
+    uint32_t incl = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    uint32_t warp_prefix = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) warp_prefix += (w < warp) ? s_scan[w] : 0u;
+    const uint32_t local_start = warp_prefix + incl - total;
+    s_local[d] = local_start;
+
+    // Decoupled look-back for digit d.
+    uint32_t excl = 0;
+    if (tile > 0) {
+        int64_t t = (int64_t)tile - 1;
+        while (true) {
+            uint32_t v = ld_volatile(lookback + (size_t)t * kRadix + d);
+            if ((v & ~kCountMask) == 0) continue;  // not yet published
+            excl += v & kCountMask;
+            if (v & kFlagPrefix) break;
+            --t;
+        }
+        atomicExch(my_slot, kFlagPrefix | (excl + total));
+    }
+    s_global[d] = (int64_t)hist[d] + excl - local_start;
+    __syncthreads();
+
+    // Scatter into shared memory in tile-sorted order.
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        uint32_t dj = (key[j] >> shift) & (kRadix - 1);
+        uint32_t pos = s_local[dj] + s_warp[warp][dj] + rank[j];
+        s_keys[pos] = key[j];
+        s_vals[pos] = val[j];
+    }
+    __syncthreads();
+
+    // Pads (key 0xFFFFFFFF, positions >= n) are last in tile order.
+    const int64_t valid = (n - tile_base) < kTile ? (n - tile_base) : kTile;
+#pragma unroll 4
+    for (int i = tid; i < kTile; i += kSortThreads) {
+        if (i < valid) {
+            uint32_t k = s_keys[i];
+            int64_t dst = s_global[(k >> shift) & (kRadix - 1)] + i;
+            keys_out[dst] = k;
+            vals_out[dst] = s_vals[i];
+        }
+    }
+}
+
+__global__ void exclusive_hist_kernel(uint32_t *hist, int passes) {
+    // One warp per pass: exclusive scan of 256 digit counts in place.
+    int p = blockIdx.x;
+    if (p >= passes) return;
+    uint32_t *h = hist + p * kRadix;
+    int lane = threadIdx.x;
+    uint32_t c[8];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        c[j] = h[lane * 8 + j];
+        s += c[j];
+    }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    uint32_t run = incl - s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        h[lane * 8 + j] = run;
+        run += c[j];
+    }
+}
+
+}  // namespace
+
+size_t sort_workspace_bytes(int64_t n) {
+    int64_t tiles = (n + kTile - 1) / kTile;
+    size_t b = 0;
+    b += align_up(sizeof(uint32_t) * (size_t)n) * 2;                  // ping-pong
+    b += align_up(sizeof(uint32_t) * kMaxPasses * kRadix);           // hist
+    b += align_up(sizeof(uint32_t) * kMaxPasses * (size_t)tiles * kRadix);  // look-back
+    b += align_up(sizeof(uint32_t) * kMaxPasses);                    // tile counters
+    return b + 256;
+}
+
+int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+               size_t ws_bytes, cudaStream_t stream) {
+    if (n <= 1) return LBVH_OK;
+    if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    if (key_bits < 1 || key_bits > 32) return LBVH_ERR_INVALID_ARG;
+    if (ws_bytes < sort_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+    const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
+    const int64_t tiles = (n + kTile - 1) / kTile;
+    Carve c(ws, ws_bytes);
+    uint32_t *k_alt = c.take<uint32_t>(n);
+    uint32_t *v_alt = c.take<uint32_t>(n);
+    // hist, look-back and counters are contiguous so one memset clears them.
+    size_t zero_begin = align_up(c.off);
+    uint32_t *hist = c.take<uint32_t>(kMaxPasses * kRadix);
+    uint32_t *lookback = c.take<uint32_t>((size_t)kMaxPasses * tiles * kRadix);
+    uint32_t *counters = c.take<uint32_t>(kMaxPasses);
+    size_t zero_end = c.off;
+    cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
+
+    unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
+    histogram_kernel<<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, hist);
+    exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes);
+
+    uint32_t *ks = keys, *vs = vals, *kd = k_alt, *vd = v_alt;
+    for (int p = 0; p < passes; ++p) {
+        onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, stream>>>(
+            ks, vs, kd, vd, n, p * kRadixBits, hist + p * kRadix,
+            lookback + (size_t)p * tiles * kRadix, counters + p);
+        uint32_t *t = ks; ks = kd; kd = t;
+        t = vs; vs = vd; vd = t;
+    }
+    if (ks != keys) {
+        cudaMemcpyAsync(keys, ks, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream);
+        cudaMemcpyAsync(vals, vs, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream);
+    }
+    return check_launch();
+}
+
+}  // namespace lbvh

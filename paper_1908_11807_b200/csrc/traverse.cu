@@ -1,0 +1,450 @@
+// traverse.cu -- batched radius and k-nearest traversal on sm_100a.
+//
+//   spatial_kernel<COUNT>   spatial_pass(store=False)   _kernels.py:179-228
+//   spatial_kernel<FILL>    spatial_pass(store=True)    _kernels.py:179-228
+//   spatial_kernel<BUFFER>  spatial_pass_buffered       _kernels.py:231-282
+//   compact_kernel          compact_rows                _kernels.py:285-290
+//   knn_kernel<K>           knn_pass, k <= K            _kernels.py:293-414
+//   knn_heap_kernel         knn_pass, any k (heap in the output span)
+//
+// One thread per query slot s; slot s serves query order[s], so Morton-sorted
+// queries put spatially close queries in the same warp and the same CTA
+// wave, and their node fetches hit in L1/L2.  Each internal node is one
+// 64-byte record (both child boxes + links), fetched with four 128-bit
+// loads.  Traversal order, stack discipline and the 64-entry stack limit
+// are the reference's, so hit order within a span and stack-exhaustion
+// behaviour are identical; kNN keeps a register-resident sorted list of
+// (dist^2, ordinal) pairs instead of the reference's heap, which yields the
+// same unique k smallest under the lexicographic order.
+
+#include <float.h>
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace lbvh {
+namespace {
+
+enum SpatialMode { kCount = 0, kFill = 1, kBuffer = 2 };
+
+__device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, int32_t id,
+                                          float4 &a, float4 &b, float4 &c, int4 &d) {
+    const PackedNode *p = nodes + id;
+    a = __ldg(&p->a);
+    b = __ldg(&p->b);
+    c = __ldg(&p->c);
+    d = __ldg(&p->d);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
+               const float *__restrict__ radii, float radius, const uint32_t *__restrict__ order,
+               int64_t nq, int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
+               int32_t *__restrict__ out, int64_t cap, uint32_t *status) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
+                pz = __ldg(centers + 3 * q + 2);
+    const float r = radii ? __ldg(radii + q) : radius;
+    const float r2 = __fmul_rn(r, r);
+    int64_t base = 0;
+    if (MODE == kFill) base = __ldg(offsets + q);
+    if (MODE == kBuffer) base = q * cap;
+    int32_t cnt = 0;
+    if (t.n == 1) {
+        const float *bx = t.root_box;
+        if (box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]) <= r2) {
+            if (MODE != kCount) out[base] = __ldg(t.leaf_obj);
+            cnt = 1;
+        }
+        if (MODE != kFill) counts[q] = cnt;
+        return;
+    }
+    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    int32_t stack[kStack];
+    int sp = 1;
+    stack[0] = 0;
+    uint32_t fail = 0;
+    while (sp > 0) {
+        const int32_t node = stack[--sp];
+        float4 a, b, c;
+        int4 d;
+        load_node(nodes, node, a, b, c, d);
+        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
+        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        // left child, then right child (_kernels.py:212-225)
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const float dc = side == 0 ? dl : dr;
+            const int32_t link = side == 0 ? d.x : d.y;
+            if (dc <= r2) {
+                if (link < 0) {
+                    if (MODE == kBuffer && cnt >= cap) {
+                        fail = LBVH_FLAG_BUFFER_OVERFLOW;
+                        goto done;
+                    }
+                    if (MODE != kCount) out[base + cnt] = link & 0x7FFFFFFF;
+                    ++cnt;
+                } else {
+                    if (sp >= kStack) {
+                        fail = LBVH_FLAG_STACK_EXHAUSTED;
+                        goto done;
+                    }
+                    stack[sp++] = link;
+                }
+            }
+        }
+    }
+done:
+    if (fail) atomicOr(status, fail);
+    if (MODE != kFill) counts[q] = cnt;
+}
+
+__global__ void __launch_bounds__(256)
+compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__restrict__ counts,
+               const int64_t *__restrict__ offsets, int64_t nq, int32_t *__restrict__ out) {
+    // One warp per query row: lanes copy the row's prefix.
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nq) return;
+    const int32_t cnt = __ldg(counts + warp);
+    const int64_t dst = __ldg(offsets + warp);
+    const int32_t *row = buf + warp * cap;
+    for (int j = lane; j < cnt; j += 32) out[dst + j] = __ldcs(row + j);
+}
+
+// Lexicographic (dist^2, ordinal) order, _kernels.py:293-296.
+__device__ __forceinline__ bool lex_less(float d1, int32_t i1, float d2, int32_t i2) {
+    return d1 < d2 || (d1 == d2 && i1 < i2);
+}
+
+template <int K>
+struct TopK {
+    float d[K];
+    int32_t id[K];
+
+    // Slots [0, K-kk) hold (-inf) sentinels that every real candidate ranks
+    // after, slots [K-kk, K) start empty (+inf, INT_MAX).  The current k-th
+    // best is always slot K-1, a compile-time index, so the whole list stays
+    // in registers.  An empty slot compares as +inf, so "full and nd > worst"
+    // (_kernels.py:367,383) is simply nd > d[K-1].
+    __device__ __forceinline__ void init(int kk) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const bool pad = j < K - kk;
+            d[j] = pad ? -INFINITY : INFINITY;
+            id[j] = pad ? (j - K) : INT32_MAX;
+        }
+    }
+    __device__ __forceinline__ float worst() const { return d[K - 1]; }
+
+    // Offer a candidate; kept iff it beats the current k-th best
+    // (_kernels.py:387-395).  Insertion keeps the list sorted.
+    __device__ __forceinline__ void offer(float cd, int32_t obj) {
+        if (!lex_less(cd, obj, d[K - 1], id[K - 1])) return;
+        bool placed = false;
+#pragma unroll
+        for (int j = K - 1; j > 0; --j) {
+            const bool shift = !placed && lex_less(cd, obj, d[j - 1], id[j - 1]);
+            const float nd = shift ? d[j - 1] : (placed ? d[j] : cd);
+            const int32_t ni = shift ? id[j - 1] : (placed ? id[j] : obj);
+            placed = placed || !shift;
+            d[j] = nd;
+            id[j] = ni;
+        }
+        if (!placed) {
+            d[0] = cd;
+            id[0] = obj;
+        }
+    }
+};
+
+template <int K>
+__global__ void __launch_bounds__(256)
+knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
+           const uint32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ offsets,
+           int32_t *__restrict__ out_idx, float *__restrict__ out_dist, uint32_t *status) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    const int64_t base = __ldg(offsets + q);
+    const int kk = (int)(__ldg(offsets + q + 1) - base);
+    if (kk <= 0) return;
+    const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
+                pz = __ldg(centers + 3 * q + 2);
+    if (t.n == 1) {
+        const float *bx = t.root_box;
+        out_dist[base] = __fsqrt_rn(
+            box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]));
+        out_idx[base] = __ldg(t.leaf_obj);
+        return;
+    }
+    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    TopK<K> top;
+    top.init(kk);
+    int32_t stack_node[kStack];
+    float stack_dist[kStack];
+    int sp = 1;
+    stack_node[0] = 0;
+    stack_dist[0] = 0.0f;  // never pruned: the list is empty at the first pop
+    uint32_t fail = 0;
+    while (sp > 0) {
+        --sp;
+        const int32_t node = stack_node[sp];
+        if (stack_dist[sp] > top.worst()) continue;
+        float4 a, b, c;
+        int4 dd;
+        load_node(nodes, node, a, b, c, dd);
+        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
+        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        // farther child first so the nearer one is on top (_kernels.py:373-379)
+        const bool left_near = dl <= dr;
+        const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
+        const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
+#pragma unroll
+        for (int pick = 0; pick < 2; ++pick) {
+            const int32_t link = pick == 0 ? fl : nl;
+            const float cd = pick == 0 ? fd : ndist;
+            if (cd > top.worst()) continue;
+            if (link < 0) {
+                top.offer(cd, link & 0x7FFFFFFF);
+            } else {
+                if (sp >= kStack) {
+                    fail = LBVH_FLAG_STACK_EXHAUSTED;
+                    goto done;
+                }
+                stack_node[sp] = link;
+                stack_dist[sp] = cd;
+                ++sp;
+            }
+        }
+    }
+done:
+    if (fail) atomicOr(status, fail);
+    // Spans are written even after a failure; the driver raises anyway.
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        if (j >= K - kk) {
+            const int64_t o = base + (j - (K - kk));
+            out_idx[o] = top.id[j];
+            out_dist[o] = __fsqrt_rn(top.d[j]);
+        }
+    }
+}
+
+// General k: the output span doubles as a bounded max-heap, exactly the
+// reference's scheme (_kernels.py:299-325, 385-414).
+__device__ __forceinline__ bool worse(float d1, int32_t i1, float d2, int32_t i2) {
+    return d1 > d2 || (d1 == d2 && i1 > i2);
+}
+
+__device__ void sift_down(float *hd, int32_t *hi, int64_t size, int64_t pos) {
+    while (true) {
+        int64_t child = 2 * pos + 1;
+        if (child >= size) break;
+        int64_t sib = child + 1;
+        if (sib < size && worse(hd[sib], hi[sib], hd[child], hi[child])) child = sib;
+        if (!worse(hd[child], hi[child], hd[pos], hi[pos])) break;
+        float td = hd[pos]; hd[pos] = hd[child]; hd[child] = td;
+        int32_t ti = hi[pos]; hi[pos] = hi[child]; hi[child] = ti;
+        pos = child;
+    }
+}
+
+__device__ void sift_up(float *hd, int32_t *hi, int64_t pos) {
+    while (pos > 0) {
+        int64_t up = (pos - 1) >> 1;
+        if (!worse(hd[pos], hi[pos], hd[up], hi[up])) break;
+        float td = hd[pos]; hd[pos] = hd[up]; hd[up] = td;
+        int32_t ti = hi[pos]; hi[pos] = hi[up]; hi[up] = ti;
+        pos = up;
+    }
+}
+
+__global__ void __launch_bounds__(128)
+knn_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                const uint32_t *__restrict__ order, int64_t nq,
+                const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
+                float *__restrict__ out_dist, uint32_t *status) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    const int64_t base = __ldg(offsets + q);
+    const int64_t kk = __ldg(offsets + q + 1) - base;
+    if (kk <= 0) return;
+    const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
+                pz = __ldg(centers + 3 * q + 2);
+    float *hd = out_dist + base;
+    int32_t *hi = out_idx + base;
+    if (t.n == 1) {
+        const float *bx = t.root_box;
+        hd[0] = __fsqrt_rn(box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]));
+        hi[0] = __ldg(t.leaf_obj);
+        return;
+    }
+    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    int32_t stack_node[kStack];
+    float stack_dist[kStack];
+    int sp = 1;
+    stack_node[0] = 0;
+    stack_dist[0] = 0.0f;
+    int64_t size = 0;
+    uint32_t fail = 0;
+    while (sp > 0) {
+        --sp;
+        const int32_t node = stack_node[sp];
+        if (size == kk && stack_dist[sp] > hd[0]) continue;
+        float4 a, b, c;
+        int4 dd;
+        load_node(nodes, node, a, b, c, dd);
+        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
+        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        const bool left_near = dl <= dr;
+        const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
+        const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
+        for (int pick = 0; pick < 2; ++pick) {
+            const int32_t link = pick == 0 ? fl : nl;
+            const float cd = pick == 0 ? fd : ndist;
+            if (size == kk && cd > hd[0]) continue;
+            if (link < 0) {
+                const int32_t obj = link & 0x7FFFFFFF;
+                if (size < kk) {
+                    hd[size] = cd;
+                    hi[size] = obj;
+                    ++size;
+                    sift_up(hd, hi, size - 1);
+                } else if (worse(hd[0], hi[0], cd, obj)) {
+                    hd[0] = cd;
+                    hi[0] = obj;
+                    sift_down(hd, hi, kk, 0);
+                }
+            } else {
+                if (sp >= kStack) {
+                    fail = LBVH_FLAG_STACK_EXHAUSTED;
+                    goto done;
+                }
+                stack_node[sp] = link;
+                stack_dist[sp] = cd;
+                ++sp;
+            }
+        }
+    }
+done:
+    if (fail) atomicOr(status, fail);
+    for (int64_t hs = size; hs > 1;) {
+        --hs;
+        float td = hd[0]; hd[0] = hd[hs]; hd[hs] = td;
+        int32_t ti = hi[0]; hi[0] = hi[hs]; hi[hs] = ti;
+        sift_down(hd, hi, hs, 0);
+    }
+    for (int64_t j = 0; j < size; ++j) hd[j] = __fsqrt_rn(hd[j]);
+}
+
+__global__ void __launch_bounds__(256)
+check_queries_kernel(const float *__restrict__ centers, int64_t nq,
+                     const float *__restrict__ radii, uint32_t *status) {
+    uint32_t bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * nq;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(__ldcs(centers + i))) bad |= LBVH_FLAG_NONFINITE;
+    if (radii)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            float r = __ldcs(radii + i);
+            if (!isfinite(r) || r < 0.0f) bad |= LBVH_FLAG_BAD_RADIUS;
+        }
+    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicOr(status, bad);
+}
+
+bool tree_ok(const lbvh_tree *t) {
+    return t && t->n >= 1 && t->leaf_obj && t->root_box && (t->n == 1 || t->nodes);
+}
+
+template <int MODE>
+int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii, float radius,
+                   const uint32_t *order, int64_t nq, int32_t *counts, const int64_t *offsets,
+                   int32_t *out, int64_t cap, uint32_t *status, cudaStream_t stream) {
+    if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0) return LBVH_OK;
+    if (!centers) return LBVH_ERR_INVALID_ARG;
+    if (MODE != kFill && !counts) return LBVH_ERR_INVALID_ARG;
+    if (MODE == kFill && !offsets) return LBVH_ERR_INVALID_ARG;
+    if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    spatial_kernel<MODE><<<div_up(nq, 256), 256, 0, stream>>>(
+        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, status);
+    return check_launch();
+}
+
+}  // namespace
+
+int spatial_count(const lbvh_tree *t, const float *centers, const float *radii, float radius,
+                  const uint32_t *order, int64_t nq, int32_t *counts, uint32_t *status,
+                  cudaStream_t stream) {
+    return launch_spatial<kCount>(t, centers, radii, radius, order, nq, counts, nullptr,
+                                  nullptr, 0, status, stream);
+}
+
+int spatial_fill(const lbvh_tree *t, const float *centers, const float *radii, float radius,
+                 const uint32_t *order, int64_t nq, const int64_t *offsets, int32_t *out,
+                 uint32_t *status, cudaStream_t stream) {
+    return launch_spatial<kFill>(t, centers, radii, radius, order, nq, nullptr, offsets, out, 0,
+                                 status, stream);
+}
+
+int spatial_1p(const lbvh_tree *t, const float *centers, const float *radii, float radius,
+               const uint32_t *order, int64_t nq, int32_t *buf, int64_t cap, int32_t *counts,
+               uint32_t *status, cudaStream_t stream) {
+    if (cap < 1 || (nq > 0 && !buf)) return LBVH_ERR_INVALID_ARG;
+    return launch_spatial<kBuffer>(t, centers, radii, radius, order, nq, counts, nullptr, buf,
+                                   cap, status, stream);
+}
+
+int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_t *offsets,
+            int64_t nq, int32_t *out, cudaStream_t stream) {
+    if (nq < 0 || cap < 1) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0) return LBVH_OK;
+    if (!buf || !counts || !offsets) return LBVH_ERR_INVALID_ARG;
+    compact_kernel<<<div_up(nq * 32, 256), 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
+    return check_launch();
+}
+
+int knn(const lbvh_tree *t, const float *centers, const uint32_t *order, int64_t nq,
+        const int64_t *offsets, int64_t max_span, int32_t *out_idx, float *out_dist,
+        uint32_t *status, cudaStream_t stream) {
+    if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0 || max_span <= 0) return LBVH_OK;
+    if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
+    if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    const unsigned g = div_up(nq, 256);
+#define LBVH_KNN_CASE(KV)                                                                   \
+    if (max_span <= KV) {                                                                   \
+        knn_kernel<KV><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets, out_idx,     \
+                                              out_dist, status);                            \
+        return check_launch();                                                              \
+    }
+    LBVH_KNN_CASE(4)
+    LBVH_KNN_CASE(8)
+    LBVH_KNN_CASE(10)
+    LBVH_KNN_CASE(16)
+    LBVH_KNN_CASE(32)
+#undef LBVH_KNN_CASE
+    knn_heap_kernel<<<div_up(nq, 128), 128, 0, stream>>>(*t, centers, order, nq, offsets,
+                                                         out_idx, out_dist, status);
+    return check_launch();
+}
+
+int check_queries(const float *centers, int64_t nq, const float *radii, uint32_t *status,
+                  cudaStream_t stream) {
+    if (nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0) return LBVH_OK;
+    if (!centers) return LBVH_ERR_INVALID_ARG;
+    unsigned g = div_up(3 * nq, 256);
+    g = g < kNumSMs * 8 ? g : kNumSMs * 8;
+    check_queries_kernel<<<g, 256, 0, stream>>>(centers, nq, radii, status);
+    return check_launch();
+}
+
+}  // namespace lbvh

@@ -1,0 +1,452 @@
+"""Batched radius and k-nearest queries on the GPU -- drop-in for reference traversal.py.
+
+Every batch runs as a short sequence of kernels on the current stream
+(csrc/traverse.cu, csrc/scan.cu, csrc/build.cu):
+
+  query_spatial_2p   check -> Morton order -> count -> scan -> [sync: total]
+                     -> fill                                  (traversal.py:184-211)
+  query_spatial_1p   check -> order -> buffered pass -> scan -> [sync]
+                     -> compact, or the 2P path on overflow   (traversal.py:214-248)
+  query_knn          check -> spans/scan -> order -> kNN      (traversal.py:251-272)
+
+Results are CRS like the reference's: ``offsets`` int64 (nq+1), ``indices``
+int32, ``distances`` float32 for kNN.  Host (numpy) inputs give a host
+ResultSet backed by pinned memory; CUDA-tensor inputs give a ResultSet of
+CUDA tensors (no D2H), the device-resident entry used by the benchmark.
+Errors carry the reference's exception types and messages.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+from .geometry import Box, Point
+from .tree import Bvh
+from .validation import check_neighbor_counts, check_points, check_radii
+
+__all__ = ["SpatialQuery", "KnnQuery", "ResultSet", "STACK_CAPACITY", "traverse_spatial_one",
+           "traverse_knn_one", "query_spatial_2p", "query_spatial_1p", "query_knn",
+           "query_sort_order"]
+
+STACK_CAPACITY = _lib.STACK_CAPACITY
+
+
+@dataclass(frozen=True)
+class SpatialQuery:
+    """All objects within ``radius`` of ``center``, inclusive (traversal.py:46-55)."""
+
+    center: Point
+    radius: float
+
+    def __post_init__(self):
+        if not math.isfinite(self.radius) or self.radius < 0:
+            raise ValueError(f"radius must be finite and non-negative, got {self.radius}")
+
+
+@dataclass(frozen=True)
+class KnnQuery:
+    """The ``k`` objects nearest to ``center`` (traversal.py:58-67)."""
+
+    center: Point
+    k: int
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError(f"k must be >= 1, got {self.k}")
+
+
+class ResultSet:
+    """CSR batch output (traversal.py:70-106).
+
+    ``offsets`` (nq+1) non-decreasing from 0, hits of query q at
+    ``indices[offsets[q]:offsets[q+1]]``; ``distances`` only for kNN.  The
+    arrays are numpy for host queries or CUDA tensors for device queries.
+    """
+
+    __slots__ = ("offsets", "indices", "distances")
+
+    def __init__(self, offsets, indices, distances=None):
+        offsets = np.asarray(offsets) if not isinstance(offsets, torch.Tensor) else offsets
+        if offsets.ndim != 1 or offsets.shape[0] < 1 or offsets[0] != 0:
+            raise ValueError("offsets must be 1-D and start at 0")
+        diff = offsets[1:] - offsets[:-1]
+        if (diff < 0).any():
+            raise ValueError("offsets must be non-decreasing")
+        if int(offsets[-1]) != indices.shape[0]:
+            raise ValueError("offsets total must equal indices length")
+        if distances is not None and tuple(distances.shape) != tuple(indices.shape):
+            raise ValueError("distances must align with indices")
+        self.offsets, self.indices, self.distances = offsets, indices, distances
+
+    @classmethod
+    def _trusted(cls, offsets, indices, distances=None) -> "ResultSet":
+        # CRS built by the device scan is well-formed by construction.
+        rs = object.__new__(cls)
+        rs.offsets, rs.indices, rs.distances = offsets, indices, distances
+        return rs
+
+    @property
+    def query_count(self) -> int:
+        return self.offsets.shape[0] - 1
+
+    @property
+    def on_device(self) -> bool:
+        return isinstance(self.indices, torch.Tensor)
+
+    def counts(self):
+        return self.offsets[1:] - self.offsets[:-1]
+
+    def hits(self, q: int):
+        return self.indices[int(self.offsets[q]):int(self.offsets[q + 1])]
+
+    def hit_distances(self, q: int):
+        if self.distances is None:
+            raise ValueError("result set carries no distances")
+        return self.distances[int(self.offsets[q]):int(self.offsets[q + 1])]
+
+    def to_host(self) -> "ResultSet":
+        if not self.on_device:
+            return self
+        o, i, d = dv.d2h_many(self.offsets, self.indices, self.distances)
+        return ResultSet._trusted(o, i, d)
+
+    def __repr__(self) -> str:
+        kind = "knn" if self.distances is not None else "spatial"
+        where = "cuda" if self.on_device else "host"
+        return f"ResultSet({kind}, queries={self.query_count}, hits={self.indices.shape[0]}, {where})"
+
+
+# ---------------------------------------------------------------------------
+# Input normalisation (traversal.py:114-143)
+# ---------------------------------------------------------------------------
+
+
+class _Batch:
+    """Query batch staged on the device."""
+
+    __slots__ = ("centers", "radii", "radius", "ks", "k", "nq", "host")
+
+    def __init__(self):
+        self.radii = self.ks = None
+        self.radius = 0.0
+        self.k = 0
+
+
+def _device_centers(c) -> torch.Tensor:
+    t = c.to(torch.float32)
+    if t.ndim == 1 and t.shape[0] == 3:
+        t = t.reshape(1, 3)
+    if t.ndim != 2 or t.shape[1] != 3:
+        raise ValueError(f"query centers must have shape (n, 3), got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def _spatial_batch(queries) -> _Batch:
+    b = _Batch()
+    if isinstance(queries, tuple) and len(queries) == 2:
+        c, r = queries
+        if dv.is_cuda_tensor(c):
+            b.host = False
+            b.centers = _device_centers(c)
+            b.nq = int(b.centers.shape[0])
+            if dv.is_cuda_tensor(r):
+                b.radii = r.to(torch.float32).reshape(-1).contiguous()
+                if b.radii.shape[0] != b.nq:
+                    raise ValueError(f"radius must be a scalar or shape ({b.nq},), "
+                                     f"got {tuple(r.shape)}")
+            else:
+                ra = check_radii(r, b.nq, device_checks=True)
+                if ra.ndim == 0:
+                    b.radius = float(ra)
+                else:
+                    b.radii = dv.h2d(ra)
+            return b
+        centers = check_points(c, "query centers", device_checks=True)
+        ra = check_radii(r, centers.shape[0], device_checks=True)
+    else:
+        qs = list(queries)
+        if not all(isinstance(q, SpatialQuery) for q in qs):
+            raise TypeError("expected SpatialQuery items or a (centers, radii) pair")
+        centers = np.array([[q.center.x, q.center.y, q.center.z] for q in qs],
+                           dtype=np.float32).reshape(-1, 3)
+        ra = np.array([q.radius for q in qs], dtype=np.float32)
+    b.host = True
+    b.nq = int(centers.shape[0])
+    if b.nq:
+        b.centers = dv.h2d(centers)
+        if ra.ndim == 0:
+            b.radius = float(ra)
+        else:
+            b.radii = dv.h2d(ra)
+    return b
+
+
+def _knn_batch(queries) -> _Batch:
+    b = _Batch()
+    if isinstance(queries, tuple) and len(queries) == 2:
+        c, k = queries
+        if dv.is_cuda_tensor(c):
+            b.host = False
+            b.centers = _device_centers(c)
+            b.nq = int(b.centers.shape[0])
+            if dv.is_cuda_tensor(k):
+                b.ks = k.to(torch.int64).reshape(-1).contiguous()
+                if b.ks.shape[0] != b.nq:
+                    raise ValueError(f"k must be a scalar or shape ({b.nq},), got {tuple(k.shape)}")
+            else:
+                ka = check_neighbor_counts(k, b.nq, device_checks=True)
+                if ka.ndim == 0:
+                    b.k = int(ka)
+                else:
+                    b.ks = dv.h2d(ka)
+            return b
+        centers = check_points(c, "query centers", device_checks=True)
+        ka = check_neighbor_counts(k, centers.shape[0], device_checks=True)
+    else:
+        qs = list(queries)
+        if not all(isinstance(q, KnnQuery) for q in qs):
+            raise TypeError("expected KnnQuery items or a (centers, k) pair")
+        centers = np.array([[q.center.x, q.center.y, q.center.z] for q in qs],
+                           dtype=np.float32).reshape(-1, 3)
+        ka = np.array([q.k for q in qs], dtype=np.int64)
+    b.host = True
+    b.nq = int(centers.shape[0])
+    if b.nq:
+        b.centers = dv.h2d(centers)
+        if ka.ndim == 0:
+            b.k = int(ka)
+        else:
+            b.ks = dv.h2d(ka)
+    return b
+
+
+def _raise_flags(flags: int) -> None:
+    """Reference exception for a device status word (validation first)."""
+    if flags & _lib.FLAG_NONFINITE:
+        raise ValueError("query centers must contain only finite values")
+    if flags & _lib.FLAG_BAD_RADIUS:
+        raise ValueError("radius must be finite and non-negative")
+    if flags & _lib.FLAG_BAD_K:
+        raise ValueError("k must be >= 1")
+    if flags & _lib.FLAG_STACK_EXHAUSTED:
+        raise RuntimeError("traversal stack exhausted")
+
+
+def _empty_result(host: bool, knn: bool) -> ResultSet:
+    if host:
+        return ResultSet._trusted(np.zeros(1, dtype=np.int64), np.empty(0, dtype=np.int32),
+                                  np.empty(0, dtype=np.float32) if knn else None)
+    dev = dv.device()
+    return ResultSet._trusted(torch.zeros(1, dtype=torch.int64, device=dev),
+                              torch.empty(0, dtype=torch.int32, device=dev),
+                              torch.empty(0, dtype=torch.float32, device=dev) if knn else None)
+
+
+def _order(tree: Bvh, b: _Batch, sort_queries: bool):
+    """Device Morton order of the batch on the tree's scene grid (or None)."""
+    if not sort_queries or b.nq <= 1:
+        return None
+    l = _lib.lib()
+    order = dv.empty(b.nq, torch.int32)
+    ws = dv.workspace(l.lbvh_query_workspace_bytes(b.nq))
+    _lib.check(l.lbvh_query_order(dv.ptr(b.centers), b.nq,
+                                  dv.ptr(tree.device_arrays()["root_box"]), dv.ptr(order),
+                                  dv.ptr(ws), ws.numel(), dv.stream()))
+    return order
+
+
+def _finish(host: bool, status: dv.Status, *arrays):
+    """Read status (+ results when host) in one sync; raise on flags."""
+    if host:
+        res = dv.d2h_many(status.dev, *arrays)
+        _raise_flags(int(res[0][0]) & 0xFFFFFFFF)
+        return res[1:]
+    _raise_flags(status.read())
+    return list(arrays)
+
+
+# ---------------------------------------------------------------------------
+# Batched queries
+# ---------------------------------------------------------------------------
+
+
+def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
+    l = _lib.lib()
+    ct = tree.ctree()
+    st = dv.stream()
+    nq = b.nq
+    counts = dv.empty(nq, torch.int32)
+    _lib.check(l.lbvh_spatial_count(ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
+                                    dv.ptr(order), nq, dv.ptr(counts), status.ptr, st))
+    offsets = dv.empty(nq + 1, torch.int64)
+    ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
+    _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
+                                     ws.numel(), st))
+    flags, total = dv.d2h_many(status.dev, offsets[nq:])
+    _raise_flags(int(flags[0]) & 0xFFFFFFFF)
+    total = int(total[0])
+    out = dv.empty(total, torch.int32)
+    if total:
+        _lib.check(l.lbvh_spatial_fill(ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
+                                       dv.ptr(order), nq, dv.ptr(offsets), dv.ptr(out),
+                                       status.ptr, st))
+    return offsets, out
+
+
+def _check_batch(b: _Batch, status: dv.Status, radii: bool) -> None:
+    l = _lib.lib()
+    _lib.check(l.lbvh_check_queries(dv.ptr(b.centers), b.nq, dv.ptr(b.radii) if radii else None,
+                                    status.ptr, dv.stream()))
+
+
+def query_spatial_2p(tree: Bvh, queries, sort_queries: bool = True,
+                     threads: int = 1) -> ResultSet:
+    """Within-radius batch, count-then-fill (traversal.py:184-211)."""
+    b = _spatial_batch(queries)
+    if b.nq == 0:
+        return _empty_result(b.host, knn=False)
+    status = dv.Status()
+    _check_batch(b, status, radii=True)
+    order = _order(tree, b, sort_queries)
+    offsets, out = _spatial_2p_device(tree, b, order, status)
+    offsets, out = _finish(b.host, status, offsets, out)
+    return ResultSet._trusted(offsets, out)
+
+
+def query_spatial_1p(tree: Bvh, queries, buffer_size: int, sort_queries: bool = True,
+                     threads: int = 1) -> tuple[ResultSet, bool]:
+    """Within-radius batch with ``buffer_size`` slots per query; falls back to
+    the two-pass path for the whole batch if any query overflows
+    (traversal.py:214-248).  Returns ``(result, fell_back)``."""
+    buffer_size = int(buffer_size)
+    if buffer_size < 1:
+        raise ValueError(f"buffer_size must be >= 1, got {buffer_size}")
+    b = _spatial_batch(queries)
+    if b.nq == 0:
+        return _empty_result(b.host, knn=False), False
+    l = _lib.lib()
+    st = dv.stream()
+    nq = b.nq
+    status = dv.Status()
+    _check_batch(b, status, radii=True)
+    order = _order(tree, b, sort_queries)
+    ct = tree.ctree()
+    buf = dv.empty((nq, buffer_size), torch.int32)
+    counts = dv.empty(nq, torch.int32)
+    _lib.check(l.lbvh_spatial_1p(ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
+                                 dv.ptr(order), nq, dv.ptr(buf), buffer_size, dv.ptr(counts),
+                                 status.ptr, st))
+    offsets = dv.empty(nq + 1, torch.int64)
+    ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
+    _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
+                                     ws.numel(), st))
+    flags, total = dv.d2h_many(status.dev, offsets[nq:])
+    flags = int(flags[0]) & 0xFFFFFFFF
+    _raise_flags(flags)
+    if flags & _lib.FLAG_BUFFER_OVERFLOW:
+        del buf
+        status = dv.Status()
+        offsets, out = _spatial_2p_device(tree, b, order, status)
+        offsets, out = _finish(b.host, status, offsets, out)
+        return ResultSet._trusted(offsets, out), True
+    total = int(total[0])
+    out = dv.empty(total, torch.int32)
+    if total:
+        _lib.check(l.lbvh_compact(dv.ptr(buf), buffer_size, dv.ptr(counts), dv.ptr(offsets), nq,
+                                  dv.ptr(out), st))
+    offsets, out = _finish(b.host, status, offsets, out)
+    return ResultSet._trusted(offsets, out), False
+
+
+def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -> ResultSet:
+    """k-nearest batch (traversal.py:251-272): spans of min(k, n) sorted by
+    (distance, ordinal) with true distances."""
+    b = _knn_batch(queries)
+    if b.nq == 0:
+        return _empty_result(b.host, knn=True)
+    l = _lib.lib()
+    st = dv.stream()
+    nq, n = b.nq, tree.leaf_count
+    status = dv.Status()
+    _check_batch(b, status, radii=False)
+    offsets = dv.empty(nq + 1, torch.int64)
+    ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
+    if b.ks is None:
+        # uniform k: spans, total and the kernel variant are known on the host
+        span = min(b.k, n)
+        max_span, total = span, span * nq
+        _lib.check(l.lbvh_knn_offsets(None, b.k, n, nq, dv.ptr(offsets), None, status.ptr,
+                                      dv.ptr(ws), ws.numel(), st))
+    else:
+        mx = dv.empty(1, torch.int32)
+        _lib.check(l.lbvh_knn_offsets(dv.ptr(b.ks), 0, n, nq, dv.ptr(offsets), dv.ptr(mx),
+                                      status.ptr, dv.ptr(ws), ws.numel(), st))
+        flags, mxh, tot = dv.d2h_many(status.dev, mx, offsets[nq:])
+        _raise_flags(int(flags[0]) & 0xFFFFFFFF)
+        max_span, total = int(mxh[0]), int(tot[0])
+    order = _order(tree, b, sort_queries)
+    out_idx = dv.empty(total, torch.int32)
+    out_dist = dv.empty(total, torch.float32)
+    _lib.check(l.lbvh_knn(tree.ctree(), dv.ptr(b.centers), dv.ptr(order), nq, dv.ptr(offsets),
+                          max_span, dv.ptr(out_idx), dv.ptr(out_dist), status.ptr, st))
+    offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
+    return ResultSet._trusted(offsets, out_idx, out_dist)
+
+
+def query_sort_order(centers, scene: Box | tuple) -> np.ndarray:
+    """Morton permutation of query centers with ordinal tie-break
+    (traversal.py:146-159), computed on the GPU (f64 codes + radix sort)."""
+    centers = check_points(centers, "query centers")
+    if isinstance(scene, Box):
+        smin = np.array([scene.min.x, scene.min.y, scene.min.z], dtype=np.float32)
+        smax = np.array([scene.max.x, scene.max.y, scene.max.z], dtype=np.float32)
+    else:
+        smin, smax = scene
+    lo = np.ascontiguousarray(smin, dtype=np.float64).reshape(3)
+    hi = np.ascontiguousarray(smax, dtype=np.float64).reshape(3)
+    nq = centers.shape[0]
+    if nq == 0:
+        return np.empty(0, dtype=np.int64)
+    l = _lib.lib()
+    st = dv.stream()
+    pts = dv.h2d(centers.astype(np.float64))
+    codes = dv.empty(nq, torch.int32)
+    _lib.check(l.lbvh_morton_codes(dv.ptr(pts), nq, lo.ctypes.data, hi.ctypes.data,
+                                   dv.ptr(codes), st))
+    perm = torch.arange(nq, dtype=torch.int32, device=dv.device())
+    ws = dv.workspace(l.lbvh_sort_workspace_bytes(nq))
+    _lib.check(l.lbvh_sort_pairs(dv.ptr(codes), dv.ptr(perm), nq, 30, dv.ptr(ws), ws.numel(),
+                                 st))
+    return dv.d2h(perm).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# Single-query entry points (traversal.py:295-378): one-query GPU batches
+# ---------------------------------------------------------------------------
+
+
+def traverse_spatial_one(tree: Bvh, query: SpatialQuery,
+                         sink: Callable[[int], None] | None = None) -> int:
+    """One within-radius query; feeds each hit ordinal to ``sink`` (in the
+    reference's traversal order) and returns the hit count."""
+    rs = query_spatial_2p(tree, [query], sort_queries=False)
+    hits = rs.hits(0)
+    if sink is not None:
+        for h in hits.tolist():
+            sink(int(h))
+    return int(hits.shape[0])
+
+
+def traverse_knn_one(tree: Bvh, query: KnnQuery) -> list[tuple[int, float]]:
+    """One k-nearest query: min(k, n) (ordinal, distance) pairs sorted by
+    (distance, ordinal)."""
+    rs = query_knn(tree, [query], sort_queries=False)
+    return [(int(i), float(d)) for i, d in zip(rs.hits(0).tolist(),
+                                               rs.hit_distances(0).tolist())]

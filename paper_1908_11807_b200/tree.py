@@ -1,0 +1,334 @@
+"""Linear BVH construction on the GPU -- drop-in for reference tree.py.
+
+``build`` runs the whole pipeline on the device in one stream (scene
+reduction, f64 Morton codes, one-sweep radix sort, fused Apetrei
+hierarchy + atomic-flag refit + packed-node write; csrc/build.cu) and returns
+a :class:`Bvh` whose arrays stay resident in HBM.  The reference-layout numpy
+fields (``node_mins`` ... ``scene_max``) are materialised lazily, read-only,
+on first access.
+
+Node numbering is the reference's (tree.py:8-12): internal nodes 0..n-2 with
+root 0, the leaf at Morton-sorted position p is node (n-1)+p.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+from .geometry import Box
+from .validation import check_boxes
+
+__all__ = ["Bvh", "Topology", "build", "common_prefix", "find_split", "node_range",
+           "generate_topology", "refit_bounds"]
+
+
+def _readonly(a: np.ndarray) -> np.ndarray:
+    a.setflags(write=False)
+    return a
+
+
+class Bvh:
+    """Immutable linear BVH (reference tree.py:122-174).
+
+    Constructed either by :func:`build` (device-resident) or directly from
+    reference-layout numpy arrays ``Bvh(node_mins, node_maxs, left, right,
+    leaf_obj, scene_min, scene_max)`` -- e.g. a hand-made or modified tree --
+    in which case the arrays are uploaded and packed on first query.
+    """
+
+    __slots__ = ("_host", "_dev", "_n")
+
+    _FIELDS = ("node_mins", "node_maxs", "left", "right", "leaf_obj", "scene_min", "scene_max")
+
+    def __init__(self, node_mins, node_maxs, left, right, leaf_obj, scene_min, scene_max):
+        host = {
+            "node_mins": np.asarray(node_mins, dtype=np.float32),
+            "node_maxs": np.asarray(node_maxs, dtype=np.float32),
+            "left": np.asarray(left, dtype=np.int32),
+            "right": np.asarray(right, dtype=np.int32),
+            "leaf_obj": np.asarray(leaf_obj, dtype=np.int32),
+            "scene_min": np.asarray(scene_min, dtype=np.float32),
+            "scene_max": np.asarray(scene_max, dtype=np.float32),
+        }
+        object.__setattr__(self, "_host", host)
+        object.__setattr__(self, "_dev", None)
+        object.__setattr__(self, "_n", int(host["leaf_obj"].shape[0]))
+
+    @classmethod
+    def _from_device(cls, dev: dict, n: int) -> "Bvh":
+        self = object.__new__(cls)
+        object.__setattr__(self, "_host", {})
+        object.__setattr__(self, "_dev", dev)
+        object.__setattr__(self, "_n", n)
+        return self
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Bvh is immutable")
+
+    # -- reference-layout host views (lazy D2H) ---------------------------
+    def _field(self, name: str) -> np.ndarray:
+        h = self._host
+        if name not in h:
+            d = self._dev
+            if name in ("scene_min", "scene_max"):
+                box = dv.d2h(d["root_box"])
+                h["scene_min"] = _readonly(box[:3].copy())
+                h["scene_max"] = _readonly(box[3:].copy())
+            else:
+                h[name] = _readonly(dv.d2h(d[name]))
+        return h[name]
+
+    node_mins = property(lambda self: self._field("node_mins"))
+    node_maxs = property(lambda self: self._field("node_maxs"))
+    left = property(lambda self: self._field("left"))
+    right = property(lambda self: self._field("right"))
+    leaf_obj = property(lambda self: self._field("leaf_obj"))
+    scene_min = property(lambda self: self._field("scene_min"))
+    scene_max = property(lambda self: self._field("scene_max"))
+
+    # -- device view -------------------------------------------------------
+    def device_arrays(self) -> dict:
+        """Device tensors: node_mins, node_maxs, left, right, leaf_obj,
+        nodes (packed (n-1) x 64 B), root_box (6 f32).  Uploads and packs a
+        host-constructed tree on first use."""
+        if self._dev is None:
+            self._upload()
+        return self._dev
+
+    def _upload(self) -> None:
+        h = self._host
+        n = self._n
+        if n < 1:
+            raise ValueError("empty scene")
+        l = _lib.lib()
+        d = {k: dv.h2d(np.ascontiguousarray(h[k])) for k in
+             ("node_mins", "node_maxs", "left", "right", "leaf_obj")}
+        d["nodes"] = dv.empty(max(n - 1, 1) * _lib.NODE_BYTES, torch.uint8)
+        d["root_box"] = dv.empty(6, torch.float32)
+        status = dv.Status()
+        ct = _ctree(d, n)
+        _lib.check(l.lbvh_pack(ct, dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), status.ptr,
+                               dv.stream()))
+        if status.read() & _lib.FLAG_BAD_TREE:
+            raise ValueError("tree links or leaf ordinals out of range")
+        object.__setattr__(self, "_dev", d)
+
+    def ctree(self) -> _lib.CTree:
+        return _ctree(self.device_arrays(), self._n)
+
+    # -- reference API -----------------------------------------------------
+    @property
+    def leaf_count(self) -> int:
+        return self._n
+
+    @property
+    def internal_count(self) -> int:
+        return self._n - 1
+
+    @property
+    def node_count(self) -> int:
+        return 2 * self._n - 1
+
+    @property
+    def scene(self) -> Box:
+        return Box.from_arrays(self.scene_min, self.scene_max)
+
+    def is_leaf(self, node: int) -> bool:
+        return node >= self.internal_count
+
+    def leaf_ordinal(self, node: int) -> int:
+        if not self.is_leaf(node):
+            raise ValueError(f"node {node} is internal")
+        return int(self.leaf_obj[node - self.internal_count])
+
+    def children(self, node: int) -> tuple[int, int]:
+        if self.is_leaf(node):
+            raise ValueError(f"node {node} is a leaf")
+        return int(self.left[node]), int(self.right[node])
+
+    def node_box(self, node: int) -> Box:
+        return Box.from_arrays(self.node_mins[node], self.node_maxs[node])
+
+    def __repr__(self) -> str:
+        return f"Bvh(leaves={self.leaf_count}, nodes={self.node_count})"
+
+
+def _ctree(d: dict, n: int) -> _lib.CTree:
+    return _lib.CTree(n, dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]),
+                      dv.ptr(d.get("left")), dv.ptr(d.get("right")), dv.ptr(d["leaf_obj"]),
+                      dv.ptr(d["nodes"]), dv.ptr(d["root_box"]))
+
+
+def _device_boxes(boxes):
+    """CUDA tensor input: (n,3) points or (n,6) rows -> (mins, maxs) views."""
+    t = boxes.to(torch.float32)
+    if t.ndim != 2 or t.shape[1] not in (3, 6):
+        raise ValueError(f"X must have shape (n, 3) or (n, 6), got {tuple(t.shape)}")
+    if t.shape[1] == 3:
+        t = t.contiguous()
+        return t, t
+    return t[:, :3].contiguous(), t[:, 3:].contiguous()
+
+
+def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> Bvh:
+    """Build from device-resident (n, 3) f32 ``mins``/``maxs`` (``maxs`` may
+    be ``mins`` for point input).  The device-resident entry of :func:`build`."""
+    n = int(mins.shape[0])
+    if n == 0:
+        raise ValueError("empty scene")
+    if n > _lib.MAX_ITEMS:
+        raise ValueError(f"at most {_lib.MAX_ITEMS} primitives per tree")
+    l = _lib.lib()
+    f32, i32 = torch.float32, torch.int32
+    d = {
+        "node_mins": dv.empty((2 * n - 1, 3), f32),
+        "node_maxs": dv.empty((2 * n - 1, 3), f32),
+        "left": dv.empty(max(n - 1, 0), i32),
+        "right": dv.empty(max(n - 1, 0), i32),
+        "leaf_obj": dv.empty(n, i32),
+        "root_box": dv.empty(6, f32),
+        "nodes": dv.empty(max(n - 1, 1) * _lib.NODE_BYTES, torch.uint8),
+    }
+    ws = dv.workspace(l.lbvh_build_workspace_bytes(n))
+    status = dv.Status()
+    _lib.check(l.lbvh_build(dv.ptr(mins), dv.ptr(maxs), n, dv.ptr(ws), ws.numel(),
+                            dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]), dv.ptr(d["left"]),
+                            dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
+                            dv.ptr(d["nodes"]), None, status.ptr, dv.stream()))
+    if check:
+        flags = status.read()
+        if flags & _lib.FLAG_NONFINITE:
+            raise ValueError("X must contain only finite values")
+        if flags & _lib.FLAG_INVERTED_BOX:
+            raise ValueError("X contains boxes with min corner above max corner")
+    return Bvh._from_device(d, n)
+
+
+def build(boxes, threads: int = 1) -> Bvh:
+    """Build a linear BVH over a non-empty collection of boxes (tree.py:177-209).
+
+    Accepts (n, 3) points, (n, 6) corner rows, a ``(mins, maxs)`` pair,
+    Box/Point sequences -- or a CUDA tensor of shape (n, 3)/(n, 6), which
+    skips the host round trip.  ``threads`` is accepted and ignored.
+    Deterministic: identical input gives bit-identical arrays.
+    """
+    if dv.is_cuda_tensor(boxes):
+        mins, maxs = _device_boxes(boxes)
+        return build_device(mins, maxs)
+    # Large ndarray inputs are value-checked on the device; pairs and
+    # sequences on the host (exact reference messages either way).
+    device_checks = isinstance(boxes, np.ndarray)
+    mins, maxs = check_boxes(boxes, device_checks=device_checks)
+    if mins.shape[0] == 0:
+        raise ValueError("empty scene")
+    dmins = dv.h2d(mins)
+    dmaxs = dmins if maxs is mins else dv.h2d(maxs)
+    return build_device(dmins, dmaxs)
+
+
+# ---------------------------------------------------------------------------
+# Topology helpers (reference tree.py:40-119)
+# ---------------------------------------------------------------------------
+
+
+def common_prefix(codes, i: int, j: int) -> int:
+    """Common-prefix length of augmented keys i and j (-1 if j out of range).
+
+    Scalar diagnostic helper (tree.py:47-58); the device kernels compute the
+    same quantity with ``__clz`` on the fly.
+    """
+    codes = np.asarray(codes, dtype=np.int64)
+    n = codes.shape[0]
+    if j < 0 or j >= n:
+        return -1
+    x = (int(codes[i]) << 32 | i) ^ (int(codes[j]) << 32 | j)
+    return 64 - x.bit_length()
+
+
+def find_split(codes, first: int, last: int) -> int:
+    """Karras split of [first, last] (tree.py:61-65); scalar helper."""
+    n = len(codes)
+    if not 0 <= first < last < n:
+        raise ValueError(f"need 0 <= first < last < {n}, got ({first}, {last})")
+    common = common_prefix(codes, first, last)
+    split, step = first, last - first
+    while True:
+        step = (step + 1) >> 1
+        cand = split + step
+        if cand < last and common_prefix(codes, first, cand) > common:
+            split = cand
+        if step <= 1:
+            return split
+
+
+def node_range(codes, i: int) -> tuple[int, int]:
+    """Leaf range of internal node i (tree.py:68-74); scalar helper."""
+    n = len(codes)
+    if not 0 <= i < n - 1:
+        raise ValueError(f"internal ordinal must be in [0, {n - 1}), got {i}")
+    d = 1 if common_prefix(codes, i, i + 1) > common_prefix(codes, i, i - 1) else -1
+    floor = common_prefix(codes, i, i - d)
+    hi = 2
+    while common_prefix(codes, i, i + hi * d) > floor:
+        hi <<= 1
+    span, t = 0, hi >> 1
+    while t >= 1:
+        if common_prefix(codes, i, i + (span + t) * d) > floor:
+            span += t
+        t >>= 1
+    j = i + span * d
+    return (i, j) if i < j else (j, i)
+
+
+class Topology(NamedTuple):
+    """Child links of the n-1 internal nodes plus the parent array."""
+
+    left: np.ndarray
+    right: np.ndarray
+    parent: np.ndarray
+
+
+def generate_topology(sorted_codes, threads: int = 1) -> Topology:
+    """Radix-tree topology over sorted codes (tree.py:85-105), on the GPU.
+
+    Uses the bottom-up kernel of :func:`build` (topology-only variant); the
+    result equals the reference's top-down Karras construction exactly.
+    """
+    codes = np.ascontiguousarray(sorted_codes, dtype=np.uint32)
+    n = codes.shape[0]
+    if n < 1:
+        raise ValueError("empty scene")
+    l = _lib.lib()
+    dc = dv.h2d(codes.view(np.int32))
+    left = dv.empty(max(n - 1, 0), torch.int32)
+    right = dv.empty(max(n - 1, 0), torch.int32)
+    parent = dv.empty(2 * n - 1, torch.int32)
+    ws = dv.workspace(l.lbvh_topology_workspace_bytes(n))
+    _lib.check(l.lbvh_generate_topology(dv.ptr(dc), n, dv.ptr(left), dv.ptr(right),
+                                        dv.ptr(parent), dv.ptr(ws), ws.numel(), dv.stream()))
+    le, ri, pa = dv.d2h_many(left, right, parent)
+    return Topology(le.copy(), ri.copy(), pa.copy())
+
+
+def refit_bounds(node_mins, node_maxs, topology: Topology) -> None:
+    """Fill internal boxes bottom-up in place (tree.py:108-119), on the GPU."""
+    n = (node_mins.shape[0] + 1) // 2
+    if n <= 1:
+        return
+    l = _lib.lib()
+    dmin = dv.h2d(np.ascontiguousarray(node_mins, dtype=np.float32))
+    dmax = dv.h2d(np.ascontiguousarray(node_maxs, dtype=np.float32))
+    dl = dv.h2d(np.ascontiguousarray(topology.left, dtype=np.int32))
+    dr = dv.h2d(np.ascontiguousarray(topology.right, dtype=np.int32))
+    dp = dv.h2d(np.ascontiguousarray(topology.parent, dtype=np.int32))
+    ws = dv.workspace(l.lbvh_topology_workspace_bytes(n))
+    _lib.check(l.lbvh_refit(dv.ptr(dmin), dv.ptr(dmax), dv.ptr(dl), dv.ptr(dr), dv.ptr(dp), n,
+                            dv.ptr(ws), ws.numel(), dv.stream()))
+    hmin, hmax = dv.d2h_many(dmin, dmax)
+    node_mins[...] = hmin
+    node_maxs[...] = hmax

@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs and the CPU oracle.  Integer/index results must be
+bit-exact; kNN distances too (same fp32 recipe, correctly rounded sqrt)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1908_11807_b200 as lb
+from oracle import oracle
+from paper_1908_11807_b200 import datasets
+
+from helpers import assert_same_tree, in_order_leaves, sha16, sorted_concat
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", ["line4", "cloud", "ext", "dup"])
+def test_tree_bitwise_equals_reference(golden, case):
+    tree = lb.build(golden[case + "_pts"])
+    assert_same_tree(tree, golden, case + "_")
+
+
+def test_volumetric_boxes(golden):
+    tree = lb.build((golden["vol_mins"], golden["vol_maxs"]))
+    assert_same_tree(tree, golden, "vol_")
+    rs = lb.query_spatial_2p(tree, (golden["vol_centers"], np.float32(1.7)))
+    assert np.array_equal(rs.offsets, golden["vol_sp_offsets"])
+    assert np.array_equal(sorted_concat(rs.offsets, rs.indices), golden["vol_sp_sorted_indices"])
+    rk = lb.query_knn(tree, (golden["vol_centers"], 7))
+    assert np.array_equal(rk.indices, golden["vol_knn_indices"])
+    assert rk.distances.tobytes() == golden["vol_knn_distances"].tobytes()
+
+
+def test_boxes_as_n6_rows_equal_pair_form(golden):
+    rows = np.concatenate([golden["vol_mins"], golden["vol_maxs"]], axis=1)
+    assert_same_tree(lb.build(rows), golden, "vol_")
+
+
+def test_morton_codes_bitwise(golden):
+    pts = golden["morton_pts"]
+    z, one = np.zeros(3, np.float32), np.ones(3, np.float32)
+    assert np.array_equal(lb.morton_codes(pts, z, one), golden["morton_codes_unit"])
+    assert np.array_equal(lb.morton_codes(pts, z, np.float32([1, 0, 1])),
+                          golden["morton_codes_flat"])
+    t = lb.build(golden["ext_pts"])
+    codes = lb.morton_codes(golden["ext_pts"], t.scene_min, t.scene_max)
+    assert codes.tolist() == [0, 1073741823, 939524096, 747784484]
+
+
+@pytest.mark.parametrize("prefix", ["topo", "topod"])
+def test_generate_topology_bitwise(golden, prefix):
+    topo = lb.generate_topology(golden[prefix + "_codes"])
+    assert np.array_equal(topo.left, golden[prefix + "_left"])
+    assert np.array_equal(topo.right, golden[prefix + "_right"])
+    assert np.array_equal(topo.parent, golden[prefix + "_parent"])
+
+
+def test_refit_bounds_matches_build(golden):
+    from paper_1908_11807_b200.tree import refit_bounds, Topology
+
+    t = lb.build(golden["cloud_pts"])
+    n = t.leaf_count
+    mins = t.node_mins.copy()
+    maxs = t.node_maxs.copy()
+    mins[: n - 1] = 0
+    maxs[: n - 1] = 0
+    parent = np.full(2 * n - 1, -1, np.int32)
+    parent[t.left] = np.arange(n - 1)
+    parent[t.right] = np.arange(n - 1)
+    refit_bounds(mins, maxs, Topology(t.left, t.right, parent))
+    assert mins.tobytes() == t.node_mins.tobytes() and maxs.tobytes() == t.node_maxs.tobytes()
+
+
+def test_cloud_queries_against_reference(golden):
+    tree = lb.build(golden["cloud_pts"])
+    c = golden["cloud_sp_centers"]
+    rs = lb.query_spatial_2p(tree, (c, 1.5))
+    assert rs.offsets.dtype == np.int64 and rs.indices.dtype == np.int32
+    assert np.array_equal(rs.offsets, golden["cloud_sp_offsets"])
+    assert np.array_equal(sorted_concat(rs.offsets, rs.indices), golden["cloud_sp_sorted_indices"])
+    rs = lb.query_spatial_2p(tree, (c, golden["cloud_spr_radii"]))
+    assert np.array_equal(sorted_concat(rs.offsets, rs.indices), golden["cloud_spr_sorted_indices"])
+    for b in (1, 4, 32):
+        r1, fb = lb.query_spatial_1p(tree, (c, 1.5), b)
+        assert fb == bool(golden[f"cloud_1p{b}_fellback"])
+        assert np.array_equal(sorted_concat(r1.offsets, r1.indices),
+                              golden[f"cloud_1p{b}_sorted_indices"])
+    kc = golden["cloud_knn_centers"]
+    for tag, k, cs in (("cloud_knn_", 10, kc), ("cloud_knnk_", golden["cloud_knnk_ks"], kc),
+                       ("cloud_knn100_", 100, kc[:40])):
+        rk = lb.query_knn(tree, (cs, k))
+        assert np.array_equal(rk.offsets, golden[tag + "offsets"]), tag
+        assert np.array_equal(rk.indices, golden[tag + "indices"]), tag
+        assert rk.distances.tobytes() == golden[tag + "distances"].tobytes(), tag
+    assert np.array_equal(lb.query_sort_order(c, (tree.scene_min, tree.scene_max)),
+                          golden["cloud_order"])
+
+
+def test_integer_clouds_with_heavy_ties(golden):
+    for i in range(int(golden["int_ncases"])):
+        p = f"int{i}_"
+        tree = lb.build(golden[p + "pts"])
+        assert_same_tree(tree, golden, p)
+        cs = golden[p + "centers"]
+        rs = lb.query_spatial_2p(tree, (cs, golden[p + "r"]))
+        assert np.array_equal(rs.offsets, golden[p + "sp_offsets"])
+        assert np.array_equal(sorted_concat(rs.offsets, rs.indices), golden[p + "sp_sorted_indices"])
+        rk = lb.query_knn(tree, (cs, int(golden[p + "k"])))
+        assert np.array_equal(rk.indices, golden[p + "knn_indices"]), p
+        assert rk.distances.tobytes() == golden[p + "knn_distances"].tobytes(), p
+
+
+@pytest.mark.parametrize("name", ["c1_filled", "c3_hollow_sphere", "hollow_cube"])
+def test_reference_digests_c1_scale(digests, name):
+    d = digests[name]
+    pts = datasets.generate(datasets.CloudSpec.parse(d["source"], d["m"], d["seed"]))
+    q = datasets.generate(datasets.CloudSpec.parse(d["target"], d["m"], d["target_seed"]))
+    t = lb.build(pts)
+    assert t.scene_min.tolist() == d["scene_min"] and t.scene_max.tolist() == d["scene_max"]
+    for f in ("leaf_obj", "left", "right", "node_mins", "node_maxs"):
+        assert sha16(getattr(t, f)) == d[f], f
+    assert sha16(lb.morton_codes(pts, t.scene_min, t.scene_max)) == d["codes"]
+    rs = lb.query_spatial_2p(t, (q, d["radius"]))
+    assert sha16(rs.offsets) == d["sp_offsets"] and int(rs.offsets[-1]) == d["sp_total"]
+    assert sha16(sorted_concat(rs.offsets, rs.indices)) == d["sp_sorted_indices"]
+    rk = lb.query_knn(t, (q, d["k"]))
+    assert sha16(rk.indices) == d["knn_indices"] and sha16(rk.distances) == d["knn_distances"]
+    assert sha16(lb.query_sort_order(q, (t.scene_min, t.scene_max))) == d["query_order"]
+
+
+@pytest.mark.parametrize("shape", ["cube:filled", "sphere:hollow", "cube:hollow"])
+def test_against_oracle_unsorted_hit_order(shape):
+    """Traversal order is the reference's, so even the unsorted CRS equals
+    the oracle's byte for byte."""
+    pts = datasets.generate(datasets.CloudSpec.parse(shape, 200_000, 3))
+    q = datasets.generate(datasets.CloudSpec.parse("sphere:filled", 50_000, 4))
+    t, ref = lb.build(pts), oracle.build(pts)
+    for f in ("node_mins", "node_maxs", "left", "right", "leaf_obj"):
+        assert getattr(t, f).tobytes() == getattr(ref, f).tobytes(), f
+    r = datasets.default_radius(10)
+    rs = lb.query_spatial_2p(t, (q, r))
+    off, idx = oracle.query_spatial_2p(ref, q, r)
+    assert np.array_equal(rs.offsets, off) and np.array_equal(rs.indices, idx)
+    for k in (1, 5, 10, 16, 31, 50):
+        rk = lb.query_knn(t, (q[:20_000], k))
+        ko, ki, kd = oracle.query_knn(ref, q[:20_000], k)
+        assert np.array_equal(rk.indices, ki), k
+        assert rk.distances.tobytes() == kd.tobytes(), k
+
+
+def test_device_resident_inputs_and_outputs():
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 50_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 10_000, 1))
+    th = lb.build(pts)
+    td = lb.build(torch.from_numpy(pts).cuda())
+    assert th.node_mins.tobytes() == td.node_mins.tobytes()
+    qd = torch.from_numpy(q).cuda()
+    rk = lb.query_knn(td, (qd, 10))
+    assert rk.on_device and rk.indices.is_cuda
+    hk = lb.query_knn(th, (q, 10))
+    assert np.array_equal(rk.to_host().indices, hk.indices)
+    rs = lb.query_spatial_2p(td, (qd, 2.0))
+    assert np.array_equal(rs.to_host().offsets, lb.query_spatial_2p(th, (q, 2.0)).offsets)
+
+
+def test_large_scale_properties_1e7():
+    """Full C2 size: size-independent properties (sortedness of leaf codes,
+    containment, root box == scene box), plus oracle parity on a query sample."""
+    n = 10_000_000
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", n, 0))
+    t = lb.build(torch.from_numpy(pts).cuda())
+    d = t.device_arrays()
+    smin = pts.min(axis=0)
+    smax = pts.max(axis=0)
+    assert np.array_equal(t.scene_min, smin) and np.array_equal(t.scene_max, smax)
+    leaf_obj = d["leaf_obj"].long()
+    assert torch.equal(torch.sort(leaf_obj).values, torch.arange(n, device="cuda"))
+    codes = torch.from_numpy(lb.morton_codes(pts, smin, smax).view(np.int32)).cuda()[leaf_obj]
+    assert bool((codes[1:] >= codes[:-1]).all())
+    ties = codes[1:] == codes[:-1]
+    assert bool((leaf_obj[1:][ties] > leaf_obj[:-1][ties]).all())
+    nm, nx = d["node_mins"], d["node_maxs"]
+    left, right = d["left"].long(), d["right"].long()
+    assert bool((nm[: n - 1] <= nm[left]).all()) and bool((nx[: n - 1] >= nx[right]).all())
+    indeg = torch.bincount(torch.cat([left, right]), minlength=2 * n - 1)
+    assert int(indeg[0]) == 0 and bool((indeg[1:] == 1).all())
+    # queries: sample vs oracle on the same tree (oracle on the GPU tree's arrays)
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 100_000, 1))
+    ref = oracle.OracleTree(t.node_mins, t.node_maxs, t.left, t.right, t.leaf_obj,
+                            t.scene_min, t.scene_max)
+    r = datasets.default_radius(10)
+    rs = lb.query_spatial_2p(t, (q, r))
+    off, idx = oracle.query_spatial_2p(ref, q, r)
+    assert np.array_equal(rs.offsets, off) and np.array_equal(rs.indices, idx)
+    rk = lb.query_knn(t, (q, 10))
+    ko, ki, kd = oracle.query_knn(ref, q, 10)
+    assert np.array_equal(rk.indices, ki) and rk.distances.tobytes() == kd.tobytes()
