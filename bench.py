@@ -1,0 +1,504 @@
+"""Benchmark of the B200 LBVH hot path (BASELINE.json metric, config C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline (``value``): kNN (k=10) queries/sec, 1e7 filled-box points indexed,
+1e7 filled-box queries (cube:filled seed 0 / seed 1, the reference bench's
+clouds), inputs resident in HBM, query Morton pre-sort included, timed with
+CUDA events on the launching stream; L2 is flushed (256 MiB write) before
+every timed step.  One step = one query batch of nq queries through
+``query_knn`` (device-resident entry).  ``e2e`` is the same metric through
+the public API with pinned host input and numpy (pinned) results.  Extra
+metrics of the same run (build prims/s, radius 2P / 1P, hollow sphere C3)
+are in ``extra``.
+
+``--impl reference`` times the CPU restatement of the reference path
+(oracle/, all host threads) on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): weak scaling, one process per GPU; every rank indexes
+its own 1e7-point shard and answers its own 1e7 queries (replicas, see
+DESIGN.md); time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+
+# Algorithmic bytes; T = box tests per query of the
+# reference algorithm on the reference tree (filled 1e7).
+T_KNN_FILLED_1E7 = 157.8
+T_RAD_FILLED_1E7 = 133.1
+T_RAD_HOLLOW_1E7 = 43.7
+BUILD_BYTES_PER_PRIM = 152
+
+
+def knn_bytes_per_query(k: int, t: float = T_KNN_FILLED_1E7) -> float:
+    return 12 + 8 + 8 * k + 28 * t
+
+
+def radius_bytes_per_query(hits: float, t: float) -> float:
+    return 12 + 4 + 8 + 4 * hits + 28 * t
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--m", type=int, default=10_000_000, help="indexed points per GPU")
+    p.add_argument("--nq", type=int, default=None, help="queries per GPU (default m)")
+    p.add_argument("--k", type=int, default=10)
+    p.add_argument("--no-extra", action="store_true", help="headline metric only")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--cpu-sample", type=int, default=1_000_000,
+                   help="queries in the CPU baseline sample")
+    p.add_argument("--profile", action="store_true",
+                   help="short run for ncu: no clocks/cpu/e2e/extra legs")
+    return p.parse_args(argv)
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    try:
+        with open(NCU_SUMMARY) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during a timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        loaded = []
+        for r in rows:
+            for i, nm in enumerate(names):
+                if "Active" in r[2 + i] and "Not" not in r[2 + i]:
+                    reasons.add(nm)
+            try:
+                if float(r[6]) > 0:
+                    loaded.append(float(r[0]))
+            except ValueError:
+                pass
+        all_sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        sm = statistics.median(loaded or all_sm) if (loaded or all_sm) else None
+        return {"sm_mhz": sm, "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+class KernelTimer:
+    """CUDA-event brackets around named launches (traversal.KERNEL_TIMER)."""
+
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.events = {}
+        self.enabled = False
+
+    def wrap(self, name, call):
+        if not self.enabled:
+            return call()
+        t = self.torch
+        s, e = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        s.record()
+        rc = call()
+        e.record()
+        self.events.setdefault(name, []).append((s, e))
+        return rc
+
+    def mean_ms(self, name):
+        ev = self.events.get(name, [])
+        if not ev:
+            return None
+        return sum(s.elapsed_time(e) for s, e in ev) / len(ev)
+
+    def reset(self):
+        self.events = {}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1908_11807_b200 as lb
+    from paper_1908_11807_b200 import _lib, traversal, tree as tree_mod
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    m = args.m
+    nq = args.nq or m
+    k = args.k
+    lib = _lib.lib()
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush_l2():
+        flush_buf.fill_(rank & 0xFF)
+
+    # Weak scaling: rank r indexes cloud seed 2r and queries cloud seed 2r+1
+    # (rank 0 = the reference bench's seeds 0 / 1).
+    src_spec = lb.CloudSpec("cube", "filled", m, 2 * rank)
+    qry_spec = lb.CloudSpec("cube", "filled", nq, 2 * rank + 1)
+    pts = lb.generate(src_spec)
+    qs = lb.generate(qry_spec)
+    pts_d = torch.from_numpy(pts).to(dev)
+    qs_d = torch.from_numpy(qs).to(dev)
+    r = lb.default_radius(k)
+
+    timer = KernelTimer()
+    traversal.KERNEL_TIMER = timer
+    tree_mod.KERNEL_TIMER = timer
+
+    def timed_loop(step_fn, steps, warmup, kernel=None):
+        for _ in range(warmup):
+            step_fn()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        timer.reset()
+        timer.enabled = True
+        launches0 = lib.lbvh_launch_count()
+        total_ms = 0.0
+        for _ in range(steps):
+            flush_l2()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step_fn()
+            e.record()
+            e.synchronize()
+            total_ms += s.elapsed_time(e)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        timer.enabled = False
+        launches = lib.lbvh_launch_count() - launches0
+        kms = timer.mean_ms(kernel) if kernel else None
+        return max_over_ranks(total_ms), launches, kms
+
+    # -- build the index once (its own timed leg below) ----------------------
+    tree = lb.build(pts_d)
+
+    def knn_step():
+        rs = lb.query_knn(tree, (qs_d, k))
+        return rs
+
+    clocks = None
+    if args.profile:
+        tot, launches, knn_ms = timed_loop(knn_step, args.steps, args.warmup, "knn")
+    else:
+        with ClockSampler(local) as cs:
+            tot, launches, knn_ms = timed_loop(knn_step, args.steps, args.warmup, "knn")
+        clocks = cs.summary()
+    ms_per_step = tot / args.steps
+    value = world * nq * args.steps / (tot / 1e3)
+
+    peak_gbs, peak_src = load_peaks()
+    bq = knn_bytes_per_query(k)
+    achieved = nq * bq / (knn_ms / 1e3) / 1e9 if knn_ms else None
+    traffic = load_traffic().get("knn_kernel_dram_bytes_per_launch")
+    roofline = {
+        "bound": "hbm", "kernel": "knn_kernel<10>",
+        "achieved": round(achieved, 1) if achieved else None, "peak": peak_gbs, "unit": "GB/s",
+        "frac": round(achieved / peak_gbs, 4) if achieved else None,
+        "traffic": traffic,
+        "kernel_ms": round(knn_ms, 4) if knn_ms else None,
+        "kernel_share_of_step": round(knn_ms / ms_per_step, 3) if knn_ms else None,
+        "algorithmic_bytes_per_query": bq,
+        "bytes_model": "12 center + 8 offset + 8k idx/dist + 28 B x T box tests, "
+                       f"T={T_KNN_FILLED_1E7} (SURVEY.md 6.3, filled 1e7)",
+        "peak_source": peak_src,
+    }
+
+    out = {
+        "metric": f"knn_queries_per_sec (k={k}, {m:.0e} filled-box points, {nq:.0e} queries)",
+        "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 Morton normalisation)",
+        "data": "synthetic: paper_1908_11807_b200.datasets PCG64 clouds (reference generators)",
+        "config": {"workload": f"C2 kNN: cube:filled m={m} seed {2 * rank} / cube:filled "
+                               f"nq={nq} seed {2 * rank + 1}, k={k}, query Morton pre-sort on",
+                   "m_per_gpu": m, "nq_per_gpu": nq, "k": k,
+                   "l2": "flushed before every timed step (256 MiB device write)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+    }
+    if clocks is not None:
+        out["clocks"] = clocks
+
+    if not args.profile:
+        # -- e2e through the public API with pinned host buffers --------------
+        pin = torch.empty((nq, 3), dtype=torch.float32, pin_memory=True)
+        pin.numpy()[:] = qs
+        host_q = pin.numpy()
+
+        def e2e_step():
+            rs = lb.query_knn(tree, (host_q, k))
+            assert rs.indices.shape[0] == nq * min(k, m)
+            return rs
+
+        e2e_tot, _, _ = timed_loop(e2e_step, max(2, args.steps // 2), 2)
+        e2e_steps = max(2, args.steps // 2)
+        span = min(k, m)
+        out["e2e"] = {"value": round(world * nq * e2e_steps / (e2e_tot / 1e3), 1),
+                      "unit": "queries/s",
+                      "h2d_bytes_per_step": nq * 12,
+                      "d2h_bytes_per_step": (nq + 1) * 8 + nq * span * 8 + 4,
+                      "ms_per_step": round(e2e_tot / e2e_steps, 3),
+                      "api": "paper_1908_11807_b200.query_knn(tree, (pinned numpy centers, k))"}
+
+    if not args.no_extra and not args.profile:
+        out["extra"] = extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank,
+                                     dev, peak_gbs)
+
+    if rank == 0 and not args.no_cpu and not args.profile:
+        out["cpu_baseline"] = cpu_baseline(args, pts, qs, k)
+
+    traversal.KERNEL_TIMER = None
+    tree_mod.KERNEL_TIMER = None
+    if world > 1:
+        tdist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, dev, peak_gbs):
+    import torch
+
+    m = int(pts_d.shape[0])
+    nq = int(qs_d.shape[0])
+    steps, warm = args.steps, args.warmup
+    ex = {}
+
+    # build prims/s (device-resident input, full pipeline)
+    def build_step():
+        return lb.build(pts_d)
+
+    tot, launches, bms = timed_loop(build_step, steps, warm, "build")
+    ex["build_prims_per_sec"] = round(world * m * steps / (tot / 1e3), 1)
+    ex["build_ms"] = round(tot / steps, 3)
+    ex["build_roofline_frac"] = round(m * BUILD_BYTES_PER_PRIM / (bms / 1e3) / 1e9 / peak_gbs, 4)
+    ex["build_launches_per_step"] = launches / steps
+
+    # radius 2P, filled/filled
+    counts_box = {}
+
+    def rad_step():
+        rs = lb.query_spatial_2p(tree, (qs_d, r))
+        counts_box["total"] = rs.offsets[-1]
+        return rs
+
+    tot, _, cms = timed_loop(rad_step, steps, warm, "spatial_count")
+    hits = float(counts_box["total"]) / nq
+    ex["radius_2p_queries_per_sec"] = round(world * nq * steps / (tot / 1e3), 1)
+    ex["radius_2p_ms"] = round(tot / steps, 3)
+    ex["radius_mean_hits"] = round(hits, 3)
+    if cms:
+        ex["radius_count_kernel_frac"] = round(
+            nq * radius_bytes_per_query(hits, T_RAD_FILLED_1E7) / (cms / 1e3) / 1e9 / peak_gbs, 4)
+
+    # radius 1P, B=32
+    fb = {}
+
+    def rad1_step():
+        rs, f = lb.query_spatial_1p(tree, (qs_d, r), 32)
+        fb["f"] = f
+        return rs
+
+    tot, _, _ = timed_loop(rad1_step, steps, warm)
+    ex["radius_1p_b32_queries_per_sec"] = round(world * nq * steps / (tot / 1e3), 1)
+    ex["radius_1p_b32_fell_back"] = bool(fb["f"])
+
+    # C3: hollow-sphere sources vs filled queries, radius 2P
+    hs = lb.generate(lb.CloudSpec("sphere", "hollow", m, 2 * rank))
+    hs_d = torch.from_numpy(hs).to(dev)
+    htree = lb.build(hs_d)
+    del hs
+
+    def c3_step():
+        rs = lb.query_spatial_2p(htree, (qs_d, r))
+        counts_box["h"] = rs.offsets[-1]
+        return rs
+
+    tot, _, _ = timed_loop(c3_step, steps, warm)
+    ex["c3_hollow_radius_2p_queries_per_sec"] = round(world * nq * steps / (tot / 1e3), 1)
+    ex["c3_mean_hits"] = round(float(counts_box["h"]) / nq, 3)
+    del htree, hs_d
+    return ex
+
+
+def cpu_baseline(args, pts, qs, k):
+    """Oracle port (oracle/lbvh_oracle.c, OpenMP, all host threads) on a
+    bounded sample: the full m-point tree, the first cpu_sample queries."""
+    from oracle import oracle
+
+    threads = oracle.max_threads()
+    ref = oracle.build(pts, threads=threads)
+    sample = qs[: args.cpu_sample]
+    oracle.query_knn(ref, sample[:1000], k, threads=threads)  # warm
+    t0 = time.perf_counter()
+    oracle.query_knn(ref, sample, k, threads=threads)
+    dt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.build(pts, threads=threads)
+    bdt = time.perf_counter() - t0
+    return {"value": round(sample.shape[0] / dt, 1), "unit": "queries/s", "cores": threads,
+            "kind": "port",
+            "sample": f"kNN k={k}: first {sample.shape[0]} of the {qs.shape[0]} queries "
+                      f"(Morton pre-sort included) against the full {pts.shape[0]}-point tree",
+            "build_prims_per_sec": round(pts.shape[0] / bdt, 1)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle
+    import paper_1908_11807_b200.datasets as ds
+
+    m = args.m
+    nq = args.nq or m
+    k = args.k
+    pts = ds.generate(ds.CloudSpec("cube", "filled", m, 0))
+    qs = ds.generate(ds.CloudSpec("cube", "filled", nq, 1))
+    threads = oracle.max_threads()
+    ref = oracle.build(pts, threads=threads)
+    sample = max(1000, min(args.cpu_sample // 4, nq))
+    for w in range(args.warmup):
+        oracle.query_knn(ref, qs[:sample], k, threads=threads)
+    total = 0.0
+    for s in range(args.steps):
+        lo = (s * sample) % max(1, nq - sample + 1)
+        t0 = time.perf_counter()
+        oracle.query_knn(ref, qs[lo:lo + sample], k, threads=threads)
+        total += time.perf_counter() - t0
+    value = args.steps * sample / total
+    out = {
+        "impl": "reference",
+        "metric": f"knn_queries_per_sec (k={k}, {m:.0e} filled-box points, {nq:.0e} queries)",
+        "value": round(value, 1), "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: same clouds as the GPU arm",
+        "config": {"workload": f"C2 kNN: cube:filled m={m} seed 0 / cube:filled nq={nq} seed 1, "
+                               f"k={k}", "m_per_gpu": m, "nq_per_gpu": nq, "k": k},
+        "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{sample} queries per step against the full {m}-point tree"},
+        "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

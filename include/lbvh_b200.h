@@ -72,6 +72,9 @@ const char *lbvh_strerror(int code);
 /* Last CUDA error string seen by this thread (for LBVH_ERR_CUDA). */
 const char *lbvh_last_cuda_error(void);
 int lbvh_abi_version(void);
+/* Number of kernels this library has launched in this process (diagnostic;
+ * lets a harness count device launches inside a timed region). */
+uint64_t lbvh_launch_count(void);
 
 /* ---------------------------------------------------------------- build */
 

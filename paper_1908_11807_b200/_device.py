@@ -8,6 +8,8 @@ speed and no extra host copy is made.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -47,7 +49,13 @@ def is_cuda_tensor(x) -> bool:
 
 def h2d(arr: np.ndarray) -> torch.Tensor:
     """Host numpy -> device tensor (async from pinned memory, else staged)."""
-    t = torch.from_numpy(np.ascontiguousarray(arr))
+    arr = np.ascontiguousarray(arr)
+    if not arr.flags.writeable:  # torch warns on read-only views; we never write them
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            t = torch.from_numpy(arr)
+    else:
+        t = torch.from_numpy(arr)
     return t.to(device(), non_blocking=True)
 
 

@@ -49,6 +49,7 @@ _SIGS = {
     "lbvh_strerror": ([ctypes.c_int], ctypes.c_char_p),
     "lbvh_last_cuda_error": ([], ctypes.c_char_p),
     "lbvh_abi_version": ([], ctypes.c_int),
+    "lbvh_launch_count": ([], ctypes.c_uint64),
     "lbvh_build_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_sort_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_topology_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),

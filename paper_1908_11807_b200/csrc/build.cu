@@ -407,14 +407,14 @@ int build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_b
 
     unsigned rg = grid_for(n, kReduceThreads, 4);
     scene_reduce_kernel<<<rg, kReduceThreads, 0, stream>>>(mins, maxs, n, partials, counter,
-                                                           root_box, status);
+                                                           root_box, status); count_launches(1);
     unsigned mg = grid_for(n, 256, 16);
-    morton_kernel<<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm);
+    morton_kernel<<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm); count_launches(1);
     int rc = sort_pairs(codes, perm, n, 30, sort_ws, sort_workspace_bytes(n), stream);
     if (rc != LBVH_OK) return rc;
     hierarchy_kernel<true><<<div_up(n, 256), 256, 0, stream>>>(
         codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-        leaf_obj, (PackedNode *)nodes, root_box);
+        leaf_obj, (PackedNode *)nodes, root_box); count_launches(1);
     if (sorted_codes)
         cudaMemcpyAsync(sorted_codes, codes, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
                         stream);
@@ -435,7 +435,7 @@ int generate_topology(const uint32_t *codes, int64_t n, int32_t *left, int32_t *
     cudaMemsetAsync(slots, 0, sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1), stream);
     hierarchy_kernel<false><<<div_up(n, 256), 256, 0, stream>>>(
         codes, nullptr, nullptr, nullptr, n, slots, nullptr, nullptr, left, right, parent,
-        nullptr, nullptr, nullptr);
+        nullptr, nullptr, nullptr); count_launches(1);
     return check_launch();
 }
 
@@ -448,7 +448,7 @@ int refit(float *node_mins, float *node_maxs, const int32_t *left, const int32_t
     uint32_t *visits = (uint32_t *)ws;
     cudaMemsetAsync(visits, 0, sizeof(uint32_t) * (size_t)(n - 1), stream);
     refit_kernel<<<div_up(n, 256), 256, 0, stream>>>(node_mins, node_maxs, left, right,
-                                                      parent, n, visits);
+                                                      parent, n, visits); count_launches(1);
     return check_launch();
 }
 
@@ -459,7 +459,7 @@ int pack(const lbvh_tree *t, void *nodes, float *root_box, uint32_t *status,
     if (t->n > 1 && (!t->left || !t->right || !nodes)) return LBVH_ERR_INVALID_ARG;
     int64_t work = t->n > 1 ? t->n - 1 : 1;
     pack_kernel<<<div_up(work, 256), 256, 0, stream>>>(*t, (PackedNode *)nodes, root_box,
-                                                       status);
+                                                       status); count_launches(1);
     return check_launch();
 }
 
@@ -467,7 +467,7 @@ int unpack_boxes(const lbvh_tree *t, float *node_mins, float *node_maxs, cudaStr
     if (!t || t->n < 1 || !t->root_box || !node_mins || !node_maxs) return LBVH_ERR_INVALID_ARG;
     if (t->n > 1 && (!t->left || !t->right || !t->nodes)) return LBVH_ERR_INVALID_ARG;
     int64_t work = t->n > 1 ? t->n - 1 : 1;
-    unpack_kernel<<<div_up(work, 256), 256, 0, stream>>>(*t, node_mins, node_maxs);
+    unpack_kernel<<<div_up(work, 256), 256, 0, stream>>>(*t, node_mins, node_maxs); count_launches(1);
     return check_launch();
 }
 
@@ -476,7 +476,7 @@ int morton_codes_f64(const double *pts, int64_t n, const double *lo, const doubl
     if (n < 0 || (n > 0 && (!pts || !codes)) || !lo || !hi) return LBVH_ERR_INVALID_ARG;
     if (n == 0) return LBVH_OK;
     morton_f64_kernel<<<grid_for(n, 256, 16), 256, 0, stream>>>(pts, n, lo[0], lo[1], lo[2],
-                                                               hi[0], hi[1], hi[2], codes);
+                                                               hi[0], hi[1], hi[2], codes); count_launches(1);
     return check_launch();
 }
 
@@ -495,7 +495,7 @@ int query_order(const float *centers, int64_t nq, const float *scene, uint32_t *
     uint32_t *codes = c.take<uint32_t>(nq);
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
     morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq, scene, codes,
-                                                             order);
+                                                             order); count_launches(1);
     int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream);
     if (rc != LBVH_OK) return rc;
     return check_launch();

@@ -3,12 +3,18 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "internal.cuh"
 
 namespace lbvh {
 
 static thread_local char g_cuda_err[256] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launches(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void set_cuda_error(cudaError_t e) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e),
@@ -76,6 +82,8 @@ const char *lbvh_strerror(int code) {
 const char *lbvh_last_cuda_error(void) { return g_cuda_err; }
 
 int lbvh_abi_version(void) { return 1; }
+
+uint64_t lbvh_launch_count(void) { return launch_count(); }
 
 size_t lbvh_build_workspace_bytes(int64_t n) { return build_workspace_bytes(n); }
 size_t lbvh_sort_workspace_bytes(int64_t n) { return sort_workspace_bytes(n); }

@@ -10,6 +10,9 @@ namespace lbvh {
 // LBVH_ERR_CUDA on a pending launch error, LBVH_OK otherwise.
 int check_launch();
 void set_cuda_error(cudaError_t e);
+// Kernel-launch accounting for lbvh_launch_count().
+void count_launches(int k);
+uint64_t launch_count();
 
 size_t sort_workspace_bytes(int64_t n);
 int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,

@@ -243,14 +243,14 @@ int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws
     cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
-    histogram_kernel<<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, hist);
-    exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes);
+    histogram_kernel<<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, hist); count_launches(1);
+    exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes); count_launches(1);
 
     uint32_t *ks = keys, *vs = vals, *kd = k_alt, *vd = v_alt;
     for (int p = 0; p < passes; ++p) {
         onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, stream>>>(
             ks, vs, kd, vd, n, p * kRadixBits, hist + p * kRadix,
-            lookback + (size_t)p * tiles * kRadix, counters + p);
+            lookback + (size_t)p * tiles * kRadix, counters + p); count_launches(1);
         uint32_t *t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
     }

@@ -153,7 +153,7 @@ int launch_scan(In in, int64_t n, int64_t *offsets, int32_t *max_out, uint32_t *
     cudaMemsetAsync(c.base, 0, c.off, stream);
     if (max_out) cudaMemsetAsync(max_out, 0, sizeof(int32_t), stream);
     scan_kernel<In><<<(unsigned)tiles, kScanThreads, 0, stream>>>(in, n, offsets, lookback,
-                                                                 counter, max_out, status);
+                                                                 counter, max_out, status); count_launches(1);
     return check_launch();
 }
 

@@ -374,7 +374,7 @@ int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii,
     if (MODE == kFill && !offsets) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     spatial_kernel<MODE><<<div_up(nq, 256), 256, 0, stream>>>(
-        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, status);
+        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, status); count_launches(1);
     return check_launch();
 }
 
@@ -407,7 +407,7 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
     if (nq < 0 || cap < 1) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (!buf || !counts || !offsets) return LBVH_ERR_INVALID_ARG;
-    compact_kernel<<<div_up(nq * 32, 256), 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
+    compact_kernel<<<div_up(nq * 32, 256), 256, 0, stream>>>(buf, cap, counts, offsets, nq, out); count_launches(1);
     return check_launch();
 }
 
@@ -422,7 +422,7 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order, int64_t
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
         knn_kernel<KV><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets, out_idx,     \
-                                              out_dist, status);                            \
+                                              out_dist, status); count_launches(1);                            \
         return check_launch();                                                              \
     }
     LBVH_KNN_CASE(4)
@@ -432,7 +432,7 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order, int64_t
     LBVH_KNN_CASE(32)
 #undef LBVH_KNN_CASE
     knn_heap_kernel<<<div_up(nq, 128), 128, 0, stream>>>(*t, centers, order, nq, offsets,
-                                                         out_idx, out_dist, status);
+                                                         out_idx, out_dist, status); count_launches(1);
     return check_launch();
 }
 
@@ -443,7 +443,7 @@ int check_queries(const float *centers, int64_t nq, const float *radii, uint32_t
     if (!centers) return LBVH_ERR_INVALID_ARG;
     unsigned g = div_up(3 * nq, 256);
     g = g < kNumSMs * 8 ? g : kNumSMs * 8;
-    check_queries_kernel<<<g, 256, 0, stream>>>(centers, nq, radii, status);
+    check_queries_kernel<<<g, 256, 0, stream>>>(centers, nq, radii, status); count_launches(1);
     return check_launch();
 }
 

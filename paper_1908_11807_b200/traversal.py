@@ -37,6 +37,15 @@ __all__ = ["SpatialQuery", "KnnQuery", "ResultSet", "STACK_CAPACITY", "traverse_
 
 STACK_CAPACITY = _lib.STACK_CAPACITY
 
+# Benchmark hook: when set to an object with ``wrap(name, call)``, the main
+# traversal launches are bracketed by CUDA events on the launching stream.
+KERNEL_TIMER = None
+
+
+def _launch(name: str, call) -> int:
+    t = KERNEL_TIMER
+    return call() if t is None else t.wrap(name, call)
+
 
 @dataclass(frozen=True)
 class SpatialQuery:
@@ -283,8 +292,9 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     st = dv.stream()
     nq = b.nq
     counts = dv.empty(nq, torch.int32)
-    _lib.check(l.lbvh_spatial_count(ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
-                                    dv.ptr(order), nq, dv.ptr(counts), status.ptr, st))
+    _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
+        ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq, dv.ptr(counts),
+        status.ptr, st)))
     offsets = dv.empty(nq + 1, torch.int64)
     ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
     _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
@@ -294,9 +304,9 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     total = int(total[0])
     out = dv.empty(total, torch.int32)
     if total:
-        _lib.check(l.lbvh_spatial_fill(ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
-                                       dv.ptr(order), nq, dv.ptr(offsets), dv.ptr(out),
-                                       status.ptr, st))
+        _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
+            ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq,
+            dv.ptr(offsets), dv.ptr(out), status.ptr, st)))
     return offsets, out
 
 
@@ -340,9 +350,9 @@ def query_spatial_1p(tree: Bvh, queries, buffer_size: int, sort_queries: bool = 
     ct = tree.ctree()
     buf = dv.empty((nq, buffer_size), torch.int32)
     counts = dv.empty(nq, torch.int32)
-    _lib.check(l.lbvh_spatial_1p(ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
-                                 dv.ptr(order), nq, dv.ptr(buf), buffer_size, dv.ptr(counts),
-                                 status.ptr, st))
+    _lib.check(_launch("spatial_1p", lambda: l.lbvh_spatial_1p(
+        ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq, dv.ptr(buf),
+        buffer_size, dv.ptr(counts), status.ptr, st)))
     offsets = dv.empty(nq + 1, torch.int64)
     ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
     _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
@@ -394,8 +404,10 @@ def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -
     order = _order(tree, b, sort_queries)
     out_idx = dv.empty(total, torch.int32)
     out_dist = dv.empty(total, torch.float32)
-    _lib.check(l.lbvh_knn(tree.ctree(), dv.ptr(b.centers), dv.ptr(order), nq, dv.ptr(offsets),
-                          max_span, dv.ptr(out_idx), dv.ptr(out_dist), status.ptr, st))
+    ct = tree.ctree()
+    _lib.check(_launch("knn", lambda: l.lbvh_knn(
+        ct, dv.ptr(b.centers), dv.ptr(order), nq, dv.ptr(offsets), max_span, dv.ptr(out_idx),
+        dv.ptr(out_dist), status.ptr, st)))
     offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
     return ResultSet._trusted(offsets, out_idx, out_dist)
 

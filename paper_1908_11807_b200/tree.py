@@ -27,6 +27,15 @@ __all__ = ["Bvh", "Topology", "build", "common_prefix", "find_split", "node_rang
            "generate_topology", "refit_bounds"]
 
 
+# Benchmark hook (see traversal.KERNEL_TIMER).
+KERNEL_TIMER = None
+
+
+def _launch(name: str, call) -> int:
+    t = KERNEL_TIMER
+    return call() if t is None else t.wrap(name, call)
+
+
 def _readonly(a: np.ndarray) -> np.ndarray:
     a.setflags(write=False)
     return a
@@ -196,10 +205,10 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> 
     }
     ws = dv.workspace(l.lbvh_build_workspace_bytes(n))
     status = dv.Status()
-    _lib.check(l.lbvh_build(dv.ptr(mins), dv.ptr(maxs), n, dv.ptr(ws), ws.numel(),
+    _lib.check(_launch("build", lambda: l.lbvh_build(dv.ptr(mins), dv.ptr(maxs), n, dv.ptr(ws), ws.numel(),
                             dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]), dv.ptr(d["left"]),
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
-                            dv.ptr(d["nodes"]), None, status.ptr, dv.stream()))
+                            dv.ptr(d["nodes"]), None, status.ptr, dv.stream())))
     if check:
         flags = status.read()
         if flags & _lib.FLAG_NONFINITE:
