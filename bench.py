@@ -393,17 +393,17 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
         ex["radius_count_kernel_frac"] = round(
             nq * radius_bytes_per_query(hits, T_RAD_FILLED_1E7) / (cms / 1e3) / 1e9 / peak_gbs, 4)
 
-    # radius 1P, B=32
+    # radius 1P, B=64 (max count at 1e7 is 33, so B=32 would fall back)
     fb = {}
 
     def rad1_step():
-        rs, f = lb.query_spatial_1p(tree, (qs_d, r), 32)
+        rs, f = lb.query_spatial_1p(tree, (qs_d, r), 64)
         fb["f"] = f
         return rs
 
     tot, _, _ = timed_loop(rad1_step, steps, warm)
-    ex["radius_1p_b32_queries_per_sec"] = round(world * nq * steps / (tot / 1e3), 1)
-    ex["radius_1p_b32_fell_back"] = bool(fb["f"])
+    ex["radius_1p_b64_queries_per_sec"] = round(world * nq * steps / (tot / 1e3), 1)
+    ex["radius_1p_b64_fell_back"] = bool(fb["f"])
 
     # C3: hollow-sphere sources vs filled queries, radius 2P
     hs = lb.generate(lb.CloudSpec("sphere", "hollow", m, 2 * rank))

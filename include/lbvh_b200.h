@@ -177,7 +177,8 @@ int lbvh_compact(const int32_t *buf, int64_t buffer_size, const int32_t *counts,
                  const int64_t *offsets, int64_t nq, int32_t *out, void *stream);
 
 /* kNN spans  replaces traversal.py:261-262: spans = min(k_q, n), offsets =
- * scan(spans).  ks may be NULL -> k.  Sets LBVH_FLAG_BAD_K for k < 1 and
+ * scan(spans).  ks may be NULL -> uniform k (k < 1 is LBVH_ERR_INVALID_ARG;
+ * offsets are written directly, no scan).  Sets LBVH_FLAG_BAD_K for ks < 1 and
  * writes max span to *max_span (device i32). */
 int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_t *offsets,
                      int32_t *max_span, uint32_t *status, void *workspace,

@@ -203,10 +203,10 @@ hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict_
     while (true) {
         const int64_t g = left_side ? r : l - 1;
         const uint32_t known = (uint32_t)(left_side ? l : r);
-        __threadfence();  // release this subtree's boxes before the handshake
-        const uint32_t other = atomicExch(slots + g, known + 1u);
+        // acq_rel exchange: releases this subtree's boxes to the sibling,
+        // acquires the sibling's when we arrive second.
+        const uint32_t other = atomic_exch_acq_rel(slots + g, known + 1u);
         if (other == 0) return;  // first arrival: sibling subtree not done
-        __threadfence();         // acquire the sibling's boxes
         const int64_t pl = left_side ? l : (int64_t)(other - 1u);
         const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
         const int64_t lc = (pl == g) ? internal + g : g;
@@ -270,9 +270,7 @@ refit_kernel(float *node_mins, float *node_maxs, const int32_t *__restrict__ lef
     while (true) {
         const int64_t par = __ldg(parent + node);
         if (par < 0) return;
-        __threadfence();
-        if (atomicAdd(visits + par, 1u) == 0) return;
-        __threadfence();
+        if (atomic_add_acq_rel(visits + par, 1u) == 0) return;
         const int64_t lc = __ldg(left + par), rc = __ldg(right + par);
         Box L, R, P;
         load_box_cg(node_mins, node_maxs, lc, L);

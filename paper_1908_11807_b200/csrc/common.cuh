@@ -84,6 +84,21 @@ __device__ __forceinline__ uint32_t morton3(double x, double y, double z, const 
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// GPU-scope release+acquire read-modify-writes (no full membar).
+__device__ __forceinline__ uint32_t atomic_exch_acq_rel(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ uint32_t atomic_add_acq_rel(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 template <typename T>
 __device__ __forceinline__ T ld_volatile(const T *p) {
     return *reinterpret_cast<const volatile T *>(p);

@@ -137,6 +137,15 @@ scan_kernel(In in, int64_t n, int64_t *__restrict__ offsets, uint64_t *lookback,
     }
 }
 
+__global__ void __launch_bounds__(256)
+uniform_offsets_kernel(int64_t *__restrict__ offsets, int64_t nq, int64_t span,
+                       int32_t *max_out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nq;
+         i += (int64_t)gridDim.x * blockDim.x)
+        offsets[i] = i * span;
+    if (max_out && blockIdx.x == 0 && threadIdx.x == 0) *max_out = (int32_t)span;
+}
+
 template <class In>
 int launch_scan(In in, int64_t n, int64_t *offsets, int32_t *max_out, uint32_t *status,
                 void *ws, size_t ws_bytes, cudaStream_t stream) {
@@ -174,6 +183,15 @@ int knn_offsets(const int64_t *ks, int64_t k, int64_t n_leaves, int64_t nq, int6
                 int32_t *max_span, uint32_t *status, void *ws, size_t ws_bytes,
                 cudaStream_t stream) {
     if (n_leaves < 1) return LBVH_ERR_INVALID_ARG;
+    if (!ks) {
+        // uniform k: offsets[i] = i * min(k, n), no scan needed
+        if (!offsets || nq < 0 || k < 1) return LBVH_ERR_INVALID_ARG;
+        const int64_t span = k < n_leaves ? k : n_leaves;
+        unsigned g = div_up(nq + 1, 256);
+        g = g < kNumSMs * 16 ? g : kNumSMs * 16;
+        uniform_offsets_kernel<<<g, 256, 0, stream>>>(offsets, nq, span, max_span); count_launches(1);
+        return check_launch();
+    }
     return launch_scan(KnnSpanIn{ks, k, n_leaves}, nq, offsets, max_span, status, ws, ws_bytes,
                        stream);
 }

@@ -63,41 +63,63 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         return;
     }
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    // The reference pushes the passing children left, right and pops the
+    // right one next.  The node about to be popped is kept in a register
+    // instead (`node`), and only the left child goes to the stack; the
+    // overflow test still counts it as a stack entry, so the node sequence,
+    // hit order and stack-exhaustion behaviour are the reference's.
     int32_t stack[kStack];
-    int sp = 1;
-    stack[0] = 0;
+    int sp = 0;
+    int32_t node = 0;
     uint32_t fail = 0;
-    while (sp > 0) {
-        const int32_t node = stack[--sp];
+    while (true) {
         float4 a, b, c;
         int4 d;
         load_node(nodes, node, a, b, c, d);
         const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
         const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        int32_t next = -1;
         // left child, then right child (_kernels.py:212-225)
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-            const float dc = side == 0 ? dl : dr;
-            const int32_t link = side == 0 ? d.x : d.y;
-            if (dc <= r2) {
-                if (link < 0) {
-                    if (MODE == kBuffer && cnt >= cap) {
-                        fail = LBVH_FLAG_BUFFER_OVERFLOW;
-                        goto done;
-                    }
-                    if (MODE != kCount) out[base + cnt] = link & 0x7FFFFFFF;
-                    ++cnt;
-                } else {
-                    if (sp >= kStack) {
-                        fail = LBVH_FLAG_STACK_EXHAUSTED;
-                        goto done;
-                    }
-                    stack[sp++] = link;
+        if (dl <= r2) {
+            if (d.x < 0) {
+                if (MODE == kBuffer && cnt >= cap) {
+                    fail = LBVH_FLAG_BUFFER_OVERFLOW;
+                    break;
                 }
+                if (MODE != kCount) out[base + cnt] = d.x & 0x7FFFFFFF;
+                ++cnt;
+            } else {
+                if (sp >= kStack) {
+                    fail = LBVH_FLAG_STACK_EXHAUSTED;
+                    break;
+                }
+                stack[sp++] = d.x;
             }
         }
+        if (dr <= r2) {
+            if (d.y < 0) {
+                if (MODE == kBuffer && cnt >= cap) {
+                    fail = LBVH_FLAG_BUFFER_OVERFLOW;
+                    break;
+                }
+                if (MODE != kCount) out[base + cnt] = d.y & 0x7FFFFFFF;
+                ++cnt;
+            } else {
+                if (sp >= kStack) {
+                    fail = LBVH_FLAG_STACK_EXHAUSTED;
+                    break;
+                }
+                next = d.y;  // pushed and immediately popped
+            }
+        }
+        if (next >= 0) {
+            node = next;
+        } else if (sp > 0) {
+            node = stack[--sp];
+        } else {
+            break;
+        }
     }
-done:
     if (fail) atomicOr(status, fail);
     if (MODE != kFill) counts[q] = cnt;
 }
@@ -184,16 +206,17 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
     TopK<K> top;
     top.init(kk);
+    // Reference order: push farther, push nearer, pop nearer.  The nearer
+    // child is kept in a register (`node`) instead of a push/pop pair; its
+    // pop-time prune test (nd > worst) cannot fire because nothing is
+    // offered between its push and its pop.  The stack-capacity test still
+    // counts it, so exhaustion behaves exactly like the reference.
     int32_t stack_node[kStack];
     float stack_dist[kStack];
-    int sp = 1;
-    stack_node[0] = 0;
-    stack_dist[0] = 0.0f;  // never pruned: the list is empty at the first pop
+    int sp = 0;
+    int32_t node = 0;  // the root; never pruned (the list is empty)
     uint32_t fail = 0;
-    while (sp > 0) {
-        --sp;
-        const int32_t node = stack_node[sp];
-        if (stack_dist[sp] > top.worst()) continue;
+    while (true) {
         float4 a, b, c;
         int4 dd;
         load_node(nodes, node, a, b, c, dd);
@@ -203,25 +226,44 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         const bool left_near = dl <= dr;
         const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
         const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
-#pragma unroll
-        for (int pick = 0; pick < 2; ++pick) {
-            const int32_t link = pick == 0 ? fl : nl;
-            const float cd = pick == 0 ? fd : ndist;
-            if (cd > top.worst()) continue;
-            if (link < 0) {
-                top.offer(cd, link & 0x7FFFFFFF);
+        int32_t next = -1;
+        if (fd <= top.worst()) {
+            if (fl < 0) {
+                top.offer(fd, fl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
-                    goto done;
+                    break;
                 }
-                stack_node[sp] = link;
-                stack_dist[sp] = cd;
+                stack_node[sp] = fl;
+                stack_dist[sp] = fd;
                 ++sp;
             }
         }
+        if (ndist <= top.worst()) {
+            if (nl < 0) {
+                top.offer(ndist, nl & 0x7FFFFFFF);
+            } else {
+                if (sp >= kStack) {
+                    fail = LBVH_FLAG_STACK_EXHAUSTED;
+                    break;
+                }
+                next = nl;
+            }
+        }
+        if (next < 0) {
+            // pop until an entry survives the prune test (_kernels.py:364-368)
+            while (sp > 0) {
+                --sp;
+                if (!(stack_dist[sp] > top.worst())) {
+                    next = stack_node[sp];
+                    break;
+                }
+            }
+            if (next < 0) break;
+        }
+        node = next;
     }
-done:
     if (fail) atomicOr(status, fail);
     // Spans are written even after a failure; the driver raises anyway.
 #pragma unroll
