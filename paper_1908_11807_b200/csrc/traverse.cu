@@ -142,48 +142,50 @@ __device__ __forceinline__ bool lex_less(float d1, int32_t i1, float d2, int32_t
     return d1 < d2 || (d1 == d2 && i1 < i2);
 }
 
+// The k best candidates as 64-bit keys (dist^2 bits << 32 | ordinal + 1),
+// kept sorted ascending in registers.  Distances are >= +0 (or +inf), so the
+// key order is exactly the reference's lexicographic (dist^2, ordinal) order
+// (_kernels.py:293-296).  Slots [0, K-kk) hold 0-keys that rank before every
+// real candidate; slots [K-kk, K) start empty (all ones: dist bits are NaN, so
+// no distance compares greater and nothing is pruned until kk candidates
+// are in, matching "size == kk and nd > worst", _kernels.py:367,383).  The
+// k-th best is always slot K-1, a compile-time index, so nothing spills.
 template <int K>
 struct TopK {
-    float d[K];
-    int32_t id[K];
+    uint64_t key[K];
 
-    // Slots [0, K-kk) hold (-inf) sentinels that every real candidate ranks
-    // after, slots [K-kk, K) start empty (+inf, INT_MAX).  The current k-th
-    // best is always slot K-1, a compile-time index, so the whole list stays
-    // in registers.  An empty slot compares as +inf, so "full and nd > worst"
-    // (_kernels.py:367,383) is simply nd > d[K-1].
     __device__ __forceinline__ void init(int kk) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const bool pad = j < K - kk;
-            d[j] = pad ? -INFINITY : INFINITY;
-            id[j] = pad ? (j - K) : INT32_MAX;
-        }
+        for (int j = 0; j < K; ++j) key[j] = (j < K - kk) ? 0ull : ~0ull;
     }
-    __device__ __forceinline__ float worst() const { return d[K - 1]; }
+    __device__ __forceinline__ float worst() const {
+        return __uint_as_float((uint32_t)(key[K - 1] >> 32));
+    }
+    __device__ __forceinline__ static uint64_t make(float d, int32_t obj) {
+        return ((uint64_t)__float_as_uint(d) << 32) | (uint32_t)(obj + 1);
+    }
 
-    // Offer a candidate; kept iff it beats the current k-th best
-    // (_kernels.py:387-395).  Insertion keeps the list sorted.
+    // Keep the candidate iff it beats the current k-th best
+    // (_kernels.py:387-395); branch-free sorted insertion dropping slot K-1.
     __device__ __forceinline__ void offer(float cd, int32_t obj) {
-        if (!lex_less(cd, obj, d[K - 1], id[K - 1])) return;
-        bool placed = false;
+        const uint64_t c = make(cd, obj);
+        if (!(c < key[K - 1])) return;
+        bool lt[K];
 #pragma unroll
-        for (int j = K - 1; j > 0; --j) {
-            const bool shift = !placed && lex_less(cd, obj, d[j - 1], id[j - 1]);
-            const float nd = shift ? d[j - 1] : (placed ? d[j] : cd);
-            const int32_t ni = shift ? id[j - 1] : (placed ? id[j] : obj);
-            placed = placed || !shift;
-            d[j] = nd;
-            id[j] = ni;
-        }
-        if (!placed) {
-            d[0] = cd;
-            id[0] = obj;
-        }
+        for (int j = 0; j < K; ++j) lt[j] = key[j] < c;
+#pragma unroll
+        for (int j = K - 1; j > 0; --j) key[j] = lt[j] ? key[j] : (lt[j - 1] ? c : key[j - 1]);
+        key[0] = lt[0] ? key[0] : c;
+    }
+    __device__ __forceinline__ float dist(int j) const {
+        return __uint_as_float((uint32_t)(key[j] >> 32));
+    }
+    __device__ __forceinline__ int32_t ordinal(int j) const {
+        return (int32_t)((uint32_t)key[j]) - 1;
     }
 };
 
-template <int K>
+template <int K, bool REGNEXT>
 __global__ void __launch_bounds__(256)
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            const uint32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ offsets,
@@ -206,17 +208,29 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
     TopK<K> top;
     top.init(kk);
-    // Reference order: push farther, push nearer, pop nearer.  The nearer
-    // child is kept in a register (`node`) instead of a push/pop pair; its
-    // pop-time prune test (nd > worst) cannot fire because nothing is
-    // offered between its push and its pop.  The stack-capacity test still
-    // counts it, so exhaustion behaves exactly like the reference.
-    int32_t stack_node[kStack];
-    float stack_dist[kStack];
-    int sp = 0;
-    int32_t node = 0;  // the root; never pruned (the list is empty)
+    // Stack entries pack (dist^2 bits << 32 | node).  Reference order: push
+    // farther, push nearer, pop (_kernels.py:363-403).  With REGNEXT the
+    // nearer child stays in a register instead of a push/pop pair: its
+    // pop-time prune test cannot fire (nothing is offered between its push
+    // and pop) and the capacity test still counts it, so node order and
+    // stack exhaustion are the reference's either way.
+    uint64_t stack[kStack];
     uint32_t fail = 0;
+    int sp;
+    int32_t node = 0;  // the root; never pruned (the list is empty)
+    if (REGNEXT) {
+        sp = 0;
+    } else {
+        sp = 1;
+        stack[0] = 0;
+    }
     while (true) {
+        if (!REGNEXT) {
+            if (sp == 0) break;
+            const uint64_t e = stack[--sp];
+            if (__uint_as_float((uint32_t)(e >> 32)) > top.worst()) continue;
+            node = (int32_t)(uint32_t)e;
+        }
         float4 a, b, c;
         int4 dd;
         load_node(nodes, node, a, b, c, dd);
@@ -235,9 +249,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                stack_node[sp] = fl;
-                stack_dist[sp] = fd;
-                ++sp;
+                stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
             }
         }
         if (ndist <= top.worst()) {
@@ -248,21 +260,26 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                next = nl;
+                if (REGNEXT)
+                    next = nl;
+                else
+                    stack[sp++] = ((uint64_t)__float_as_uint(ndist) << 32) | (uint32_t)nl;
             }
         }
-        if (next < 0) {
-            // pop until an entry survives the prune test (_kernels.py:364-368)
-            while (sp > 0) {
-                --sp;
-                if (!(stack_dist[sp] > top.worst())) {
-                    next = stack_node[sp];
-                    break;
+        if (REGNEXT) {
+            if (next < 0) {
+                // pop until an entry survives the prune test (_kernels.py:364-368)
+                while (sp > 0) {
+                    const uint64_t e = stack[--sp];
+                    if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
+                        next = (int32_t)(uint32_t)e;
+                        break;
+                    }
                 }
+                if (next < 0) break;
             }
-            if (next < 0) break;
+            node = next;
         }
-        node = next;
     }
     if (fail) atomicOr(status, fail);
     // Spans are written even after a failure; the driver raises anyway.
@@ -270,8 +287,8 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     for (int j = 0; j < K; ++j) {
         if (j >= K - kk) {
             const int64_t o = base + (j - (K - kk));
-            out_idx[o] = top.id[j];
-            out_dist[o] = __fsqrt_rn(top.d[j]);
+            out_idx[o] = top.ordinal(j);
+            out_dist[o] = __fsqrt_rn(top.dist(j));
         }
     }
 }
@@ -461,10 +478,16 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order, int64_t
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     const unsigned g = div_up(nq, 256);
+    static const int variant = env_int("LBVH_KNN_VARIANT", 0);
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
-        knn_kernel<KV><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets, out_idx,     \
-                                              out_dist, status); count_launches(1);                            \
+        if (variant == 1)                                                                   \
+            knn_kernel<KV, true><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets,    \
+                                                        out_idx, out_dist, status);         \
+        else                                                                                \
+            knn_kernel<KV, false><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets,   \
+                                                         out_idx, out_dist, status);        \
+        count_launches(1);                                                                  \
         return check_launch();                                                              \
     }
     LBVH_KNN_CASE(4)
