@@ -241,7 +241,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
         const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
         int32_t next = -1;
-        if (fd <= top.worst()) {
+        if (!(fd > top.worst())) {  // NaN worst = list not full yet
             if (fl < 0) {
                 top.offer(fd, fl & 0x7FFFFFFF);
             } else {
@@ -252,7 +252,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
                 stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
             }
         }
-        if (ndist <= top.worst()) {
+        if (!(ndist > top.worst())) {
             if (nl < 0) {
                 top.offer(ndist, nl & 0x7FFFFFFF);
             } else {
