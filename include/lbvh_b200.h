@@ -53,7 +53,10 @@ enum {
  * leaf p at (n-1)+p.  `nodes` is the traversal layout: one 64-byte record
  * per internal node holding both child boxes and both child links (a leaf
  * child is stored as its object ordinal with bit 31 set).  `root_box` points
- * to 6 floats (min xyz, max xyz) of node 0.
+ * to 6 floats (min xyz, max xyz) of node 0.  `leaf_codes` (optional, n u32)
+ * are the Morton codes in leaf order, as produced by lbvh_build; when present
+ * (and the query codes are passed) kNN seeds its search radius from the
+ * leaves nearest in Morton order.
  */
 typedef struct lbvh_tree {
     int64_t n;
@@ -64,6 +67,7 @@ typedef struct lbvh_tree {
     const int32_t *leaf_obj;
     const void *nodes;
     const float *root_box;
+    const uint32_t *leaf_codes;
 } lbvh_tree;
 
 #define LBVH_NODE_BYTES 64
@@ -135,11 +139,12 @@ int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
 /* ---------------------------------------------------------------- query */
 
 /* query_sort_order(centers, scene)   replaces traversal.py:146-165.
- * order: nq u32 permutation.  scene_box: 6 floats DEVICE (tree root box). */
+ * order: nq u32 permutation.  scene_box: 6 floats DEVICE (tree root box).
+ * sorted_codes (optional): the queries' Morton codes in `order` order. */
 size_t lbvh_query_workspace_bytes(int64_t nq);
 int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box,
-                     uint32_t *order, void *workspace, size_t workspace_bytes,
-                     void *stream);
+                     uint32_t *order, uint32_t *sorted_codes, void *workspace,
+                     size_t workspace_bytes, void *stream);
 
 /* Finite check of nq x 3 query centers and (optional) radii >= 0. */
 int lbvh_check_queries(const float *centers, int64_t nq, const float *radii,
@@ -185,10 +190,14 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
                      size_t workspace_bytes, void *stream);
 
 /* knn_pass  replaces _kernels.py:328-414 (query_knn, traversal.py:251-272).
- * max_span: host upper bound of min(k_q, n) (selects the kernel variant). */
+ * max_span: host upper bound of min(k_q, n) (selects the kernel variant).
+ * query_codes (optional): Morton codes of the queries in `order` order (from
+ * lbvh_query_order); with tree->leaf_codes they enable the search-radius
+ * seed, which never changes results. */
 int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
-             int64_t nq, const int64_t *offsets, int64_t max_span, int32_t *out_idx,
-             float *out_dist, uint32_t *status, void *stream);
+             const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
+             int64_t max_span, int32_t *out_idx, float *out_dist, uint32_t *status,
+             void *stream);
 
 #ifdef __cplusplus
 }

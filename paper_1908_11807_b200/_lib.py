@@ -42,7 +42,7 @@ class CTree(ctypes.Structure):
                 ("node_mins", ctypes.c_void_p), ("node_maxs", ctypes.c_void_p),
                 ("left", ctypes.c_void_p), ("right", ctypes.c_void_p),
                 ("leaf_obj", ctypes.c_void_p), ("nodes", ctypes.c_void_p),
-                ("root_box", ctypes.c_void_p)]
+                ("root_box", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p)]
 
 
 _SIGS = {
@@ -68,7 +68,8 @@ _SIGS = {
     "lbvh_pack": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 4, ctypes.c_int),
     "lbvh_unpack_boxes": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 3, ctypes.c_int),
     "lbvh_query_order": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
-                          ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+                         ctypes.c_int),
     "lbvh_check_queries": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                             ctypes.c_void_p], ctypes.c_int),
     "lbvh_spatial_count": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
@@ -88,9 +89,9 @@ _SIGS = {
     "lbvh_knn_offsets": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                           ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
-    "lbvh_knn": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
-                  ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
-                  ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_knn": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                  ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
 }
 
 

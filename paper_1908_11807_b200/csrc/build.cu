@@ -484,13 +484,13 @@ size_t query_workspace_bytes(int64_t nq) {
 }
 
 int query_order(const float *centers, int64_t nq, const float *scene, uint32_t *order,
-                void *ws, size_t ws_bytes, cudaStream_t stream) {
+                uint32_t *sorted_codes, void *ws, size_t ws_bytes, cudaStream_t stream) {
     if (nq < 0 || (nq > 0 && (!centers || !order)) || !scene) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     if (ws_bytes < query_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
     Carve c(ws, ws_bytes);
-    uint32_t *codes = c.take<uint32_t>(nq);
+    uint32_t *codes = sorted_codes ? sorted_codes : c.take<uint32_t>(nq);
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
     morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq, scene, codes,
                                                              order); count_launches(1);

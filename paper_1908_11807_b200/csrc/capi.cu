@@ -44,7 +44,8 @@ int unpack_boxes(const lbvh_tree *, float *, float *, cudaStream_t);
 int morton_codes_f64(const double *, int64_t, const double *, const double *, uint32_t *,
                      cudaStream_t);
 size_t query_workspace_bytes(int64_t nq);
-int query_order(const float *, int64_t, const float *, uint32_t *, void *, size_t, cudaStream_t);
+int query_order(const float *, int64_t, const float *, uint32_t *, uint32_t *, void *, size_t,
+                cudaStream_t);
 int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
                   int64_t, int32_t *, uint32_t *, cudaStream_t);
 int spatial_fill(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
@@ -55,8 +56,8 @@ int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t,
             cudaStream_t);
 int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
                 void *, size_t, cudaStream_t);
-int knn(const lbvh_tree *, const float *, const uint32_t *, int64_t, const int64_t *, int64_t,
-        int32_t *, float *, uint32_t *, cudaStream_t);
+int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
+        const int64_t *, int64_t, int32_t *, float *, uint32_t *, cudaStream_t);
 int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
 
 }  // namespace lbvh
@@ -131,8 +132,8 @@ int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
 }
 
 int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box, uint32_t *order,
-                     void *ws, size_t ws_bytes, void *stream) {
-    return query_order(centers, nq, scene_box, order, ws, ws_bytes, S(stream));
+                     uint32_t *sorted_codes, void *ws, size_t ws_bytes, void *stream) {
+    return query_order(centers, nq, scene_box, order, sorted_codes, ws, ws_bytes, S(stream));
 }
 
 int lbvh_check_queries(const float *centers, int64_t nq, const float *radii, uint32_t *status,
@@ -176,11 +177,11 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
     return knn_offsets(ks, k, n, nq, offsets, max_span, status, ws, ws_bytes, S(stream));
 }
 
-int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order, int64_t nq,
-             const int64_t *offsets, int64_t max_span, int32_t *out_idx, float *out_dist,
-             uint32_t *status, void *stream) {
-    return knn(tree, centers, order, nq, offsets, max_span, out_idx, out_dist, status,
-               S(stream));
+int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
+             const uint32_t *query_codes, int64_t nq, const int64_t *offsets, int64_t max_span,
+             int32_t *out_idx, float *out_dist, uint32_t *status, void *stream) {
+    return knn(tree, centers, order, query_codes, nq, offsets, max_span, out_idx, out_dist,
+               status, S(stream));
 }
 
 }  // extern "C"

@@ -154,9 +154,18 @@ template <int K>
 struct TopK {
     uint64_t key[K];
 
-    __device__ __forceinline__ void init(int kk) {
+    // `bound` (optional, may be NaN = none): a distance^2 known to have at
+    // least kk candidates at or below it.  Empty slots then carry
+    // (bound, 0xFFFFFFFF) -- a virtual candidate every real one at the same
+    // distance beats -- so nodes farther than the bound are pruned from the
+    // start and leaves beyond it are never offered.  All virtual slots are
+    // displaced by real candidates by the end, so results are unchanged.
+    __device__ __forceinline__ void init(int kk, float bound) {
+        const uint64_t empty = isnan(bound)
+                                   ? ~0ull
+                                   : (((uint64_t)__float_as_uint(bound) << 32) | 0xFFFFFFFFull);
 #pragma unroll
-        for (int j = 0; j < K; ++j) key[j] = (j < K - kk) ? 0ull : ~0ull;
+        for (int j = 0; j < K; ++j) key[j] = (j < K - kk) ? 0ull : empty;
     }
     __device__ __forceinline__ float worst() const {
         return __uint_as_float((uint32_t)(key[K - 1] >> 32));
@@ -185,11 +194,55 @@ struct TopK {
     }
 };
 
+// Search-radius seed for one query: the kk-th smallest distance^2 among the
+// 2*kk leaves that neighbour the query's Morton code in leaf order (a real
+// upper bound of the true k-th distance).  Leaves are found by a lower_bound
+// over the build's sorted leaf codes.
+template <int K>
+__device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, int kk,
+                                            float px, float py, float pz) {
+    const int64_t n = t.n;
+    const uint32_t *__restrict__ codes = t.leaf_codes;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(codes + mid) < qcode)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    const int64_t w = 2 * (int64_t)kk;
+    int64_t w0 = lo - kk;
+    w0 = w0 < 0 ? 0 : w0;
+    w0 = (w0 + w > n) ? (n - w > 0 ? n - w : 0) : w0;
+    const int64_t w1 = (w0 + w < n) ? w0 + w : n;
+    float best[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) best[j] = (j < K - kk) ? -INFINITY : INFINITY;
+    const float *__restrict__ mn = t.node_mins + 3 * (n - 1);
+    const float *__restrict__ mx = t.node_maxs + 3 * (n - 1);
+    for (int64_t p = w0; p < w1; ++p) {
+        const float d = box_dist_sq(px, py, pz, __ldg(mn + 3 * p), __ldg(mn + 3 * p + 1),
+                                    __ldg(mn + 3 * p + 2), __ldg(mx + 3 * p),
+                                    __ldg(mx + 3 * p + 1), __ldg(mx + 3 * p + 2));
+        if (d < best[K - 1]) {
+            bool lt[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) lt[j] = best[j] <= d;
+#pragma unroll
+            for (int j = K - 1; j > 0; --j) best[j] = lt[j] ? best[j] : (lt[j - 1] ? d : best[j - 1]);
+            best[0] = lt[0] ? best[0] : d;
+        }
+    }
+    return best[K - 1];
+}
+
 template <int K, bool REGNEXT>
 __global__ void __launch_bounds__(256)
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
-           const uint32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ offsets,
-           int32_t *__restrict__ out_idx, float *__restrict__ out_dist, uint32_t *status) {
+           const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
+           const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
+           float *__restrict__ out_dist, uint32_t *status) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
@@ -207,7 +260,10 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     }
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
     TopK<K> top;
-    top.init(kk);
+    const float bound = (qcodes && t.leaf_codes)
+                            ? seed_bound<K>(t, __ldg(qcodes + s), kk, px, py, pz)
+                            : __int_as_float(0x7FFFFFFF);
+    top.init(kk, bound);
     // Stack entries pack (dist^2 bits << 32 | node).  Reference order: push
     // farther, push nearer, pop (_kernels.py:363-403).  With REGNEXT the
     // nearer child stays in a register instead of a push/pop pair: its
@@ -470,23 +526,24 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
     return check_launch();
 }
 
-int knn(const lbvh_tree *t, const float *centers, const uint32_t *order, int64_t nq,
-        const int64_t *offsets, int64_t max_span, int32_t *out_idx, float *out_dist,
-        uint32_t *status, cudaStream_t stream) {
+int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
+        const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
+        int32_t *out_idx, float *out_dist, uint32_t *status, cudaStream_t stream) {
     if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0 || max_span <= 0) return LBVH_OK;
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     const unsigned g = div_up(nq, 256);
     static const int variant = env_int("LBVH_KNN_VARIANT", 0);
+    if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
         if (variant == 1)                                                                   \
-            knn_kernel<KV, true><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets,    \
-                                                        out_idx, out_dist, status);         \
+            knn_kernel<KV, true><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,     \
+                                                        offsets, out_idx, out_dist, status); \
         else                                                                                \
-            knn_kernel<KV, false><<<g, 256, 0, stream>>>(*t, centers, order, nq, offsets,   \
-                                                         out_idx, out_dist, status);        \
+            knn_kernel<KV, false><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,    \
+                                                         offsets, out_idx, out_dist, status); \
         count_launches(1);                                                                  \
         return check_launch();                                                              \
     }

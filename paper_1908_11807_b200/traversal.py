@@ -258,17 +258,19 @@ def _empty_result(host: bool, knn: bool) -> ResultSet:
                               torch.empty(0, dtype=torch.float32, device=dev) if knn else None)
 
 
-def _order(tree: Bvh, b: _Batch, sort_queries: bool):
-    """Device Morton order of the batch on the tree's scene grid (or None)."""
+def _order(tree: Bvh, b: _Batch, sort_queries: bool, with_codes: bool = False):
+    """Device Morton order of the batch on the tree's scene grid (or None);
+    with ``with_codes`` also the sorted query codes (kNN radius seed)."""
     if not sort_queries or b.nq <= 1:
-        return None
+        return (None, None) if with_codes else None
     l = _lib.lib()
     order = dv.empty(b.nq, torch.int32)
+    codes = dv.empty(b.nq, torch.int32) if with_codes else None
     ws = dv.workspace(l.lbvh_query_workspace_bytes(b.nq))
     _lib.check(l.lbvh_query_order(dv.ptr(b.centers), b.nq,
                                   dv.ptr(tree.device_arrays()["root_box"]), dv.ptr(order),
-                                  dv.ptr(ws), ws.numel(), dv.stream()))
-    return order
+                                  dv.ptr(codes), dv.ptr(ws), ws.numel(), dv.stream()))
+    return (order, codes) if with_codes else order
 
 
 def _finish(host: bool, status: dv.Status, *arrays):
@@ -401,13 +403,13 @@ def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -
         flags, mxh, tot = dv.d2h_many(status.dev, mx, offsets[nq:])
         _raise_flags(int(flags[0]) & 0xFFFFFFFF)
         max_span, total = int(mxh[0]), int(tot[0])
-    order = _order(tree, b, sort_queries)
+    order, qcodes = _order(tree, b, sort_queries, with_codes=True)
     out_idx = dv.empty(total, torch.int32)
     out_dist = dv.empty(total, torch.float32)
     ct = tree.ctree()
     _lib.check(_launch("knn", lambda: l.lbvh_knn(
-        ct, dv.ptr(b.centers), dv.ptr(order), nq, dv.ptr(offsets), max_span, dv.ptr(out_idx),
-        dv.ptr(out_dist), status.ptr, st)))
+        ct, dv.ptr(b.centers), dv.ptr(order), dv.ptr(qcodes), nq, dv.ptr(offsets), max_span,
+        dv.ptr(out_idx), dv.ptr(out_dist), status.ptr, st)))
     offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
     return ResultSet._trusted(offsets, out_idx, out_dist)
 

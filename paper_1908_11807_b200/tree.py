@@ -170,7 +170,7 @@ class Bvh:
 def _ctree(d: dict, n: int) -> _lib.CTree:
     return _lib.CTree(n, dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]),
                       dv.ptr(d.get("left")), dv.ptr(d.get("right")), dv.ptr(d["leaf_obj"]),
-                      dv.ptr(d["nodes"]), dv.ptr(d["root_box"]))
+                      dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), dv.ptr(d.get("leaf_codes")))
 
 
 def _device_boxes(boxes):
@@ -202,13 +202,15 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> 
         "leaf_obj": dv.empty(n, i32),
         "root_box": dv.empty(6, f32),
         "nodes": dv.empty(max(n - 1, 1) * _lib.NODE_BYTES, torch.uint8),
+        "leaf_codes": dv.empty(n, i32),  # Morton codes in leaf order (kNN seed)
     }
     ws = dv.workspace(l.lbvh_build_workspace_bytes(n))
     status = dv.Status()
     _lib.check(_launch("build", lambda: l.lbvh_build(dv.ptr(mins), dv.ptr(maxs), n, dv.ptr(ws), ws.numel(),
                             dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]), dv.ptr(d["left"]),
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
-                            dv.ptr(d["nodes"]), None, status.ptr, dv.stream())))
+                            dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), status.ptr,
+                            dv.stream())))
     if check:
         flags = status.read()
         if flags & _lib.FLAG_NONFINITE:
