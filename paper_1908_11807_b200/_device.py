@@ -59,6 +59,22 @@ def h2d(arr: np.ndarray) -> torch.Tensor:
     return t.to(device(), non_blocking=True)
 
 
+def as_tensor(arr: np.ndarray) -> torch.Tensor:
+    """Zero-copy host tensor view of a numpy array (read-only views allowed)."""
+    arr = np.ascontiguousarray(arr)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(arr)
+
+
+def is_pinned(arr: np.ndarray) -> bool:
+    """True when the array's memory is page-locked (cudaHostAlloc'ed)."""
+    try:
+        return bool(as_tensor(arr).is_pinned())
+    except Exception:
+        return False
+
+
 def pinned(shape, dtype) -> torch.Tensor:
     return torch.empty(shape, dtype=dtype, pin_memory=True)
 

@@ -37,6 +37,12 @@ __all__ = ["SpatialQuery", "KnnQuery", "ResultSet", "STACK_CAPACITY", "traverse_
 
 STACK_CAPACITY = _lib.STACK_CAPACITY
 
+# Host batches at least this large, from pinned memory, run as a chunked
+# pipeline: H2D of chunk i+1, compute of chunk i and D2H of chunk i-1
+# overlap on three streams (copy engines both ways + SMs).
+_PIPELINE_MIN = 1 << 20
+_PIPELINE_CHUNK = 1 << 20
+
 # Benchmark hook: when set to an object with ``wrap(name, call)``, the main
 # traversal launches are bracketed by CUDA events on the launching stream.
 KERNEL_TIMER = None
@@ -140,10 +146,10 @@ class ResultSet:
 class _Batch:
     """Query batch staged on the device."""
 
-    __slots__ = ("centers", "radii", "radius", "ks", "k", "nq", "host")
+    __slots__ = ("centers", "radii", "radius", "ks", "k", "nq", "host", "host_centers")
 
     def __init__(self):
-        self.radii = self.ks = None
+        self.radii = self.ks = self.centers = self.host_centers = None
         self.radius = 0.0
         self.k = 0
 
@@ -228,11 +234,15 @@ def _knn_batch(queries) -> _Batch:
     b.host = True
     b.nq = int(centers.shape[0])
     if b.nq:
-        b.centers = dv.h2d(centers)
         if ka.ndim == 0:
             b.k = int(ka)
+            if b.nq >= _PIPELINE_MIN and dv.is_pinned(centers):
+                # large pinned batch: H2D is chunked inside the pipelined path
+                b.host_centers = centers
+                return b
         else:
             b.ks = dv.h2d(ka)
+        b.centers = dv.h2d(centers)
     return b
 
 
@@ -383,6 +393,8 @@ def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -
     b = _knn_batch(queries)
     if b.nq == 0:
         return _empty_result(b.host, knn=True)
+    if b.host_centers is not None:
+        return _knn_pipelined(tree, b, sort_queries)
     l = _lib.lib()
     st = dv.stream()
     nq, n = b.nq, tree.leaf_count
@@ -412,6 +424,73 @@ def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -
         dv.ptr(out_idx), dv.ptr(out_dist), status.ptr, st)))
     offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
     return ResultSet._trusted(offsets, out_idx, out_dist)
+
+
+def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet:
+    """Host kNN batch as an H2D / compute / D2H pipeline over query chunks.
+
+    Chunk results are identical to the one-shot path: every query's span is
+    independent and sits at its global offset; only the Morton pre-sort is
+    per chunk, and query order never changes results (traversal.py:146-165).
+    """
+    l = _lib.lib()
+    dev = dv.device()
+    nq, n = b.nq, tree.leaf_count
+    span = min(b.k, n)
+    total = span * nq
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    status = dv.Status()
+    host_c = dv.as_tensor(b.host_centers)
+    dev_c = torch.empty((nq, 3), dtype=torch.float32, device=dev)
+    offsets = dv.empty(nq + 1, torch.int64)
+    out_idx = dv.empty(total, torch.int32)
+    out_dist = dv.empty(total, torch.float32)
+    h_off = dv.pinned(nq + 1, torch.int64)
+    h_idx = dv.pinned(total, torch.int32)
+    h_dist = dv.pinned(total, torch.float32)
+    chunk = _PIPELINE_CHUNK
+    order = dv.empty(chunk, torch.int32) if sort_queries else None
+    qcodes = dv.empty(chunk, torch.int32) if sort_queries else None
+    ws = dv.workspace(max(l.lbvh_query_workspace_bytes(chunk), l.lbvh_scan_workspace_bytes(nq)))
+    _lib.check(l.lbvh_knn_offsets(None, b.k, n, nq, dv.ptr(offsets), None, status.ptr,
+                                  dv.ptr(ws), ws.numel(), comp.cuda_stream))
+    ev = torch.cuda.Event()
+    ev.record(comp)
+    s_out.wait_event(ev)
+    with torch.cuda.stream(s_out):
+        h_off.copy_(offsets, non_blocking=True)
+    ct = tree.ctree()
+    root_box = dv.ptr(tree.device_arrays()["root_box"])
+    c_ptr, o_ptr = dv.ptr(dev_c), dv.ptr(offsets)
+    for c0 in range(0, nq, chunk):
+        c1 = min(nq, c0 + chunk)
+        m = c1 - c0
+        e_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            dev_c[c0:c1].copy_(host_c[c0:c1], non_blocking=True)
+            e_in.record(s_in)
+        comp.wait_event(e_in)
+        cc = c_ptr + 12 * c0
+        _lib.check(l.lbvh_check_queries(cc, m, None, status.ptr, comp.cuda_stream))
+        srt = sort_queries and m > 1
+        if srt:
+            _lib.check(l.lbvh_query_order(cc, m, root_box, dv.ptr(order), dv.ptr(qcodes),
+                                          dv.ptr(ws), ws.numel(), comp.cuda_stream))
+        _lib.check(_launch("knn", lambda: l.lbvh_knn(
+            ct, cc, dv.ptr(order) if srt else None, dv.ptr(qcodes) if srt else None, m,
+            o_ptr + 8 * c0, span, dv.ptr(out_idx), dv.ptr(out_dist), status.ptr,
+            comp.cuda_stream)))
+        e_c = torch.cuda.Event()
+        e_c.record(comp)
+        s_out.wait_event(e_c)
+        with torch.cuda.stream(s_out):
+            h_idx[c0 * span:c1 * span].copy_(out_idx[c0 * span:c1 * span], non_blocking=True)
+            h_dist[c0 * span:c1 * span].copy_(out_dist[c0 * span:c1 * span], non_blocking=True)
+    comp.wait_stream(s_out)
+    comp.wait_stream(s_in)
+    _raise_flags(status.read())  # synchronises the current stream
+    return ResultSet._trusted(h_off.numpy(), h_idx.numpy(), h_dist.numpy())
 
 
 def query_sort_order(centers, scene: Box | tuple) -> np.ndarray:

@@ -196,3 +196,26 @@ def test_large_scale_properties_1e7():
     rk = lb.query_knn(t, (q, 10))
     ko, ki, kd = oracle.query_knn(ref, q, 10)
     assert np.array_equal(rk.indices, ki) and rk.distances.tobytes() == kd.tobytes()
+
+
+def test_pipelined_host_knn_equals_device_path():
+    """Large pinned host batches take the chunked H2D/compute/D2H pipeline;
+    results must equal the one-shot device path and the oracle."""
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 400_000, 0))
+    q = datasets.generate(datasets.CloudSpec("sphere", "filled", (1 << 20) + 12345, 1))
+    t = lb.build(pts)
+    pin = torch.empty(q.shape, dtype=torch.float32, pin_memory=True)
+    pin.numpy()[:] = q
+    from paper_1908_11807_b200 import _device
+    assert _device.is_pinned(pin.numpy())
+    for k in (1, 10):
+        host = lb.query_knn(t, (pin.numpy(), k))
+        dev = lb.query_knn(t, (torch.from_numpy(q).cuda(), k)).to_host()
+        assert np.array_equal(host.offsets, dev.offsets)
+        assert np.array_equal(host.indices, dev.indices)
+        assert host.distances.tobytes() == dev.distances.tobytes()
+    ref = oracle.build(pts)
+    ko, ki, kd = oracle.query_knn(ref, q[-5000:], 10)
+    assert np.array_equal(host.indices[-50000:], ki)
+    unsorted = lb.query_knn(t, (pin.numpy(), 10), sort_queries=False)
+    assert np.array_equal(unsorted.indices, host.indices)
