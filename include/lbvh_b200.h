@@ -152,17 +152,22 @@ int lbvh_check_queries(const float *centers, int64_t nq, const float *radii,
 
 /* spatial_pass(store=False)  replaces _kernels.py:179-228 (count pass of
  * query_spatial_2p, traversal.py:197-201).  radii may be NULL -> radius.
- * order may be NULL -> identity.  counts: nq i32. */
+ * order may be NULL -> identity.  counts: nq i32.  buf (optional, nq x
+ * buffer_size i32): the first buffer_size hits of every query are kept in
+ * its row in traversal order, so the fill pass only has to revisit queries
+ * whose count exceeds buffer_size (see lbvh_spatial_fill / lbvh_compact). */
 int lbvh_spatial_count(const lbvh_tree *tree, const float *centers, const float *radii,
                        float radius, const uint32_t *order, int64_t nq, int32_t *counts,
-                       uint32_t *status, void *stream);
+                       int32_t *buf, int64_t buffer_size, uint32_t *status, void *stream);
 
 /* spatial_pass(store=True)  replaces _kernels.py:179-228 (fill pass,
- * traversal.py:205-209); writes out[offsets[q] ...]. */
+ * traversal.py:205-209); writes out[offsets[q] ...].  skip_counts
+ * (optional): counts of a buffered count pass; queries with count <=
+ * buffer_size are skipped (lbvh_compact copies their rows). */
 int lbvh_spatial_fill(const lbvh_tree *tree, const float *centers, const float *radii,
                       float radius, const uint32_t *order, int64_t nq,
-                      const int64_t *offsets, int32_t *out, uint32_t *status,
-                      void *stream);
+                      const int64_t *offsets, int32_t *out, const int32_t *skip_counts,
+                      int64_t buffer_size, uint32_t *status, void *stream);
 
 /* _exclusive_scan   replaces traversal.py:173-176: offsets[0]=0,
  * offsets[i+1] = sum(counts[0..i]); offsets is nq+1 i64.  Also copies the
@@ -177,7 +182,8 @@ int lbvh_spatial_1p(const lbvh_tree *tree, const float *centers, const float *ra
                     float radius, const uint32_t *order, int64_t nq, int32_t *buf,
                     int64_t buffer_size, int32_t *counts, uint32_t *status, void *stream);
 
-/* compact_rows  replaces _kernels.py:285-290. */
+/* compact_rows  replaces _kernels.py:285-290.  Rows with counts[q] >
+ * buffer_size are skipped (they did not fit; see lbvh_spatial_fill). */
 int lbvh_compact(const int32_t *buf, int64_t buffer_size, const int32_t *counts,
                  const int64_t *offsets, int64_t nq, int32_t *out, void *stream);
 

@@ -74,10 +74,12 @@ _SIGS = {
                             ctypes.c_void_p], ctypes.c_int),
     "lbvh_spatial_count": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
                             ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
-                            ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+                            ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p],
+                           ctypes.c_int),
     "lbvh_spatial_fill": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
-                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                           ctypes.c_void_p], ctypes.c_int),
     "lbvh_exclusive_scan": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                              ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "lbvh_spatial_1p": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,

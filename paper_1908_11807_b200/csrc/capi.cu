@@ -47,9 +47,10 @@ size_t query_workspace_bytes(int64_t nq);
 int query_order(const float *, int64_t, const float *, uint32_t *, uint32_t *, void *, size_t,
                 cudaStream_t);
 int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
-                  int64_t, int32_t *, uint32_t *, cudaStream_t);
+                  int64_t, int32_t *, int32_t *, int64_t, uint32_t *, cudaStream_t);
 int spatial_fill(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
-                 int64_t, const int64_t *, int32_t *, uint32_t *, cudaStream_t);
+                 int64_t, const int64_t *, int32_t *, const int32_t *, int64_t, uint32_t *,
+                 cudaStream_t);
 int spatial_1p(const lbvh_tree *, const float *, const float *, float, const uint32_t *, int64_t,
                int32_t *, int64_t, int32_t *, uint32_t *, cudaStream_t);
 int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t, int32_t *,
@@ -143,15 +144,17 @@ int lbvh_check_queries(const float *centers, int64_t nq, const float *radii, uin
 
 int lbvh_spatial_count(const lbvh_tree *tree, const float *centers, const float *radii,
                        float radius, const uint32_t *order, int64_t nq, int32_t *counts,
-                       uint32_t *status, void *stream) {
-    return spatial_count(tree, centers, radii, radius, order, nq, counts, status, S(stream));
+                       int32_t *buf, int64_t buffer_size, uint32_t *status, void *stream) {
+    return spatial_count(tree, centers, radii, radius, order, nq, counts, buf, buffer_size,
+                         status, S(stream));
 }
 
 int lbvh_spatial_fill(const lbvh_tree *tree, const float *centers, const float *radii,
                       float radius, const uint32_t *order, int64_t nq, const int64_t *offsets,
-                      int32_t *out, uint32_t *status, void *stream) {
-    return spatial_fill(tree, centers, radii, radius, order, nq, offsets, out, status,
-                        S(stream));
+                      int32_t *out, const int32_t *skip_counts, int64_t buffer_size,
+                      uint32_t *status, void *stream) {
+    return spatial_fill(tree, centers, radii, radius, order, nq, offsets, out, skip_counts,
+                        buffer_size, status, S(stream));
 }
 
 int lbvh_exclusive_scan(const int32_t *counts, int64_t nq, int64_t *offsets, void *ws,

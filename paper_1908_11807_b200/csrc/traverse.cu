@@ -25,7 +25,12 @@
 namespace lbvh {
 namespace {
 
-enum SpatialMode { kCount = 0, kFill = 1, kBuffer = 2 };
+enum SpatialMode {
+    kCount = 0,     // count only                        (spatial_pass store=False)
+    kFill = 1,      // write at offsets[q]               (spatial_pass store=True)
+    kBuffer = 2,    // 1P: row of `cap`, abort on overflow (spatial_pass_buffered)
+    kCountBuf = 3,  // count all, keep the first `cap` hits in the row
+};
 
 __device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, int32_t id,
                                           float4 &a, float4 &b, float4 &c, int4 &d) {
@@ -36,29 +41,43 @@ __device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, 
     d = __ldg(&p->d);
 }
 
+// One hit (leaf ordinal `obj`); returns false when the 1P row overflows.
+template <int MODE>
+__device__ __forceinline__ bool emit(int32_t *__restrict__ out, int64_t base, int32_t &cnt,
+                                     int64_t cap, int32_t obj) {
+    if (MODE == kBuffer && cnt >= cap) return false;
+    if (MODE == kFill || MODE == kBuffer) out[base + cnt] = obj;
+    if (MODE == kCountBuf && cnt < cap) out[base + cnt] = obj;
+    ++cnt;
+    return true;
+}
+
+// `skip` (kFill only, optional): counts of a kCountBuf pass; queries whose
+// hits all fit in its rows (count <= cap) are skipped -- the compaction
+// kernel copies those.
 template <int MODE>
 __global__ void __launch_bounds__(256)
 spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
                const float *__restrict__ radii, float radius, const uint32_t *__restrict__ order,
                int64_t nq, int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
-               int32_t *__restrict__ out, int64_t cap, uint32_t *status) {
+               int32_t *__restrict__ out, int64_t cap, const int32_t *__restrict__ skip,
+               uint32_t *status) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    if (MODE == kFill && skip && __ldg(skip + q) <= cap) return;
     const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
                 pz = __ldg(centers + 3 * q + 2);
     const float r = radii ? __ldg(radii + q) : radius;
     const float r2 = __fmul_rn(r, r);
     int64_t base = 0;
     if (MODE == kFill) base = __ldg(offsets + q);
-    if (MODE == kBuffer) base = q * cap;
+    if (MODE == kBuffer || MODE == kCountBuf) base = q * cap;
     int32_t cnt = 0;
     if (t.n == 1) {
         const float *bx = t.root_box;
-        if (box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]) <= r2) {
-            if (MODE != kCount) out[base] = __ldg(t.leaf_obj);
-            cnt = 1;
-        }
+        if (box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]) <= r2)
+            emit<MODE>(out, base, cnt, cap, __ldg(t.leaf_obj));
         if (MODE != kFill) counts[q] = cnt;
         return;
     }
@@ -82,12 +101,10 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         // left child, then right child (_kernels.py:212-225)
         if (dl <= r2) {
             if (d.x < 0) {
-                if (MODE == kBuffer && cnt >= cap) {
+                if (!emit<MODE>(out, base, cnt, cap, d.x & 0x7FFFFFFF)) {
                     fail = LBVH_FLAG_BUFFER_OVERFLOW;
                     break;
                 }
-                if (MODE != kCount) out[base + cnt] = d.x & 0x7FFFFFFF;
-                ++cnt;
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
@@ -98,12 +115,10 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         }
         if (dr <= r2) {
             if (d.y < 0) {
-                if (MODE == kBuffer && cnt >= cap) {
+                if (!emit<MODE>(out, base, cnt, cap, d.y & 0x7FFFFFFF)) {
                     fail = LBVH_FLAG_BUFFER_OVERFLOW;
                     break;
                 }
-                if (MODE != kCount) out[base + cnt] = d.y & 0x7FFFFFFF;
-                ++cnt;
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
@@ -132,6 +147,7 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
     const int lane = threadIdx.x & 31;
     if (warp >= nq) return;
     const int32_t cnt = __ldg(counts + warp);
+    if (cnt > cap) return;  // did not fit its row: written by the overflow fill pass
     const int64_t dst = __ldg(offsets + warp);
     const int32_t *row = buf + warp * cap;
     for (int j = lane; j < cnt; j += 32) out[dst + j] = __ldcs(row + j);
@@ -481,7 +497,8 @@ bool tree_ok(const lbvh_tree *t) {
 template <int MODE>
 int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii, float radius,
                    const uint32_t *order, int64_t nq, int32_t *counts, const int64_t *offsets,
-                   int32_t *out, int64_t cap, uint32_t *status, cudaStream_t stream) {
+                   int32_t *out, int64_t cap, const int32_t *skip, uint32_t *status,
+                   cudaStream_t stream) {
     if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (!centers) return LBVH_ERR_INVALID_ARG;
@@ -489,24 +506,31 @@ int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii,
     if (MODE == kFill && !offsets) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     spatial_kernel<MODE><<<div_up(nq, 256), 256, 0, stream>>>(
-        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, status); count_launches(1);
+        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, skip, status);
+    count_launches(1);
     return check_launch();
 }
 
 }  // namespace
 
 int spatial_count(const lbvh_tree *t, const float *centers, const float *radii, float radius,
-                  const uint32_t *order, int64_t nq, int32_t *counts, uint32_t *status,
-                  cudaStream_t stream) {
+                  const uint32_t *order, int64_t nq, int32_t *counts, int32_t *buf, int64_t cap,
+                  uint32_t *status, cudaStream_t stream) {
+    if (buf) {
+        if (cap < 1) return LBVH_ERR_INVALID_ARG;
+        return launch_spatial<kCountBuf>(t, centers, radii, radius, order, nq, counts, nullptr,
+                                         buf, cap, nullptr, status, stream);
+    }
     return launch_spatial<kCount>(t, centers, radii, radius, order, nq, counts, nullptr,
-                                  nullptr, 0, status, stream);
+                                  nullptr, 0, nullptr, status, stream);
 }
 
 int spatial_fill(const lbvh_tree *t, const float *centers, const float *radii, float radius,
                  const uint32_t *order, int64_t nq, const int64_t *offsets, int32_t *out,
-                 uint32_t *status, cudaStream_t stream) {
-    return launch_spatial<kFill>(t, centers, radii, radius, order, nq, nullptr, offsets, out, 0,
-                                 status, stream);
+                 const int32_t *skip_counts, int64_t cap, uint32_t *status,
+                 cudaStream_t stream) {
+    return launch_spatial<kFill>(t, centers, radii, radius, order, nq, nullptr, offsets, out,
+                                 skip_counts ? cap : 0, skip_counts, status, stream);
 }
 
 int spatial_1p(const lbvh_tree *t, const float *centers, const float *radii, float radius,
@@ -514,7 +538,7 @@ int spatial_1p(const lbvh_tree *t, const float *centers, const float *radii, flo
                uint32_t *status, cudaStream_t stream) {
     if (cap < 1 || (nq > 0 && !buf)) return LBVH_ERR_INVALID_ARG;
     return launch_spatial<kBuffer>(t, centers, radii, radius, order, nq, counts, nullptr, buf,
-                                   cap, status, stream);
+                                   cap, nullptr, status, stream);
 }
 
 int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_t *offsets,

@@ -298,15 +298,25 @@ def _finish(host: bool, status: dv.Status, *arrays):
 # ---------------------------------------------------------------------------
 
 
+# Two-pass radius queries keep the first _ROW_HITS hits of every query from
+# the count pass (in traversal order, so bytes are the reference's fill
+# order); the fill pass then revisits only queries with more hits.  The row
+# buffer is skipped when it would exceed _ROW_BUDGET bytes.
+_ROW_HITS = 16
+_ROW_BUDGET = 4 << 30
+
+
 def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     l = _lib.lib()
     ct = tree.ctree()
     st = dv.stream()
     nq = b.nq
     counts = dv.empty(nq, torch.int32)
+    rows = _ROW_HITS if nq * _ROW_HITS * 4 <= _ROW_BUDGET else 0
+    buf = dv.empty((nq, rows), torch.int32) if rows else None
     _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
         ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq, dv.ptr(counts),
-        status.ptr, st)))
+        dv.ptr(buf), rows, status.ptr, st)))
     offsets = dv.empty(nq + 1, torch.int64)
     ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
     _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
@@ -316,9 +326,13 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     total = int(total[0])
     out = dv.empty(total, torch.int32)
     if total:
+        if rows:
+            _lib.check(l.lbvh_compact(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), nq,
+                                      dv.ptr(out), st))
         _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
             ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq,
-            dv.ptr(offsets), dv.ptr(out), status.ptr, st)))
+            dv.ptr(offsets), dv.ptr(out), dv.ptr(counts) if rows else None, rows, status.ptr,
+            st)))
     return offsets, out
 
 
