@@ -199,11 +199,21 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
  * max_span: host upper bound of min(k_q, n) (selects the kernel variant).
  * query_codes (optional): Morton codes of the queries in `order` order (from
  * lbvh_query_order); with tree->leaf_codes they enable the search-radius
- * seed, which never changes results. */
+ * seed, which never changes results.  flags: LBVH_KNN_SQUARED writes the
+ * squared distances (no sqrt) -- used by the distributed merge, which must
+ * order candidates by exact (d^2, ordinal). */
+#define LBVH_KNN_SQUARED 0x1
 int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
-             int64_t max_span, int32_t *out_idx, float *out_dist, uint32_t *status,
-             void *stream);
+             int64_t max_span, int32_t *out_idx, float *out_dist, int flags,
+             uint32_t *status, void *stream);
+
+/* Distributed kNN merge epilogue (no reference counterpart):
+ * merged candidate keys (dist^2 bits << 32 | global ordinal) -> ordinals and
+ * correctly rounded distances sqrt(dist^2), as knn_pass's final sqrt
+ * (_kernels.py:413-414). */
+int lbvh_unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *ordinals, float *dist,
+                         void *stream);
 
 #ifdef __cplusplus
 }

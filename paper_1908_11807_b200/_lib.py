@@ -25,6 +25,7 @@ FLAG_BAD_RADIUS = 0x10
 FLAG_BAD_K = 0x20
 FLAG_BAD_TREE = 0x40
 NODE_BYTES = 64
+KNN_SQUARED = 0x1
 MAX_ITEMS = (1 << 30) - 1
 
 _lock = threading.Lock()
@@ -93,7 +94,10 @@ _SIGS = {
                           ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                   ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
-                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
+                 ctypes.c_int),
+    "lbvh_unpack_knn_keys": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p], ctypes.c_int),
 }
 
 

@@ -58,8 +58,9 @@ int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t,
 int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
                 void *, size_t, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
-        const int64_t *, int64_t, int32_t *, float *, uint32_t *, cudaStream_t);
+        const int64_t *, int64_t, int32_t *, float *, int, uint32_t *, cudaStream_t);
 int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
+int unpack_knn_keys(const uint64_t *, int64_t, int64_t *, float *, cudaStream_t);
 
 }  // namespace lbvh
 
@@ -182,9 +183,14 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
 
 int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              const uint32_t *query_codes, int64_t nq, const int64_t *offsets, int64_t max_span,
-             int32_t *out_idx, float *out_dist, uint32_t *status, void *stream) {
+             int32_t *out_idx, float *out_dist, int flags, uint32_t *status, void *stream) {
     return knn(tree, centers, order, query_codes, nq, offsets, max_span, out_idx, out_dist,
-               status, S(stream));
+               flags, status, S(stream));
+}
+
+int lbvh_unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *ordinals, float *dist,
+                         void *stream) {
+    return unpack_knn_keys(keys, n, ordinals, dist, S(stream));
 }
 
 }  // extern "C"

@@ -25,6 +25,8 @@
 namespace lbvh {
 namespace {
 
+__device__ __forceinline__ float bx_of(const lbvh_tree &t, int i) { return __ldg(t.root_box + i); }
+
 enum SpatialMode {
     kCount = 0,     // count only                        (spatial_pass store=False)
     kFill = 1,      // write at offsets[q]               (spatial_pass store=True)
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(256)
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
            const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-           float *__restrict__ out_dist, uint32_t *status) {
+           float *__restrict__ out_dist, bool squared, uint32_t *status) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
@@ -269,8 +271,8 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
                 pz = __ldg(centers + 3 * q + 2);
     if (t.n == 1) {
         const float *bx = t.root_box;
-        out_dist[base] = __fsqrt_rn(
-            box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]));
+        const float d2 = box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]);
+        out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
         out_idx[base] = __ldg(t.leaf_obj);
         return;
     }
@@ -360,7 +362,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         if (j >= K - kk) {
             const int64_t o = base + (j - (K - kk));
             out_idx[o] = top.ordinal(j);
-            out_dist[o] = __fsqrt_rn(top.dist(j));
+            out_dist[o] = squared ? top.dist(j) : __fsqrt_rn(top.dist(j));
         }
     }
 }
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(128)
 knn_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
                 const uint32_t *__restrict__ order, int64_t nq,
                 const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-                float *__restrict__ out_dist, uint32_t *status) {
+                float *__restrict__ out_dist, bool squared, uint32_t *status) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
@@ -410,8 +412,9 @@ knn_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
     float *hd = out_dist + base;
     int32_t *hi = out_idx + base;
     if (t.n == 1) {
-        const float *bx = t.root_box;
-        hd[0] = __fsqrt_rn(box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]));
+        const float d2 = box_dist_sq(px, py, pz, bx_of(t, 0), bx_of(t, 1), bx_of(t, 2),
+                                     bx_of(t, 3), bx_of(t, 4), bx_of(t, 5));
+        hd[0] = squared ? d2 : __fsqrt_rn(d2);
         hi[0] = __ldg(t.leaf_obj);
         return;
     }
@@ -470,7 +473,8 @@ done:
         int32_t ti = hi[0]; hi[0] = hi[hs]; hi[hs] = ti;
         sift_down(hd, hi, hs, 0);
     }
-    for (int64_t j = 0; j < size; ++j) hd[j] = __fsqrt_rn(hd[j]);
+    if (!squared)
+        for (int64_t j = 0; j < size; ++j) hd[j] = __fsqrt_rn(hd[j]);
 }
 
 __global__ void __launch_bounds__(256)
@@ -552,7 +556,7 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
 
 int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
-        int32_t *out_idx, float *out_dist, uint32_t *status, cudaStream_t stream) {
+        int32_t *out_idx, float *out_dist, int flags, uint32_t *status, cudaStream_t stream) {
     if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0 || max_span <= 0) return LBVH_OK;
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
@@ -566,13 +570,16 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     if (max_span <= KV) {                                                                   \
         if (variant == 1)                                                                   \
             knn_kernel<KV, true><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,     \
-                                                        offsets, out_idx, out_dist, status); \
+                                                        offsets, out_idx, out_dist, squared, \
+                                                        status);                            \
         else                                                                                \
             knn_kernel<KV, false><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,    \
-                                                         offsets, out_idx, out_dist, status); \
+                                                         offsets, out_idx, out_dist,        \
+                                                         squared, status);                  \
         count_launches(1);                                                                  \
         return check_launch();                                                              \
     }
+    const bool squared = (flags & LBVH_KNN_SQUARED) != 0;
     LBVH_KNN_CASE(4)
     LBVH_KNN_CASE(8)
     LBVH_KNN_CASE(10)
@@ -580,7 +587,32 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     LBVH_KNN_CASE(32)
 #undef LBVH_KNN_CASE
     knn_heap_kernel<<<div_up(nq, 128), 128, 0, stream>>>(*t, centers, order, nq, offsets,
-                                                         out_idx, out_dist, status); count_launches(1);
+                                                         out_idx, out_dist, squared, status);
+    count_launches(1);
+    return check_launch();
+}
+
+namespace {
+__global__ void __launch_bounds__(256)
+unpack_knn_keys_kernel(const uint64_t *__restrict__ keys, int64_t n, int64_t *__restrict__ gid,
+                       float *__restrict__ dist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = __ldg(keys + i);
+        gid[i] = (int64_t)(k & 0xFFFFFFFFull);
+        dist[i] = __fsqrt_rn(__uint_as_float((uint32_t)(k >> 32)));
+    }
+}
+}  // namespace
+
+int unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *gid, float *dist,
+                    cudaStream_t stream) {
+    if (n < 0 || (n > 0 && (!keys || !gid || !dist))) return LBVH_ERR_INVALID_ARG;
+    if (n == 0) return LBVH_OK;
+    unsigned g = div_up(n, 256);
+    g = g < kNumSMs * 16 ? g : kNumSMs * 16;
+    unpack_knn_keys_kernel<<<g, 256, 0, stream>>>(keys, n, gid, dist);
+    count_launches(1);
     return check_launch();
 }
 

@@ -1,0 +1,395 @@
+"""Sharded multi-GPU search: local BVHs under a top tree of rank boxes.
+
+SURVEY.md §8(e).  One process per GPU (``torch.distributed``, NCCL over
+NVLink/NVSwitch).  The reference has no distributed path (PAPER.md:1127-1137,
+SPEC.md:14); results here are defined as the single-process reference result
+on the concatenated cloud with **global** ordinals, and every step below keeps
+that exact:
+
+build
+  1. global scene box: all-reduce min / max of the local primitives;
+  2. 30-bit Morton codes on that grid (the reference recipe, f64) and keys
+     ``code << 32 | global ordinal``;
+  3. splitters from an all-gathered key sample cut the key space into P
+     contiguous Morton ranges; primitives move to their range's rank with one
+     variable all-to-all (counts first, then payload);
+  4. each rank builds a local BVH on its range (device kernels) and keeps
+     the global ordinal of every local primitive;
+  5. the top tree is the all-gathered array of P rank boxes.
+
+kNN
+  1. every query goes to its *home* rank (the Morton range holding its
+     code); the home runs a local kNN (squared distances) and takes its k-th
+     distance^2 R (inf if the home has fewer than k primitives);
+  2. the query is forwarded to every other rank whose box distance^2 <= R
+     (non-strict, so ordinal ties survive); those run a local kNN;
+  3. candidates return to the home, which keeps the k smallest by the
+     reference's lexicographic (d^2, global ordinal) order
+     (_kernels.py:293-296) and takes sqrt;
+  4. results return to the query's origin rank, in its query order.
+  Any point of the global top-k lies on a rank whose box distance is <= its
+  distance <= R, so nothing is lost; the merge order is exact.
+
+radius
+  a query goes to every rank whose box distance^2 <= r*r (fp32, as the
+  kernels); hits come back as global ordinals, sorted per query.
+
+The local search and the few dense helpers go through an ``Engine``: the
+default :class:`GpuEngine` uses this package's CUDA kernels; tests may plug a
+CPU engine (the oracle) to exercise the routing on ``gloo``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+__all__ = ["GpuEngine", "DistributedBvh", "build_distributed", "query_knn_distributed",
+           "query_spatial_distributed"]
+
+
+# ---------------------------------------------------------------------------
+# engines
+# ---------------------------------------------------------------------------
+
+
+class GpuEngine:
+    """Local search on this rank's GPU through the C ABI (no CPU path)."""
+
+    def __init__(self, device: torch.device | None = None):
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+
+    def morton(self, pts: torch.Tensor, lo: np.ndarray, hi: np.ndarray) -> torch.Tensor:
+        from . import _device as dv
+        from . import _lib
+
+        n = int(pts.shape[0])
+        codes = torch.empty(n, dtype=torch.int32, device=self.device)
+        if n:
+            p64 = pts.to(torch.float64).contiguous()
+            lo = np.ascontiguousarray(lo, dtype=np.float64)
+            hi = np.ascontiguousarray(hi, dtype=np.float64)
+            _lib.check(_lib.lib().lbvh_morton_codes(dv.ptr(p64), n, lo.ctypes.data,
+                                                    hi.ctypes.data, dv.ptr(codes), dv.stream()))
+        return codes.to(torch.int64)
+
+    def build(self, pts: torch.Tensor):
+        from .tree import build
+
+        return build(pts.contiguous())
+
+    def box(self, tree) -> torch.Tensor:
+        return tree.device_arrays()["root_box"].clone()
+
+    def knn_sq(self, tree, centers: torch.Tensor, k: int):
+        from .traversal import query_knn_squared
+
+        m = int(centers.shape[0])
+        kk = min(k, tree.leaf_count)
+        rs = query_knn_squared(tree, (centers.contiguous(), k))
+        return (rs.indices.to(torch.int64).reshape(m, kk), rs.distances.reshape(m, kk))
+
+    def radius(self, tree, centers: torch.Tensor, radii: torch.Tensor):
+        from .traversal import query_spatial_2p
+
+        rs = query_spatial_2p(tree, (centers.contiguous(), radii.contiguous()))
+        return rs.offsets, rs.indices.to(torch.int64)
+
+    def unpack_keys(self, keys: torch.Tensor):
+        """(d^2 bits << 32 | ordinal) keys -> (ordinals, __fsqrt_rn(d^2))."""
+        from . import _device as dv
+        from . import _lib
+
+        gid = torch.empty(keys.shape, dtype=torch.int64, device=self.device)
+        dd = torch.empty(keys.shape, dtype=torch.float32, device=self.device)
+        _lib.check(_lib.lib().lbvh_unpack_knn_keys(dv.ptr(keys), keys.numel(), dv.ptr(gid),
+                                                   dv.ptr(dd), dv.stream()))
+        return gid, dd
+
+
+# ---------------------------------------------------------------------------
+# collectives
+# ---------------------------------------------------------------------------
+
+
+_COMM = {}  # group -> device collectives run on (the data device unless overridden)
+
+
+def _comm_device(group, data_dev):
+    return _COMM.get(group, data_dev)
+
+
+def _alltoallv(rows: torch.Tensor, dest: torch.Tensor, world: int, group=None):
+    """Send row i of ``rows`` to rank ``dest[i]``; returns (received rows,
+    per-source counts).  Counts are exchanged first, then the payload."""
+    cdev = _comm_device(group, rows.device)
+    order = torch.argsort(dest, stable=True)
+    send = rows[order].contiguous().to(cdev)
+    counts = torch.bincount(dest, minlength=world).to(torch.int64).to(cdev)
+    recv_counts = torch.empty_like(counts)
+    dist.all_to_all_single(recv_counts, counts, group=group)
+    sc, rc = counts.tolist(), recv_counts.tolist()
+    recv = torch.empty((sum(rc),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=cdev)
+    dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc,
+                           group=group)
+    return recv.to(rows.device), rc
+
+
+def _all_reduce(x: torch.Tensor, op, group):
+    cdev = _comm_device(group, x.device)
+    y = x.to(cdev)
+    dist.all_reduce(y, op=op, group=group)
+    return y.to(x.device)
+
+
+def _all_gather(x: torch.Tensor, world: int, group):
+    cdev = _comm_device(group, x.device)
+    y = x.to(cdev)
+    out = [torch.empty_like(y) for _ in range(world)]
+    dist.all_gather(out, y, group=group)
+    return [o.to(x.device) for o in out]
+
+
+def set_comm_device(device, group=None) -> None:
+    """Run this group's collectives on ``device`` (e.g. CPU tensors for a
+    gloo group whose ranks share one GPU in tests)."""
+    _COMM[group] = torch.device(device)
+
+
+def _source_ranks(counts, device) -> torch.Tensor:
+    return torch.repeat_interleave(torch.arange(len(counts), device=device),
+                                   torch.tensor(counts, device=device))
+
+
+def _box_dist_sq(c: torch.Tensor, boxes: torch.Tensor) -> torch.Tensor:
+    """(m,3) centers x (P,6) boxes -> (m,P) fp32 distance^2, the kernels'
+    recipe: per-axis clamp gap, squared, summed x -> y -> z, unfused."""
+    d = None
+    for a in range(3):
+        v = c[:, a:a + 1]
+        lo, hi = boxes[None, :, a], boxes[None, :, 3 + a]
+        g = torch.clamp(torch.maximum(lo - v, v - hi), min=0.0)
+        g2 = g * g
+        d = g2 if d is None else d + g2
+    return d
+
+
+# ---------------------------------------------------------------------------
+# distributed tree
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class DistributedBvh:
+    engine: object
+    tree: object | None          # local BVH (None when this rank got no primitives)
+    gids: torch.Tensor           # global ordinal of each local primitive
+    boxes: torch.Tensor          # (P, 6) rank boxes (+inf / -inf for empty ranks)
+    counts: list                 # primitives per rank
+    split_codes: torch.Tensor    # (P-1,) Morton codes cutting the ranges
+    scene_lo: np.ndarray
+    scene_hi: np.ndarray
+    world: int
+    rank: int
+    group: object = None
+    monotone: bool = True        # local ordinal order == global ordinal order
+
+    @property
+    def total(self) -> int:
+        return int(sum(self.counts))
+
+
+def build_distributed(local_points, global_offset: int, engine=None, group=None,
+                      samples_per_rank: int = 1024) -> DistributedBvh:
+    """Collective: every rank passes its (n_r, 3) primitives whose global
+    ordinals are ``global_offset .. global_offset + n_r - 1``."""
+    engine = engine or GpuEngine()
+    dev = engine.device
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pts = torch.as_tensor(local_points, dtype=torch.float32).to(dev).reshape(-1, 3)
+    n = int(pts.shape[0])
+    # 1. global scene box
+    if n:
+        lo, hi = pts.min(dim=0).values, pts.max(dim=0).values
+    else:
+        lo = torch.full((3,), math.inf, device=dev)
+        hi = torch.full((3,), -math.inf, device=dev)
+    lo = _all_reduce(lo, dist.ReduceOp.MIN, group)
+    hi = _all_reduce(hi, dist.ReduceOp.MAX, group)
+    scene_lo = lo.cpu().numpy().astype(np.float64)
+    scene_hi = hi.cpu().numpy().astype(np.float64)
+    # 2. keys on the global grid
+    codes = engine.morton(pts, scene_lo, scene_hi)
+    gids = torch.arange(n, dtype=torch.int64, device=dev) + int(global_offset)
+    keys = (codes << 32) | gids
+    # 3. splitters from a gathered sample of sorted keys
+    skeys = torch.sort(keys).values
+    s = samples_per_rank
+    if n:
+        pick = torch.linspace(0, n - 1, s, device=dev).round().to(torch.int64)
+        sample = skeys[pick]
+    else:
+        sample = torch.full((s,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    gathered = _all_gather(sample, world, group)
+    allsamp = torch.sort(torch.cat(gathered)).values
+    cut = [allsamp[(i * allsamp.numel()) // world] for i in range(1, world)]
+    splitters = torch.stack(cut) if cut else torch.empty(0, dtype=torch.int64, device=dev)
+    dest = torch.searchsorted(splitters, keys, right=True)
+    # exchange primitives with their global ordinals (f64 rows: exact for both)
+    payload = torch.cat([pts.to(torch.float64), gids.to(torch.float64)[:, None]], dim=1)
+    recv, _ = _alltoallv(payload, dest, world, group)
+    rpts = recv[:, :3].to(torch.float32).contiguous()
+    rgids = recv[:, 3].to(torch.int64)
+    # 4. local build
+    m = int(rpts.shape[0])
+    tree = engine.build(rpts) if m else None
+    box = engine.box(tree).to(dev) if m else torch.tensor(
+        [math.inf] * 3 + [-math.inf] * 3, dtype=torch.float32, device=dev)
+    # 5. top tree
+    boxes = _all_gather(box.to(torch.float32), world, group)
+    cnts = _all_gather(torch.tensor([m], dtype=torch.int64, device=dev), world, group)
+    monotone = bool((rgids[1:] > rgids[:-1]).all().item()) if m > 1 else True
+    return DistributedBvh(engine, tree, rgids, torch.stack(boxes), [int(c.item()) for c in cnts],
+                          splitters >> 32, scene_lo, scene_hi, world, rank, group, monotone)
+
+
+def _local_knn(t: DistributedBvh, centers: torch.Tensor, k: int):
+    """(m, k) global ordinals and d^2 (padded with -1 / inf) from this rank."""
+    dev = t.engine.device
+    m = int(centers.shape[0])
+    gid = torch.full((m, k), -1, dtype=torch.int64, device=dev)
+    d2 = torch.full((m, k), math.inf, dtype=torch.float32, device=dev)
+    if m and t.tree is not None:
+        idx, dd = t.engine.knn_sq(t.tree, centers, k)
+        kk = idx.shape[1]
+        gid[:, :kk] = t.gids[idx]
+        d2[:, :kk] = dd
+    return gid, d2
+
+
+def _merge_keys(gid: torch.Tensor, d2: torch.Tensor) -> torch.Tensor:
+    """Lexicographic (d^2, ordinal) as one int64 key; padding sorts last."""
+    bits = d2.contiguous().view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    key = (bits << 32) | (gid & 0xFFFFFFFF)
+    return torch.where(gid < 0, torch.full_like(key, torch.iinfo(torch.int64).max), key)
+
+
+def query_knn_distributed(t: DistributedBvh, centers, k: int):
+    """Collective kNN over the sharded cloud.  Returns (offsets int64,
+    global ordinals int64, distances f32) for this rank's queries, in order;
+    spans are min(k, total) long, sorted by (distance, ordinal)."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    dev, world, g = t.engine.device, t.world, t.group
+    c = torch.as_tensor(centers, dtype=torch.float32).to(dev).reshape(-1, 3)
+    nq = int(c.shape[0])
+    kk = min(k, t.total)
+    # 1. to the home rank
+    codes = t.engine.morton(c, t.scene_lo, t.scene_hi)
+    home = torch.searchsorted(t.split_codes, codes, right=True)
+    q_id = torch.arange(nq, dtype=torch.float64, device=dev)
+    rows = torch.cat([c.to(torch.float64), q_id[:, None]], dim=1)
+    hq, hcounts = _alltoallv(rows, home, world, g)
+    origin = _source_ranks(hcounts, dev)
+    hc = hq[:, :3].to(torch.float32).contiguous()
+    mh = int(hc.shape[0])
+    own_gid, own_d2 = _local_knn(t, hc, k)
+    if t.tree is not None and t.counts[t.rank] >= k:
+        bound = own_d2[:, k - 1]
+    else:
+        bound = torch.full((mh,), math.inf, dtype=torch.float32, device=dev)
+    # 2. forward to ranks within the bound
+    bd = _box_dist_sq(hc, t.boxes)                                  # (mh, P)
+    need = (bd <= bound[:, None]) & (torch.tensor(t.counts, device=dev) > 0)[None, :]
+    need[:, t.rank] = False
+    qi, rr = torch.nonzero(need, as_tuple=True)
+    frows = torch.cat([hc[qi].to(torch.float64), qi.to(torch.float64)[:, None]], dim=1)
+    fq, fcounts = _alltoallv(frows, rr, world, g)
+    fsrc = _source_ranks(fcounts, dev)
+    f_gid, f_d2 = _local_knn(t, fq[:, :3].to(torch.float32).contiguous(), k)
+    back = torch.cat([fq[:, 3:4], f_d2.to(torch.float64), f_gid.to(torch.float64)], dim=1)
+    bq, _ = _alltoallv(back, fsrc, world, g)
+    # 3. merge at home: own candidates + every responder's
+    brow = bq[:, 0].to(torch.int64)
+    nresp = torch.bincount(brow, minlength=mh) if brow.numel() else torch.zeros(
+        mh, dtype=torch.int64, device=dev)
+    own_keys = _merge_keys(own_gid, own_d2)
+    if t.monotone:
+        # local ordinals map to global ones in increasing order, so an own
+        # list (sorted by (d^2, local ordinal)) is already in merge order
+        top = own_keys[:, :kk].clone()
+        rows = torch.nonzero(nresp > 0, as_tuple=True)[0]
+    else:
+        top = torch.empty((mh, kk), dtype=torch.int64, device=dev)
+        rows = torch.arange(mh, device=dev)
+    if rows.numel():
+        nr = rows.numel()
+        pos = torch.full((mh,), -1, dtype=torch.int64, device=dev)
+        pos[rows] = torch.arange(nr, device=dev)
+        width = k * (1 + int(nresp[rows].max().item()))
+        cand = torch.full((nr, width), torch.iinfo(torch.int64).max, dtype=torch.int64,
+                          device=dev)
+        cand[:, :k] = own_keys[rows]
+        if brow.numel():
+            o = torch.argsort(brow, stable=True)
+            brow_s = brow[o]
+            starts = torch.cumsum(nresp, 0) - nresp
+            slot = torch.arange(brow_s.numel(), device=dev) - starts[brow_s]
+            cols = (1 + slot)[:, None] * k + torch.arange(k, device=dev)[None, :]
+            cand[pos[brow_s][:, None], cols] = _merge_keys(
+                bq[o, 1 + k:1 + 2 * k].to(torch.int64), bq[o, 1:1 + k].to(torch.float32))
+        top[rows] = torch.sort(cand, dim=1).values[:, :kk]
+    # ordinals and correctly rounded sqrt(d^2) (torch's CPU sqrt is not)
+    res_gid, res_dist = t.engine.unpack_keys(top.contiguous())
+    # 4. back to the origin rank, in query order
+    ret = torch.cat([hq[:, 3:4], res_dist.to(torch.float64), res_gid.to(torch.float64)], dim=1)
+    got, _ = _alltoallv(ret, origin, world, g)
+    qix = got[:, 0].to(torch.int64)
+    o = torch.argsort(qix)
+    dist_out = got[o, 1:1 + kk].to(torch.float32).reshape(-1)
+    gid_out = got[o, 1 + kk:1 + 2 * kk].to(torch.int64).reshape(-1)
+    offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
+    return offsets, gid_out, dist_out
+
+
+def query_spatial_distributed(t: DistributedBvh, centers, radius):
+    """Collective radius search.  Returns (offsets int64, global ordinals
+    int64 sorted within each query) for this rank's queries, in order."""
+    dev, world, g = t.engine.device, t.world, t.group
+    c = torch.as_tensor(centers, dtype=torch.float32).to(dev).reshape(-1, 3)
+    nq = int(c.shape[0])
+    r = torch.as_tensor(radius, dtype=torch.float32).to(dev)
+    r = r.expand(nq).contiguous() if r.ndim == 0 else r.reshape(-1)
+    r2 = r * r
+    bd = _box_dist_sq(c, t.boxes)
+    need = (bd <= r2[:, None]) & (torch.tensor(t.counts, device=dev) > 0)[None, :]
+    qi, rr = torch.nonzero(need, as_tuple=True)
+    rows = torch.cat([c[qi].to(torch.float64), r[qi].to(torch.float64)[:, None],
+                      qi.to(torch.float64)[:, None]], dim=1)
+    rq, rcounts = _alltoallv(rows, rr, world, g)
+    src = _source_ranks(rcounts, dev)
+    m = int(rq.shape[0])
+    if m and t.tree is not None:
+        off, idx = t.engine.radius(t.tree, rq[:, :3].to(torch.float32).contiguous(),
+                                   rq[:, 3].to(torch.float32).contiguous())
+        cnt = off[1:] - off[:-1]
+        owner = torch.repeat_interleave(torch.arange(m, device=dev), cnt)
+        hit_rows = torch.stack([rq[owner, 4], t.gids[idx].to(torch.float64)], dim=1)
+        hit_dest = src[owner]
+    else:
+        hit_rows = torch.empty((0, 2), dtype=torch.float64, device=dev)
+        hit_dest = torch.empty(0, dtype=torch.int64, device=dev)
+    got, _ = _alltoallv(hit_rows, hit_dest, world, g)
+    qix = got[:, 0].to(torch.int64)
+    gids = got[:, 1].to(torch.int64)
+    key = qix * (1 << 32) + gids
+    o = torch.argsort(key)
+    counts = torch.bincount(qix, minlength=nq) if qix.numel() else torch.zeros(
+        nq, dtype=torch.int64, device=dev)
+    offsets = torch.zeros(nq + 1, dtype=torch.int64, device=dev)
+    offsets[1:] = torch.cumsum(counts, 0)
+    return offsets, gids[o]

@@ -404,11 +404,22 @@ def query_spatial_1p(tree: Bvh, queries, buffer_size: int, sort_queries: bool = 
 def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -> ResultSet:
     """k-nearest batch (traversal.py:251-272): spans of min(k, n) sorted by
     (distance, ordinal) with true distances."""
+    return _query_knn(tree, queries, sort_queries, squared=False)
+
+
+def query_knn_squared(tree: Bvh, queries, sort_queries: bool = True) -> ResultSet:
+    """As :func:`query_knn` but ``distances`` holds the exact squared fp32
+    distances (no sqrt); the distributed merge orders by these."""
+    return _query_knn(tree, queries, sort_queries, squared=True)
+
+
+def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultSet:
+    flags = _lib.KNN_SQUARED if squared else 0
     b = _knn_batch(queries)
     if b.nq == 0:
         return _empty_result(b.host, knn=True)
     if b.host_centers is not None:
-        return _knn_pipelined(tree, b, sort_queries)
+        return _knn_pipelined(tree, b, sort_queries, flags)
     l = _lib.lib()
     st = dv.stream()
     nq, n = b.nq, tree.leaf_count
@@ -435,12 +446,12 @@ def query_knn(tree: Bvh, queries, sort_queries: bool = True, threads: int = 1) -
     ct = tree.ctree()
     _lib.check(_launch("knn", lambda: l.lbvh_knn(
         ct, dv.ptr(b.centers), dv.ptr(order), dv.ptr(qcodes), nq, dv.ptr(offsets), max_span,
-        dv.ptr(out_idx), dv.ptr(out_dist), status.ptr, st)))
+        dv.ptr(out_idx), dv.ptr(out_dist), flags, status.ptr, st)))
     offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
     return ResultSet._trusted(offsets, out_idx, out_dist)
 
 
-def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet:
+def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> ResultSet:
     """Host kNN batch as an H2D / compute / D2H pipeline over query chunks.
 
     Chunk results are identical to the one-shot path: every query's span is
@@ -493,7 +504,7 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet:
                                           dv.ptr(ws), ws.numel(), comp.cuda_stream))
         _lib.check(_launch("knn", lambda: l.lbvh_knn(
             ct, cc, dv.ptr(order) if srt else None, dv.ptr(qcodes) if srt else None, m,
-            o_ptr + 8 * c0, span, dv.ptr(out_idx), dv.ptr(out_dist), status.ptr,
+            o_ptr + 8 * c0, span, dv.ptr(out_idx), dv.ptr(out_dist), flags, status.ptr,
             comp.cuda_stream)))
         e_c = torch.cuda.Event()
         e_c.record(comp)
