@@ -244,6 +244,11 @@ def build_distributed(local_points, global_offset: int, engine=None, group=None,
     recv, _ = _alltoallv(payload, dest, world, group)
     rpts = recv[:, :3].to(torch.float32).contiguous()
     rgids = recv[:, 3].to(torch.int64)
+    # local ordinal order must be global ordinal order: the local kNN breaks
+    # distance ties by local ordinal (_kernels.py:293-296)
+    gorder = torch.argsort(rgids)
+    rgids = rgids[gorder]
+    rpts = rpts[gorder].contiguous()
     # 4. local build
     m = int(rpts.shape[0])
     tree = engine.build(rpts) if m else None
