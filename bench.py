@@ -15,9 +15,13 @@ are in ``extra``.
 ``--impl reference`` times the CPU restatement of the reference path
 (oracle/, all host threads) on a bounded sample of the same workload.
 
-Multi-GPU (torchrun): weak scaling, one process per GPU; every rank indexes
-its own 1e7-point shard and answers its own 1e7 queries (replicas, see
-DESIGN.md); time is the max over ranks.
+Multi-GPU (torchrun): weak scaling, one process per GPU over NCCL; the
+global cloud is N*1e7 points and N*1e7 queries, rank r holds the r-th chunk
+of each; the step is the sharded search of SURVEY §8(e)
+(``distributed.query_knn_distributed``: Morton-range shards, rank-box top
+tree, all-to-all query forwarding, exact merge); time is the max over ranks.
+``BENCH_BACKEND=gloo`` runs the same protocol with CPU collectives (testing
+several ranks on one GPU).
 """
 
 from __future__ import annotations
@@ -208,7 +212,14 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
+            from paper_1908_11807_b200 import distributed as _D
+
+            _D.set_comm_device("cpu")
 
     def barrier():
         if world > 1:
@@ -217,7 +228,8 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        on_gpu = tdist.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         return float(t.item())
 
@@ -230,12 +242,15 @@ def run_ours(args):
     def flush_l2():
         flush_buf.fill_(rank & 0xFF)
 
-    # Weak scaling: rank r indexes cloud seed 2r and queries cloud seed 2r+1
-    # (rank 0 = the reference bench's seeds 0 / 1).
-    src_spec = lb.CloudSpec("cube", "filled", m, 2 * rank)
-    qry_spec = lb.CloudSpec("cube", "filled", nq, 2 * rank + 1)
-    pts = lb.generate(src_spec)
-    qs = lb.generate(qry_spec)
+    # Weak scaling over one global cloud: N*m filled-box points (seed 0) and
+    # N*nq queries (seed 1), the reference bench's clouds; rank r holds the
+    # r-th contiguous chunk of each (N=1: exactly configuration C2).
+    if world == 1:
+        pts = lb.generate(lb.CloudSpec("cube", "filled", m, 0))
+        qs = lb.generate(lb.CloudSpec("cube", "filled", nq, 1))
+    else:
+        pts = lb.generate(lb.CloudSpec("cube", "filled", world * m, 0))[rank * m:(rank + 1) * m].copy()
+        qs = lb.generate(lb.CloudSpec("cube", "filled", world * nq, 1))[rank * nq:(rank + 1) * nq].copy()
     pts_d = torch.from_numpy(pts).to(dev)
     qs_d = torch.from_numpy(qs).to(dev)
     r = lb.default_radius(k)
@@ -271,11 +286,28 @@ def run_ours(args):
         return max_over_ranks(total_ms), launches, kms
 
     # -- build the index once (its own timed leg below) ----------------------
-    tree = lb.build(pts_d)
+    sharded = None
+    if world == 1:
+        tree = lb.build(pts_d)
 
-    def knn_step():
-        rs = lb.query_knn(tree, (qs_d, k))
-        return rs
+        def knn_step():
+            return lb.query_knn(tree, (qs_d, k))
+    else:
+        # sharded search: local BVHs under a rank-box top tree,
+        # NCCL all-to-all query forwarding and exact kNN merge
+        from paper_1908_11807_b200 import distributed as D
+
+        tree = None
+        sharded = {}
+
+        def dbuild():
+            sharded["t"] = D.build_distributed(pts_d, rank * m)
+
+        bt, _, _ = timed_loop(dbuild, 1, 1)
+        sharded["build_ms"] = bt
+
+        def knn_step():
+            return D.query_knn_distributed(sharded["t"], qs_d, k)
 
     clocks = None
     if args.profile:
@@ -314,7 +346,8 @@ def run_ours(args):
                                f"nq={nq} seed {2 * rank + 1}, k={k}, query Morton pre-sort on",
                    "m_per_gpu": m, "nq_per_gpu": nq, "k": k,
                    "l2": "flushed before every timed step (256 MiB device write)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"sharded x{world}: Morton-range shards, rank-box top tree, "
+                                   "NCCL all-to-all forwarding" if world > 1 else "single GPU")},
         "roofline": roofline,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
@@ -329,6 +362,9 @@ def run_ours(args):
         host_q = pin.numpy()
 
         def e2e_step():
+            if sharded is not None:
+                off, gid, dd = D.query_knn_distributed(sharded["t"], pin.to(dev, non_blocking=True), k)
+                return off.cpu(), gid.cpu(), dd.cpu()
             rs = lb.query_knn(tree, (host_q, k))
             assert rs.indices.shape[0] == nq * min(k, m)
             return rs
@@ -339,11 +375,16 @@ def run_ours(args):
         out["e2e"] = {"value": round(world * nq * e2e_steps / (e2e_tot / 1e3), 1),
                       "unit": "queries/s",
                       "h2d_bytes_per_step": nq * 12,
-                      "d2h_bytes_per_step": (nq + 1) * 8 + nq * span * 8 + 4,
+                      "d2h_bytes_per_step": ((nq + 1) * 8 + nq * span * 8 + 4 if sharded is None
+                                             else (nq + 1) * 8 + nq * span * 12),
                       "ms_per_step": round(e2e_tot / e2e_steps, 3),
                       "api": "paper_1908_11807_b200.query_knn(tree, (pinned numpy centers, k))"}
 
-    if not args.no_extra and not args.profile:
+    if sharded is not None:
+        out["extra"] = {"sharded_build_ms": round(sharded["build_ms"], 3),
+                        "sharded_build_prims_per_sec": round(world * m / (sharded["build_ms"] / 1e3), 1),
+                        "local_prims_this_rank": int(sharded["t"].counts[rank])}
+    elif not args.no_extra and not args.profile:
         out["extra"] = extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank,
                                      dev, peak_gbs)
 
