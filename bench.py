@@ -66,8 +66,8 @@ def parse_args(argv=None):
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--m", type=int, default=10_000_000, help="indexed points per GPU")
-    p.add_argument("--nq", type=int, default=None, help="queries per GPU (default m)")
+    p.add_argument("--points", dest="m", type=int, default=10_000_000, help="indexed points per GPU")
+    p.add_argument("--queries", dest="nq", type=int, default=None, help="queries per GPU (default m)")
     p.add_argument("--k", type=int, default=10)
     p.add_argument("--no-extra", action="store_true", help="headline metric only")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

@@ -437,8 +437,8 @@ def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultS
         mx = dv.empty(1, torch.int32)
         _lib.check(l.lbvh_knn_offsets(dv.ptr(b.ks), 0, n, nq, dv.ptr(offsets), dv.ptr(mx),
                                       status.ptr, dv.ptr(ws), ws.numel(), st))
-        flags, mxh, tot = dv.d2h_many(status.dev, mx, offsets[nq:])
-        _raise_flags(int(flags[0]) & 0xFFFFFFFF)
+        st_word, mxh, tot = dv.d2h_many(status.dev, mx, offsets[nq:])
+        _raise_flags(int(st_word[0]) & 0xFFFFFFFF)
         max_span, total = int(mxh[0]), int(tot[0])
     order, qcodes = _order(tree, b, sort_queries, with_codes=True)
     out_idx = dv.empty(total, torch.int32)
