@@ -341,7 +341,8 @@ def run_ours(args):
         "metric": f"knn_queries_per_sec (k={k}, {m:.0e} filled-box points, {nq:.0e} queries)",
         "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 Morton normalisation)",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "dtype_note": "fp32 box distances (reference recipe, unfused); f64 Morton normalisation",
         "data": "synthetic: paper_1908_11807_b200.datasets PCG64 clouds (reference generators)",
         "config": {"workload": f"C2 kNN: cube:filled m={m} seed {2 * rank} / cube:filled "
                                f"nq={nq} seed {2 * rank + 1}, k={k}, query Morton pre-sort on",
