@@ -215,6 +215,20 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
 int lbvh_unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *ordinals, float *dist,
                          void *stream);
 
+/* ---------------------------------------------------------- brute force */
+
+/* brute_knn / brute_knn_batch   replaces oracle.py:35-45, 62-70: O(n) per
+ * query; out_idx / out_dist are nq x min(k, n), sorted by (d, ordinal). */
+int lbvh_brute_knn(const float *points, int64_t n, const float *centers, int64_t nq, int64_t k,
+                   int32_t *out_idx, float *out_dist, void *stream);
+
+/* brute_radius / brute_radius_sets   replaces oracle.py:26-32, 48-59.
+ * offsets == NULL: writes counts (nq i32); else fills ascending ordinals at
+ * out[offsets[q] ...].  radii may be NULL -> radius. */
+int lbvh_brute_radius(const float *points, int64_t n, const float *centers, const float *radii,
+                      float radius, int64_t nq, int32_t *counts, const int64_t *offsets,
+                      int32_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,10 @@ int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, in
         const int64_t *, int64_t, int32_t *, float *, int, uint32_t *, cudaStream_t);
 int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
 int unpack_knn_keys(const uint64_t *, int64_t, int64_t *, float *, cudaStream_t);
+int brute_knn(const float *, int64_t, const float *, int64_t, int64_t, int32_t *, float *,
+              cudaStream_t);
+int brute_radius(const float *, int64_t, const float *, const float *, float, int64_t, int32_t *,
+                 const int64_t *, int32_t *, cudaStream_t);
 
 }  // namespace lbvh
 
@@ -191,6 +195,17 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
 int lbvh_unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *ordinals, float *dist,
                          void *stream) {
     return unpack_knn_keys(keys, n, ordinals, dist, S(stream));
+}
+
+int lbvh_brute_knn(const float *points, int64_t n, const float *centers, int64_t nq, int64_t k,
+                   int32_t *out_idx, float *out_dist, void *stream) {
+    return brute_knn(points, n, centers, nq, k, out_idx, out_dist, S(stream));
+}
+
+int lbvh_brute_radius(const float *points, int64_t n, const float *centers, const float *radii,
+                      float radius, int64_t nq, int32_t *counts, const int64_t *offsets,
+                      int32_t *out, void *stream) {
+    return brute_radius(points, n, centers, radii, radius, nq, counts, offsets, out, S(stream));
 }
 
 }  // extern "C"

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "internal.cuh"
+#include "topk.cuh"
 
 namespace lbvh {
 namespace {
@@ -155,62 +156,6 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
     for (int j = lane; j < cnt; j += 32) out[dst + j] = __ldcs(row + j);
 }
 
-// Lexicographic (dist^2, ordinal) order, _kernels.py:293-296.
-__device__ __forceinline__ bool lex_less(float d1, int32_t i1, float d2, int32_t i2) {
-    return d1 < d2 || (d1 == d2 && i1 < i2);
-}
-
-// The k best candidates as 64-bit keys (dist^2 bits << 32 | ordinal + 1),
-// kept sorted ascending in registers.  Distances are >= +0 (or +inf), so the
-// key order is exactly the reference's lexicographic (dist^2, ordinal) order
-// (_kernels.py:293-296).  Slots [0, K-kk) hold 0-keys that rank before every
-// real candidate; slots [K-kk, K) start empty (all ones: dist bits are NaN, so
-// no distance compares greater and nothing is pruned until kk candidates
-// are in, matching "size == kk and nd > worst", _kernels.py:367,383).  The
-// k-th best is always slot K-1, a compile-time index, so nothing spills.
-template <int K>
-struct TopK {
-    uint64_t key[K];
-
-    // `bound` (optional, may be NaN = none): a distance^2 known to have at
-    // least kk candidates at or below it.  Empty slots then carry
-    // (bound, 0xFFFFFFFF) -- a virtual candidate every real one at the same
-    // distance beats -- so nodes farther than the bound are pruned from the
-    // start and leaves beyond it are never offered.  All virtual slots are
-    // displaced by real candidates by the end, so results are unchanged.
-    __device__ __forceinline__ void init(int kk, float bound) {
-        const uint64_t empty = isnan(bound)
-                                   ? ~0ull
-                                   : (((uint64_t)__float_as_uint(bound) << 32) | 0xFFFFFFFFull);
-#pragma unroll
-        for (int j = 0; j < K; ++j) key[j] = (j < K - kk) ? 0ull : empty;
-    }
-    __device__ __forceinline__ float worst() const {
-        return __uint_as_float((uint32_t)(key[K - 1] >> 32));
-    }
-    __device__ __forceinline__ static uint64_t make(float d, int32_t obj) {
-        return ((uint64_t)__float_as_uint(d) << 32) | (uint32_t)(obj + 1);
-    }
-
-    // Keep the candidate iff it beats the current k-th best
-    // (_kernels.py:387-395); branch-free sorted insertion dropping slot K-1.
-    __device__ __forceinline__ void offer(float cd, int32_t obj) {
-        const uint64_t c = make(cd, obj);
-        if (!(c < key[K - 1])) return;
-        bool lt[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) lt[j] = key[j] < c;
-#pragma unroll
-        for (int j = K - 1; j > 0; --j) key[j] = lt[j] ? key[j] : (lt[j - 1] ? c : key[j - 1]);
-        key[0] = lt[0] ? key[0] : c;
-    }
-    __device__ __forceinline__ float dist(int j) const {
-        return __uint_as_float((uint32_t)(key[j] >> 32));
-    }
-    __device__ __forceinline__ int32_t ordinal(int j) const {
-        return (int32_t)((uint32_t)key[j]) - 1;
-    }
-};
 
 // Search-radius seed for one query: the kk-th smallest distance^2 among the
 // 2*kk leaves that neighbour the query's Morton code in leaf order (a real

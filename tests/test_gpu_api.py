@@ -385,3 +385,27 @@ def test_estimator_facade():
     assert clone(est).get_params() == est.get_params()
     with pytest.raises(TypeError):
         est.query([SpatialQuery(Point(0, 0, 0), 1.0), KnnQuery(Point(0, 0, 0), 1)])
+
+
+def test_brute_force_helpers_match_reference_semantics():
+    """oracle.py KATs (pkg/tests/test_oracle.py) and numpy brute force."""
+    assert lb.brute_radius(np.float32([[0, 0, 0], [3, 0, 0]]),
+                           SpatialQuery(Point(0, 0, 0), 1.0)).tolist() == [0]
+    assert lb.brute_radius(np.float32([[1, 1, 1], [2, 2, 2], [1, 1, 1]]),
+                           SpatialQuery(Point(1, 1, 1), 0.0)).tolist() == [0, 2]
+    idx, dist = lb.brute_knn(np.float32([[0, 0, 0], [2, 0, 0], [1, 0, 0]]),
+                             KnnQuery(Point(0, 0, 0), 3))
+    assert idx.tolist() == [0, 2, 1] and dist.tolist() == [0.0, 1.0, 2.0]
+    idx, _ = lb.brute_knn(np.float32([[1, 0, 0], [-1, 0, 0], [0, 1, 0]]), KnnQuery(Point(0, 0, 0), 2))
+    assert idx.tolist() == [0, 1]
+    rng = np.random.default_rng(5)
+    pts = rng.integers(-20, 21, size=(3000, 3)).astype(np.float32)
+    cs = rng.integers(-25, 26, size=(200, 3)).astype(np.float32)
+    for k in (1, 10, 33, 70):
+        wi, wd = oracle.brute_knn_batch(pts, cs, k)
+        gi, gd = lb.brute_knn_batch(pts, cs, k)
+        assert np.array_equal(gi, wi) and gd.tobytes() == wd.tobytes(), k
+    for r in (0.0, 2.0, 7.5):
+        want = oracle.brute_radius_sets(pts, cs, r)
+        got = lb.brute_radius_sets(pts, cs, r)
+        assert all(np.array_equal(a, b) for a, b in zip(got, want)), r
