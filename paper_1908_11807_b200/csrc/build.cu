@@ -162,7 +162,7 @@ __device__ __forceinline__ void store_packed(PackedNode *nodes, int64_t id, cons
 
 // K4 + K5.  WITH_BOXES=false is the topology-only variant behind
 // lbvh_generate_topology (sorted codes in, left/right/parent out).
-template <bool WITH_BOXES>
+template <bool WITH_BOXES, bool ROWS_LATE = false>
 __global__ void __launch_bounds__(256)
 hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict__ perm,
                  const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
@@ -224,7 +224,18 @@ hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict_
         if (WITH_BOXES) {
             const int64_t sib = left_side ? rc : lc;
             Box sb;
-            load_box_cg(node_mins, node_maxs, sib, sb);
+            if (ROWS_LATE && sib < internal) {
+                // sibling box = union of its children, from its packed record
+                // (written before its release); same left-first fold as below
+                const PackedNode *sp = nodes + sib;
+                const float4 a = __ldcg(&sp->a), b = __ldcg(&sp->b), c = __ldcg(&sp->c);
+                sb.lo[0] = min_left(a.x, b.z); sb.lo[1] = min_left(a.y, b.w);
+                sb.lo[2] = min_left(a.z, c.x);
+                sb.hi[0] = max_left(a.w, c.y); sb.hi[1] = max_left(b.x, c.z);
+                sb.hi[2] = max_left(b.y, c.w);
+            } else {
+                load_box_cg(node_mins, node_maxs, sib, sb);
+            }
             int32_t sib_link;
             if (sib >= internal)
                 sib_link = (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
@@ -240,7 +251,7 @@ hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict_
             }
             store_packed(nodes, pid, L, R, left_side ? my_link : sib_link,
                          left_side ? sib_link : my_link);
-            store_box(node_mins, node_maxs, pid, P);
+            if (!ROWS_LATE) store_box(node_mins, node_maxs, pid, P);
             mine = P;
             my_link = (int32_t)pid;
             if (root) {
@@ -255,6 +266,26 @@ hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict_
         l = pl;
         r = pr;
         left_side = parent_left;
+    }
+}
+
+// Reference-layout rows of the internal nodes, written after the hierarchy
+// pass: row i = union of the two child boxes in packed record i, folded with
+// the refit's left-first rule (identical bits to an in-pass write).  Thread i
+// reads record i and writes row i: fully coalesced.
+__global__ void __launch_bounds__(256)
+internal_rows_kernel(const PackedNode *__restrict__ nodes, int64_t n_internal,
+                     float *__restrict__ node_mins, float *__restrict__ node_maxs) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_internal;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const PackedNode *p = nodes + i;
+        const float4 a = __ldcs(&p->a), b = __ldcs(&p->b), c = __ldcs(&p->c);
+        node_mins[3 * i] = min_left(a.x, b.z);
+        node_mins[3 * i + 1] = min_left(a.y, b.w);
+        node_mins[3 * i + 2] = min_left(a.z, c.x);
+        node_maxs[3 * i] = max_left(a.w, c.y);
+        node_maxs[3 * i + 1] = max_left(b.x, c.z);
+        node_maxs[3 * i + 2] = max_left(b.y, c.w);
     }
 }
 
@@ -410,9 +441,20 @@ int build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_b
     morton_kernel<<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm); count_launches(1);
     int rc = sort_pairs(codes, perm, n, 30, sort_ws, sort_workspace_bytes(n), stream);
     if (rc != LBVH_OK) return rc;
-    hierarchy_kernel<true><<<div_up(n, 256), 256, 0, stream>>>(
-        codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-        leaf_obj, (PackedNode *)nodes, root_box); count_launches(1);
+    static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 0);
+    if (rows_late && n > 1) {
+        hierarchy_kernel<true, true><<<div_up(n, 256), 256, 0, stream>>>(
+            codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
+            leaf_obj, (PackedNode *)nodes, root_box);
+        internal_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
+            (const PackedNode *)nodes, n - 1, node_mins, node_maxs);
+        count_launches(2);
+    } else {
+        hierarchy_kernel<true><<<div_up(n, 256), 256, 0, stream>>>(
+            codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
+            leaf_obj, (PackedNode *)nodes, root_box);
+        count_launches(1);
+    }
     if (sorted_codes)
         cudaMemcpyAsync(sorted_codes, codes, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
                         stream);
