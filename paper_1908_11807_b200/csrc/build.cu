@@ -441,7 +441,9 @@ int build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_b
     morton_kernel<<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm); count_launches(1);
     int rc = sort_pairs(codes, perm, n, 30, sort_ws, sort_workspace_bytes(n), stream);
     if (rc != LBVH_OK) return rc;
-    static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 0);
+    // 1 (measured 15% faster at 1e7): sibling boxes from packed records,
+    // internal reference rows in a separate coalesced pass.
+    static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 1);
     if (rows_late && n > 1) {
         hierarchy_kernel<true, true><<<div_up(n, 256), 256, 0, stream>>>(
             codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
