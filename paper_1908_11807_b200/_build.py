@@ -82,5 +82,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list) -> str:
+    """A/B build with extra -D defines into _lib/variants/<name>.so (load it
+    with LBVH_LIB=<path>); used only for kernel experiments."""
+    vdir = os.path.join(OUT_DIR, "variants", name)
+    os.makedirs(vdir, exist_ok=True)
+    cc = nvcc()
+    objs = []
+    for src in _sources():
+        obj = os.path.join(vdir, os.path.basename(src).replace(".cu", ".o"))
+        subprocess.run([cc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o",
+                        obj], check=True)
+        objs.append(obj)
+    lib = os.path.join(OUT_DIR, "variants", f"{name}.so")
+    subprocess.run([cc, *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl",
+                    "-lpthread"], check=True)
+    return lib
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -14,7 +14,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblbvh_b200.so")
+# LBVH_LIB overrides the library path (A/B builds of kernel variants).
+LIB_PATH = os.environ.get("LBVH_LIB") or os.path.join(_HERE, "_lib", "liblbvh_b200.so")
 
 STACK_CAPACITY = 64
 FLAG_STACK_EXHAUSTED = 0x01

@@ -28,6 +28,19 @@ namespace {
 
 __device__ __forceinline__ float bx_of(const lbvh_tree &t, int i) { return __ldg(t.root_box + i); }
 
+// Children of an internal node sit at adjacent Karras ordinals (g, g+1), so
+// the next node is very likely in the line(s) these prefetches pull into L1
+// while the current node's boxes are being tested.
+#ifndef LBVH_PREFETCH_CHILDREN
+#define LBVH_PREFETCH_CHILDREN 1
+#endif
+__device__ __forceinline__ void prefetch_children(const PackedNode *nodes, int4 d) {
+    if (LBVH_PREFETCH_CHILDREN) {
+        if (d.x >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + d.x));
+        if (d.y >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + d.y));
+    }
+}
+
 enum SpatialMode {
     kCount = 0,     // count only                        (spatial_pass store=False)
     kFill = 1,      // write at offsets[q]               (spatial_pass store=True)
@@ -98,6 +111,7 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         float4 a, b, c;
         int4 d;
         load_node(nodes, node, a, b, c, d);
+        prefetch_children(nodes, d);
         const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
         const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
         int32_t next = -1;
@@ -253,6 +267,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         float4 a, b, c;
         int4 dd;
         load_node(nodes, node, a, b, c, dd);
+        prefetch_children(nodes, dd);
         const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
         const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
         // farther child first so the nearer one is on top (_kernels.py:373-379)
