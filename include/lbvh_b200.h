@@ -203,10 +203,14 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
  * squared distances (no sqrt) -- used by the distributed merge, which must
  * order candidates by exact (d^2, ordinal). */
 #define LBVH_KNN_SQUARED 0x1
+/* workspace (optional, lbvh_knn_workspace_bytes(nq)): enables the persistent
+ * kernel with per-lane query refill and a separate seed pass; without it
+ * the one-thread-per-query kernel runs.  Results are identical. */
+size_t lbvh_knn_workspace_bytes(int64_t nq);
 int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
              int64_t max_span, int32_t *out_idx, float *out_dist, int flags,
-             uint32_t *status, void *stream);
+             void *workspace, size_t workspace_bytes, uint32_t *status, void *stream);
 
 /* Distributed kNN merge epilogue (no reference counterpart):
  * merged candidate keys (dist^2 bits << 32 | global ordinal) -> ordinals and

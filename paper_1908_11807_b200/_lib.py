@@ -95,8 +95,9 @@ _SIGS = {
                           ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                   ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
-                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
-                 ctypes.c_int),
+                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                  ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_knn_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_unpack_knn_keys": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.c_void_p], ctypes.c_int),
     "lbvh_brute_knn": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,

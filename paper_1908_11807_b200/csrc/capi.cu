@@ -58,7 +58,9 @@ int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t,
 int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
                 void *, size_t, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
-        const int64_t *, int64_t, int32_t *, float *, int, uint32_t *, cudaStream_t);
+        const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
+        cudaStream_t);
+size_t knn_workspace_bytes(int64_t nq);
 int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
 int unpack_knn_keys(const uint64_t *, int64_t, int64_t *, float *, cudaStream_t);
 int brute_knn(const float *, int64_t, const float *, int64_t, int64_t, int32_t *, float *,
@@ -187,10 +189,13 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
 
 int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              const uint32_t *query_codes, int64_t nq, const int64_t *offsets, int64_t max_span,
-             int32_t *out_idx, float *out_dist, int flags, uint32_t *status, void *stream) {
+             int32_t *out_idx, float *out_dist, int flags, void *workspace,
+             size_t workspace_bytes, uint32_t *status, void *stream) {
     return knn(tree, centers, order, query_codes, nq, offsets, max_span, out_idx, out_dist,
-               flags, status, S(stream));
+               flags, workspace, workspace_bytes, status, S(stream));
 }
+
+size_t lbvh_knn_workspace_bytes(int64_t nq) { return knn_workspace_bytes(nq); }
 
 int lbvh_unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *ordinals, float *dist,
                          void *stream) {

@@ -32,7 +32,7 @@ __device__ __forceinline__ float bx_of(const lbvh_tree &t, int i) { return __ldg
 // the next node is very likely in the line(s) these prefetches pull into L1
 // while the current node's boxes are being tested.
 #ifndef LBVH_PREFETCH_CHILDREN
-#define LBVH_PREFETCH_CHILDREN 1
+#define LBVH_PREFETCH_CHILDREN 0  // measured slower (extra L1 traffic); kept for A/B
 #endif
 __device__ __forceinline__ void prefetch_children(const PackedNode *nodes, int4 d) {
     if (LBVH_PREFETCH_CHILDREN) {
@@ -327,6 +327,171 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent kNN with per-lane query refill.
+//
+// One thread per query leaves lanes idle while the slowest query of a warp
+// finishes (traversal lengths vary ~2x).  Here each warp owns a run of
+// kChunk consecutive Morton-ordered query slots (grabbed with one atomic),
+// and a lane that finishes its query immediately starts the next slot of the
+// run, so lanes stay busy and the warp's queries stay spatially coherent.
+// The search-radius seeds are computed by a separate convergent pass.  Per
+// query the traversal is exactly knn_kernel<K, true>'s, so results (and
+// stack-exhaustion behaviour) are identical.
+// ---------------------------------------------------------------------------
+
+constexpr int kChunk = 128;
+
+__device__ __forceinline__ uint32_t lanemask_lt_() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+knn_seed_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
+                int64_t nq, const int64_t *__restrict__ offsets, float *__restrict__ bounds) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    const int kk = (int)(__ldg(offsets + q + 1) - __ldg(offsets + q));
+    float b = __int_as_float(0x7FFFFFFF);
+    if (kk > 0 && t.n > 1)
+        b = seed_bound<K>(t, __ldg(qcodes + s), kk, __ldg(centers + 3 * q),
+                          __ldg(centers + 3 * q + 1), __ldg(centers + 3 * q + 2));
+    bounds[s] = b;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+knn_persistent_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                      const uint32_t *__restrict__ order, const float *__restrict__ bounds,
+                      int64_t nq, const int64_t *__restrict__ offsets,
+                      int32_t *__restrict__ out_idx, float *__restrict__ out_dist, bool squared,
+                      uint32_t *status, unsigned long long *counter) {
+    const unsigned kFull = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt_();
+    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    int64_t chunk_next = 0, chunk_end = 0;
+    bool exhausted = false, active = false;
+    int64_t base = 0;
+    int kk = 0;
+    float px = 0.f, py = 0.f, pz = 0.f;
+    TopK<K> top;
+    top.init(K, __int_as_float(0x7FFFFFFF));
+    uint64_t stack[kStack];
+    int sp = 0;
+    int32_t node = 0;
+    uint32_t fail = 0;
+    while (true) {
+        // ---- refill idle lanes from this warp's run of query slots
+        const unsigned need = __ballot_sync(kFull, !active);
+        if (need) {
+            if (chunk_next >= chunk_end && !exhausted) {
+                unsigned long long s0 = 0;
+                if (lane == 0) s0 = atomicAdd(counter, (unsigned long long)kChunk);
+                s0 = __shfl_sync(kFull, s0, 0);
+                if ((int64_t)s0 >= nq) {
+                    exhausted = true;
+                } else {
+                    chunk_next = (int64_t)s0;
+                    chunk_end = chunk_next + kChunk < nq ? chunk_next + kChunk : nq;
+                }
+            }
+            const int64_t slot = chunk_next + __popc(need & lt);
+            if (!active && slot < chunk_end) {
+                const int64_t q = order ? (int64_t)__ldg(order + slot) : slot;
+                base = __ldg(offsets + q);
+                kk = (int)(__ldg(offsets + q + 1) - base);
+                px = __ldg(centers + 3 * q);
+                py = __ldg(centers + 3 * q + 1);
+                pz = __ldg(centers + 3 * q + 2);
+                if (kk > 0) {
+                    if (t.n == 1) {
+                        const float d2 = box_dist_sq(px, py, pz, bx_of(t, 0), bx_of(t, 1),
+                                                     bx_of(t, 2), bx_of(t, 3), bx_of(t, 4),
+                                                     bx_of(t, 5));
+                        out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
+                        out_idx[base] = __ldg(t.leaf_obj);
+                    } else {
+                        top.init(kk, bounds ? __ldg(bounds + slot) : __int_as_float(0x7FFFFFFF));
+                        sp = 0;
+                        node = 0;
+                        active = true;
+                    }
+                }
+            }
+            const int64_t avail = chunk_end - chunk_next;
+            const int64_t took = __popc(need) < avail ? (int64_t)__popc(need) : avail;
+            chunk_next += took;
+        }
+        if (!__any_sync(kFull, active)) {
+            if (exhausted) break;
+            continue;
+        }
+        if (!active) continue;
+        // ---- one node of this lane's traversal (knn_kernel<K, true> step)
+        float4 a, b, c;
+        int4 dd;
+        load_node(nodes, node, a, b, c, dd);
+        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
+        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        const bool left_near = dl <= dr;
+        const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
+        const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
+        int32_t next = -1;
+        bool done = false;
+        if (!(fd > top.worst())) {
+            if (fl < 0) {
+                top.offer(fd, fl & 0x7FFFFFFF);
+            } else if (sp >= kStack) {
+                fail = LBVH_FLAG_STACK_EXHAUSTED;
+                done = true;
+            } else {
+                stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
+            }
+        }
+        if (!done && !(ndist > top.worst())) {
+            if (nl < 0) {
+                top.offer(ndist, nl & 0x7FFFFFFF);
+            } else if (sp >= kStack) {
+                fail = LBVH_FLAG_STACK_EXHAUSTED;
+                done = true;
+            } else {
+                next = nl;
+            }
+        }
+        if (!done && next < 0) {
+            while (sp > 0) {
+                const uint64_t e = stack[--sp];
+                if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
+                    next = (int32_t)(uint32_t)e;
+                    break;
+                }
+            }
+            if (next < 0) done = true;
+        }
+        if (!done) {
+            node = next;
+            continue;
+        }
+        // ---- query finished: write its span, go idle
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            if (j >= K - kk) {
+                const int64_t o = base + (j - (K - kk));
+                out_idx[o] = top.ordinal(j);
+                out_dist[o] = squared ? top.dist(j) : __fsqrt_rn(top.dist(j));
+            }
+        }
+        active = false;
+    }
+    if (fail) atomicOr(status, fail);
+}
+
 // General k: the output span doubles as a bounded max-heap, exactly the
 // reference's scheme (_kernels.py:299-325, 385-414).
 __device__ __forceinline__ bool worse(float d1, int32_t i1, float d2, int32_t i2) {
@@ -514,9 +679,47 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
     return check_launch();
 }
 
+size_t knn_workspace_bytes(int64_t nq) {
+    return align_up(sizeof(float) * (size_t)(nq > 0 ? nq : 1)) + 256;
+}
+
+template <int K>
+int launch_knn_persistent(const lbvh_tree *t, const float *centers, const uint32_t *order,
+                          const uint32_t *qcodes, int64_t nq, const int64_t *offsets,
+                          int32_t *out_idx, float *out_dist, bool squared, uint32_t *status,
+                          void *ws, cudaStream_t stream) {
+    Carve c(ws, knn_workspace_bytes(nq));
+    float *bounds = c.take<float>(nq);
+    unsigned long long *counter = (unsigned long long *)((char *)ws + knn_workspace_bytes(nq) - 64);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    const bool seed = qcodes && t->leaf_codes;
+    if (seed) {
+        knn_seed_kernel<K><<<div_up(nq, 256), 256, 0, stream>>>(*t, centers, order, qcodes, nq,
+                                                                offsets, bounds);
+        count_launches(1);
+    }
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_persistent_kernel<K>, 256, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    unsigned g = div_up(nq, 256);
+    const unsigned cap = (unsigned)(sms * per_sm);
+    g = g < cap ? g : cap;
+    knn_persistent_kernel<K><<<g, 256, 0, stream>>>(*t, centers, order, seed ? bounds : nullptr,
+                                                    nq, offsets, out_idx, out_dist, squared,
+                                                    status, counter);
+    count_launches(1);
+    return check_launch();
+}
+
 int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
-        int32_t *out_idx, float *out_dist, int flags, uint32_t *status, cudaStream_t stream) {
+        int32_t *out_idx, float *out_dist, int flags, void *ws, size_t ws_bytes,
+        uint32_t *status, cudaStream_t stream) {
     if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0 || max_span <= 0) return LBVH_OK;
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
@@ -525,9 +728,16 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     // 1 = nearer child kept in a register (measured faster with the seed),
     // 0 = reference push/pop per node.  Same results either way.
     static const int variant = env_int("LBVH_KNN_VARIANT", 1);
+    // 1 = persistent kernel with per-lane query refill (needs the workspace).
+    static const int persistent = env_int("LBVH_KNN_PERSISTENT", 1);
     if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
+    const bool use_persistent = persistent && ws && ws_bytes >= knn_workspace_bytes(nq);
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
+        if (use_persistent)                                                                 \
+            return launch_knn_persistent<KV>(t, centers, order, qcodes, nq, offsets,        \
+                                             out_idx, out_dist, squared, status, ws,        \
+                                             stream);                                       \
         if (variant == 1)                                                                   \
             knn_kernel<KV, true><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,     \
                                                         offsets, out_idx, out_dist, squared, \

@@ -444,9 +444,10 @@ def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultS
     out_idx = dv.empty(total, torch.int32)
     out_dist = dv.empty(total, torch.float32)
     ct = tree.ctree()
+    kws = dv.workspace(l.lbvh_knn_workspace_bytes(nq))
     _lib.check(_launch("knn", lambda: l.lbvh_knn(
         ct, dv.ptr(b.centers), dv.ptr(order), dv.ptr(qcodes), nq, dv.ptr(offsets), max_span,
-        dv.ptr(out_idx), dv.ptr(out_dist), flags, status.ptr, st)))
+        dv.ptr(out_idx), dv.ptr(out_dist), flags, dv.ptr(kws), kws.numel(), status.ptr, st)))
     offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
     return ResultSet._trusted(offsets, out_idx, out_dist)
 
@@ -478,6 +479,7 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> 
     order = dv.empty(chunk, torch.int32) if sort_queries else None
     qcodes = dv.empty(chunk, torch.int32) if sort_queries else None
     ws = dv.workspace(max(l.lbvh_query_workspace_bytes(chunk), l.lbvh_scan_workspace_bytes(nq)))
+    kws = dv.workspace(l.lbvh_knn_workspace_bytes(chunk))
     _lib.check(l.lbvh_knn_offsets(None, b.k, n, nq, dv.ptr(offsets), None, status.ptr,
                                   dv.ptr(ws), ws.numel(), comp.cuda_stream))
     ev = torch.cuda.Event()
@@ -504,8 +506,8 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> 
                                           dv.ptr(ws), ws.numel(), comp.cuda_stream))
         _lib.check(_launch("knn", lambda: l.lbvh_knn(
             ct, cc, dv.ptr(order) if srt else None, dv.ptr(qcodes) if srt else None, m,
-            o_ptr + 8 * c0, span, dv.ptr(out_idx), dv.ptr(out_dist), flags, status.ptr,
-            comp.cuda_stream)))
+            o_ptr + 8 * c0, span, dv.ptr(out_idx), dv.ptr(out_dist), flags, dv.ptr(kws),
+            kws.numel(), status.ptr, comp.cuda_stream)))
         e_c = torch.cuda.Event()
         e_c.record(comp)
         s_out.wait_event(e_c)
