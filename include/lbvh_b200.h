@@ -182,6 +182,12 @@ int lbvh_spatial_1p(const lbvh_tree *tree, const float *centers, const float *ra
                     float radius, const uint32_t *order, int64_t nq, int32_t *buf,
                     int64_t buffer_size, int32_t *counts, uint32_t *status, void *stream);
 
+/* Queries (taken in `order`, may be NULL) whose count exceeds buffer_size:
+ * written to list (u32 query ids), *list_len (device u32) = how many.  The
+ * fill pass then runs with order = list, nq = *list_len. */
+int lbvh_select_overflow(const uint32_t *order, const int32_t *counts, int64_t nq,
+                         int64_t buffer_size, uint32_t *list, uint32_t *list_len, void *stream);
+
 /* compact_rows  replaces _kernels.py:285-290.  Rows with counts[q] >
  * buffer_size are skipped (they did not fit; see lbvh_spatial_fill). */
 int lbvh_compact(const int32_t *buf, int64_t buffer_size, const int32_t *counts,

@@ -98,6 +98,8 @@ _SIGS = {
                   ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                   ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_select_overflow": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_unpack_knn_keys": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.c_void_p], ctypes.c_int),
     "lbvh_brute_knn": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,

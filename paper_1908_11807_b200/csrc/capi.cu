@@ -61,6 +61,8 @@ int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, in
         const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
         cudaStream_t);
 size_t knn_workspace_bytes(int64_t nq);
+int select_overflow(const uint32_t *, const int32_t *, int64_t, int64_t, uint32_t *, uint32_t *,
+                    cudaStream_t);
 int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
 int unpack_knn_keys(const uint64_t *, int64_t, int64_t *, float *, cudaStream_t);
 int brute_knn(const float *, int64_t, const float *, int64_t, int64_t, int32_t *, float *,
@@ -196,6 +198,11 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
 }
 
 size_t lbvh_knn_workspace_bytes(int64_t nq) { return knn_workspace_bytes(nq); }
+
+int lbvh_select_overflow(const uint32_t *order, const int32_t *counts, int64_t nq,
+                         int64_t buffer_size, uint32_t *list, uint32_t *list_len, void *stream) {
+    return select_overflow(order, counts, nq, buffer_size, list, list_len, S(stream));
+}
 
 int lbvh_unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *ordinals, float *dist,
                          void *stream) {

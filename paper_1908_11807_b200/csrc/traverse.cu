@@ -729,7 +729,9 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     // 0 = reference push/pop per node.  Same results either way.
     static const int variant = env_int("LBVH_KNN_VARIANT", 1);
     // 1 = persistent kernel with per-lane query refill (needs the workspace).
-    static const int persistent = env_int("LBVH_KNN_PERSISTENT", 1);
+    // Measured 1.7x slower on C2 (lanes drift apart in Morton order and lose
+    // L1 locality), so off by default; kept as an A/B variant.
+    static const int persistent = env_int("LBVH_KNN_PERSISTENT", 0);
     if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
     const bool use_persistent = persistent && ws && ws_bytes >= knn_workspace_bytes(nq);
 #define LBVH_KNN_CASE(KV)                                                                   \
@@ -774,6 +776,42 @@ unpack_knn_keys_kernel(const uint64_t *__restrict__ keys, int64_t n, int64_t *__
     }
 }
 }  // namespace
+
+namespace {
+// Queries whose hits overflowed their row, listed (in traversal order within
+// each warp) so the fill pass runs on full warps of them only.
+__global__ void __launch_bounds__(256)
+select_overflow_kernel(const uint32_t *__restrict__ order, const int32_t *__restrict__ counts,
+                       int64_t nq, int64_t cap, uint32_t *__restrict__ list, uint32_t *count) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t q = 0;
+    bool over = false;
+    if (s < nq) {
+        q = order ? __ldg(order + s) : (uint32_t)s;
+        over = __ldg(counts + q) > cap;
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, over);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    if (over) list[base + __popc(m & ((1u << lane) - 1u))] = q;
+}
+}  // namespace
+
+int select_overflow(const uint32_t *order, const int32_t *counts, int64_t nq, int64_t cap,
+                    uint32_t *list, uint32_t *count, cudaStream_t stream) {
+    if (nq < 0 || (nq > 0 && (!counts || !list || !count))) return LBVH_ERR_INVALID_ARG;
+    if (!count) return LBVH_ERR_INVALID_ARG;
+    cudaMemsetAsync(count, 0, sizeof(uint32_t), stream);
+    if (nq == 0) return check_launch();
+    select_overflow_kernel<<<div_up(nq, 256), 256, 0, stream>>>(order, counts, nq, cap, list,
+                                                                count);
+    count_launches(1);
+    return check_launch();
+}
 
 int unpack_knn_keys(const uint64_t *keys, int64_t n, int64_t *gid, float *dist,
                     cudaStream_t stream) {

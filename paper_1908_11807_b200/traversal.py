@@ -312,7 +312,7 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     st = dv.stream()
     nq = b.nq
     counts = dv.empty(nq, torch.int32)
-    rows = _ROW_HITS if nq * _ROW_HITS * 4 <= _ROW_BUDGET else 0
+    rows = next((r for r in (2 * _ROW_HITS, _ROW_HITS) if nq * r * 4 <= _ROW_BUDGET), 0)
     buf = dv.empty((nq, rows), torch.int32) if rows else None
     _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
         ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq, dv.ptr(counts),
@@ -321,7 +321,16 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
     _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
                                      ws.numel(), st))
-    flags, total = dv.d2h_many(status.dev, offsets[nq:])
+    if rows:
+        # queries whose hits did not fit their row, listed for a dense fill pass
+        over_list = dv.empty(nq, torch.int32)
+        over_n = dv.empty(1, torch.int32)
+        _lib.check(l.lbvh_select_overflow(dv.ptr(order), dv.ptr(counts), nq, rows,
+                                          dv.ptr(over_list), dv.ptr(over_n), st))
+        flags, total, n_over = dv.d2h_many(status.dev, offsets[nq:], over_n)
+        n_over = int(n_over[0])
+    else:
+        flags, total = dv.d2h_many(status.dev, offsets[nq:])
     _raise_flags(int(flags[0]) & 0xFFFFFFFF)
     total = int(total[0])
     out = dv.empty(total, torch.int32)
@@ -329,10 +338,14 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
         if rows:
             _lib.check(l.lbvh_compact(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), nq,
                                       dv.ptr(out), st))
-        _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
-            ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq,
-            dv.ptr(offsets), dv.ptr(out), dv.ptr(counts) if rows else None, rows, status.ptr,
-            st)))
+            if n_over:
+                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
+                    ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(over_list), n_over,
+                    dv.ptr(offsets), dv.ptr(out), None, 0, status.ptr, st)))
+        else:
+            _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
+                ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq,
+                dv.ptr(offsets), dv.ptr(out), None, 0, status.ptr, st)))
     return offsets, out
 
 
