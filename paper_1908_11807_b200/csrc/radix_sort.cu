@@ -20,7 +20,10 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kItems = 16;
+#ifndef LBVH_SORT_ITEMS
+#define LBVH_SORT_ITEMS 16
+#endif
+constexpr int kItems = LBVH_SORT_ITEMS;
 constexpr int kTile = kSortThreads * kItems;  // 4096
 constexpr int kMaxPasses = 4;
 
