@@ -140,10 +140,13 @@ int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
 
 /* query_sort_order(centers, scene)   replaces traversal.py:146-165.
  * order: nq u32 permutation.  scene_box: 6 floats DEVICE (tree root box).
- * sorted_codes (optional): the queries' Morton codes in `order` order. */
+ * sorted_codes (optional): the queries' Morton codes in `order` order.
+ * order_bits: sort by the top order_bits of the 30-bit code (stable; 30 =
+ * the reference's exact order).  Any order gives identical results; the
+ * traversal drivers use 24 bits (3 radix passes, same warp coherence). */
 size_t lbvh_query_workspace_bytes(int64_t nq);
 int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box,
-                     uint32_t *order, uint32_t *sorted_codes, void *workspace,
+                     int order_bits, uint32_t *order, uint32_t *sorted_codes, void *workspace,
                      size_t workspace_bytes, void *stream);
 
 /* Finite check of nq x 3 query centers and (optional) radii >= 0. */

@@ -69,9 +69,9 @@ _SIGS = {
                                             ctypes.c_void_p], ctypes.c_int),
     "lbvh_pack": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 4, ctypes.c_int),
     "lbvh_unpack_boxes": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 3, ctypes.c_int),
-    "lbvh_query_order": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
-                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
-                         ctypes.c_int),
+    "lbvh_query_order": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                          ctypes.c_void_p], ctypes.c_int),
     "lbvh_check_queries": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                             ctypes.c_void_p], ctypes.c_int),
     "lbvh_spatial_count": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,

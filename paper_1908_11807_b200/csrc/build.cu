@@ -527,9 +527,11 @@ size_t query_workspace_bytes(int64_t nq) {
     return align_up(sizeof(uint32_t) * (size_t)nq) + sort_workspace_bytes(nq) + 512;
 }
 
-int query_order(const float *centers, int64_t nq, const float *scene, uint32_t *order,
-                uint32_t *sorted_codes, void *ws, size_t ws_bytes, cudaStream_t stream) {
+int query_order(const float *centers, int64_t nq, const float *scene, int order_bits,
+                uint32_t *order, uint32_t *sorted_codes, void *ws, size_t ws_bytes,
+                cudaStream_t stream) {
     if (nq < 0 || (nq > 0 && (!centers || !order)) || !scene) return LBVH_ERR_INVALID_ARG;
+    if (order_bits < 1 || order_bits > 30) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     if (ws_bytes < query_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
@@ -538,7 +540,8 @@ int query_order(const float *centers, int64_t nq, const float *scene, uint32_t *
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
     morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq, scene, codes,
                                                              order); count_launches(1);
-    int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream);
+    int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
+                        30 - order_bits);
     if (rc != LBVH_OK) return rc;
     return check_launch();
 }

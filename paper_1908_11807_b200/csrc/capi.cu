@@ -44,8 +44,8 @@ int unpack_boxes(const lbvh_tree *, float *, float *, cudaStream_t);
 int morton_codes_f64(const double *, int64_t, const double *, const double *, uint32_t *,
                      cudaStream_t);
 size_t query_workspace_bytes(int64_t nq);
-int query_order(const float *, int64_t, const float *, uint32_t *, uint32_t *, void *, size_t,
-                cudaStream_t);
+int query_order(const float *, int64_t, const float *, int, uint32_t *, uint32_t *, void *,
+                size_t, cudaStream_t);
 int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
                   int64_t, int32_t *, int32_t *, int64_t, uint32_t *, cudaStream_t);
 int spatial_fill(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
@@ -141,9 +141,11 @@ int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
     return unpack_boxes(tree, node_mins, node_maxs, S(stream));
 }
 
-int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box, uint32_t *order,
-                     uint32_t *sorted_codes, void *ws, size_t ws_bytes, void *stream) {
-    return query_order(centers, nq, scene_box, order, sorted_codes, ws, ws_bytes, S(stream));
+int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box, int order_bits,
+                     uint32_t *order, uint32_t *sorted_codes, void *ws, size_t ws_bytes,
+                     void *stream) {
+    return query_order(centers, nq, scene_box, order_bits, order, sorted_codes, ws, ws_bytes,
+                       S(stream));
 }
 
 int lbvh_check_queries(const float *centers, int64_t nq, const float *radii, uint32_t *status,

@@ -15,8 +15,9 @@ void count_launches(int k);
 uint64_t launch_count();
 
 size_t sort_workspace_bytes(int64_t n);
+// Stable LSD sort on key bits [first_bit, key_bits).
 int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
-               size_t ws_bytes, cudaStream_t stream);
+               size_t ws_bytes, cudaStream_t stream, int first_bit = 0);
 
 size_t scan_workspace_bytes(int64_t n);
 // offsets[0] = 0, offsets[i+1] = offsets[i] + f(i); f reads counts (i32) or

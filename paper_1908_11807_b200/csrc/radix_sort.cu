@@ -36,7 +36,7 @@ constexpr int kHistItems = 16;
 
 // Digit histograms of every pass in one read of the keys.
 __global__ void __launch_bounds__(kHistThreads)
-histogram_kernel(const uint32_t *__restrict__ keys, int64_t n, int passes,
+histogram_kernel(const uint32_t *__restrict__ keys, int64_t n, int passes, int first_bit,
                  uint32_t *__restrict__ hist) {
     __shared__ uint32_t s_hist[kMaxPasses][kRadix];
     for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x)
@@ -48,7 +48,7 @@ histogram_kernel(const uint32_t *__restrict__ keys, int64_t n, int passes,
         if (i < n) {
             uint32_t k = __ldcs(keys + i);
             for (int p = 0; p < passes; ++p)
-                atomicAdd(&s_hist[p][(k >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+                atomicAdd(&s_hist[p][(k >> (first_bit + p * kRadixBits)) & (kRadix - 1)], 1u);
         }
     }
     __syncthreads();
@@ -227,12 +227,13 @@ size_t sort_workspace_bytes(int64_t n) {
 }
 
 int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
-               size_t ws_bytes, cudaStream_t stream) {
+               size_t ws_bytes, cudaStream_t stream, int first_bit) {
     if (n <= 1) return LBVH_OK;
     if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
-    if (key_bits < 1 || key_bits > 32) return LBVH_ERR_INVALID_ARG;
+    if (key_bits < 1 || key_bits > 32 || first_bit < 0 || first_bit >= key_bits)
+        return LBVH_ERR_INVALID_ARG;
     if (ws_bytes < sort_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
-    const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
+    const int passes = (key_bits - first_bit + kRadixBits - 1) / kRadixBits;
     const int64_t tiles = (n + kTile - 1) / kTile;
     Carve c(ws, ws_bytes);
     uint32_t *k_alt = c.take<uint32_t>(n);
@@ -246,13 +247,14 @@ int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws
     cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
-    histogram_kernel<<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, hist); count_launches(1);
+    histogram_kernel<<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, first_bit, hist);
+    count_launches(1);
     exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes); count_launches(1);
 
     uint32_t *ks = keys, *vs = vals, *kd = k_alt, *vd = v_alt;
     for (int p = 0; p < passes; ++p) {
         onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, stream>>>(
-            ks, vs, kd, vd, n, p * kRadixBits, hist + p * kRadix,
+            ks, vs, kd, vd, n, first_bit + p * kRadixBits, hist + p * kRadix,
             lookback + (size_t)p * tiles * kRadix, counters + p); count_launches(1);
         uint32_t *t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
