@@ -214,8 +214,11 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
     return best[K - 1];
 }
 
+#ifndef LBVH_KNN_MINBLOCKS
+#define LBVH_KNN_MINBLOCKS 1
+#endif
 template <int K, bool REGNEXT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, LBVH_KNN_MINBLOCKS)
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
            const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
