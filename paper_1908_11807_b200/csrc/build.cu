@@ -169,7 +169,7 @@ hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict_
                  uint32_t *slots, float *node_mins, float *node_maxs, int32_t *__restrict__ left,
                  int32_t *__restrict__ right, int32_t *__restrict__ parent,
                  int32_t *__restrict__ leaf_obj, PackedNode *__restrict__ nodes,
-                 float *__restrict__ root_box, bool buckets) {
+                 float *__restrict__ root_box) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int64_t internal = n - 1;
@@ -249,16 +249,8 @@ hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict_
                 P.lo[a] = min_left(L.lo[a], R.lo[a]);
                 P.hi[a] = max_left(L.hi[a], R.hi[a]);
             }
-            int32_t lk = left_side ? my_link : sib_link;
-            int32_t rk = left_side ? sib_link : my_link;
-            if (buckets) {
-                // children covering 2..kBucket leaves become leaf buckets: the
-                // traversal scans those leaves directly (sorted positions)
-                const int64_t ls = g - pl + 1, rs = pr - g;
-                if (ls > 1 && ls <= kBucket) lk = bucket_link(pl, ls);
-                if (rs > 1 && rs <= kBucket) rk = bucket_link(g + 1, rs);
-            }
-            store_packed(nodes, pid, L, R, lk, rk);
+            store_packed(nodes, pid, L, R, left_side ? my_link : sib_link,
+                         left_side ? sib_link : my_link);
             if (!ROWS_LATE) store_box(node_mins, node_maxs, pid, P);
             mine = P;
             my_link = (int32_t)pid;
@@ -452,20 +444,17 @@ int build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_b
     // 1 (measured 15% faster at 1e7): sibling boxes from packed records,
     // internal reference rows in a separate coalesced pass.
     static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 1);
-    // Leaf buckets in the traversal layout (bucket start needs 28 bits).
-    static const int use_buckets = env_int("LBVH_BUCKETS", 1);
-    const bool buckets = use_buckets && n <= kMaxBucketLeaves;
     if (rows_late && n > 1) {
         hierarchy_kernel<true, true><<<div_up(n, 256), 256, 0, stream>>>(
             codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-            leaf_obj, (PackedNode *)nodes, root_box, buckets);
+            leaf_obj, (PackedNode *)nodes, root_box);
         internal_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
             (const PackedNode *)nodes, n - 1, node_mins, node_maxs);
         count_launches(2);
     } else {
         hierarchy_kernel<true><<<div_up(n, 256), 256, 0, stream>>>(
             codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-            leaf_obj, (PackedNode *)nodes, root_box, buckets);
+            leaf_obj, (PackedNode *)nodes, root_box);
         count_launches(1);
     }
     if (sorted_codes)
@@ -488,7 +477,7 @@ int generate_topology(const uint32_t *codes, int64_t n, int32_t *left, int32_t *
     cudaMemsetAsync(slots, 0, sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1), stream);
     hierarchy_kernel<false><<<div_up(n, 256), 256, 0, stream>>>(
         codes, nullptr, nullptr, nullptr, n, slots, nullptr, nullptr, left, right, parent,
-        nullptr, nullptr, nullptr, false); count_launches(1);
+        nullptr, nullptr, nullptr); count_launches(1);
     return check_launch();
 }
 

@@ -10,28 +10,7 @@
 namespace lbvh {
 
 constexpr int kStack = LBVH_STACK_CAPACITY;
-// Child links in the traversal layout:
-//   >= 0                 internal node ordinal
-//   0b10 | obj (30 bit)  leaf, original object ordinal
-//   0b11 | start << 2 | count-1
-//                        leaf bucket: sorted leaf positions start..start+count-1
-//                        (count <= kBucket), set by build() for children that
-//                        cover 2..kBucket leaves; the traversal scans them.
 constexpr uint32_t kLeafTag = 0x80000000u;
-constexpr uint32_t kBucketTag = 0xC0000000u;
-constexpr int kBucket = 4;
-constexpr int64_t kMaxBucketLeaves = (int64_t)1 << 28;
-
-__host__ __device__ __forceinline__ int32_t bucket_link(int64_t start, int64_t count) {
-    return (int32_t)(kBucketTag | ((uint32_t)start << 2) | (uint32_t)(count - 1));
-}
-__device__ __forceinline__ bool is_bucket(int32_t link) {
-    return ((uint32_t)link & kBucketTag) == kBucketTag;
-}
-__device__ __forceinline__ int64_t bucket_start(int32_t link) {
-    return (int64_t)(((uint32_t)link & 0x3FFFFFFFu) >> 2);
-}
-__device__ __forceinline__ int bucket_count(int32_t link) { return ((uint32_t)link & 3u) + 1; }
 constexpr int kNumSMs = 148;  // B200
 
 // Traversal layout of one internal node: both child boxes + both links,

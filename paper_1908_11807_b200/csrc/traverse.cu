@@ -68,31 +68,6 @@ __device__ __forceinline__ bool emit(int32_t *__restrict__ out, int64_t base, in
     return true;
 }
 
-// Squared distance to the leaf at sorted position p (reference layout row).
-__device__ __forceinline__ float leaf_dist_sq(const lbvh_tree &t, int64_t p, float px, float py,
-                                              float pz) {
-    const float *mn = t.node_mins + 3 * (t.n - 1 + p);
-    const float *mx = t.node_maxs + 3 * (t.n - 1 + p);
-    return box_dist_sq(px, py, pz, __ldg(mn), __ldg(mn + 1), __ldg(mn + 2), __ldg(mx),
-                       __ldg(mx + 1), __ldg(mx + 2));
-}
-
-// A passing leaf or leaf-bucket child of a radius query: emit its hit(s).
-// Returns false when a 1P row overflows.
-template <int MODE>
-__device__ __forceinline__ bool emit_link(const lbvh_tree &t, int32_t link, float px, float py,
-                                          float pz, float r2, int32_t *__restrict__ out,
-                                          int64_t base, int32_t &cnt, int64_t cap) {
-    if (!is_bucket(link)) return emit<MODE>(out, base, cnt, cap, link & 0x7FFFFFFF);
-    const int64_t s0 = bucket_start(link);
-    const int c = bucket_count(link);
-    for (int j = 0; j < c; ++j)
-        if (leaf_dist_sq(t, s0 + j, px, py, pz) <= r2 &&
-            !emit<MODE>(out, base, cnt, cap, __ldg(t.leaf_obj + s0 + j)))
-            return false;
-    return true;
-}
-
 // `skip` (kFill only, optional): counts of a kCountBuf pass; queries whose
 // hits all fit in its rows (count <= cap) are skipped -- the compaction
 // kernel copies those.
@@ -143,7 +118,7 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         // left child, then right child (_kernels.py:212-225)
         if (dl <= r2) {
             if (d.x < 0) {
-                if (!emit_link<MODE>(t, d.x, px, py, pz, r2, out, base, cnt, cap)) {
+                if (!emit<MODE>(out, base, cnt, cap, d.x & 0x7FFFFFFF)) {
                     fail = LBVH_FLAG_BUFFER_OVERFLOW;
                     break;
                 }
@@ -157,7 +132,7 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         }
         if (dr <= r2) {
             if (d.y < 0) {
-                if (!emit_link<MODE>(t, d.y, px, py, pz, r2, out, base, cnt, cap)) {
+                if (!emit<MODE>(out, base, cnt, cap, d.y & 0x7FFFFFFF)) {
                     fail = LBVH_FLAG_BUFFER_OVERFLOW;
                     break;
                 }
@@ -195,23 +170,6 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
     for (int j = lane; j < cnt; j += 32) out[dst + j] = __ldcs(row + j);
 }
 
-
-// A kNN leaf or leaf-bucket child that survived the prune test: offer its
-// object(s) (_kernels.py:385-395); bucket leaves are tested one by one.
-template <int K>
-__device__ __forceinline__ void offer_link(TopK<K> &top, const lbvh_tree &t, int32_t link,
-                                           float cd, float px, float py, float pz) {
-    if (!is_bucket(link)) {
-        top.offer(cd, link & 0x7FFFFFFF);
-        return;
-    }
-    const int64_t s0 = bucket_start(link);
-    const int c = bucket_count(link);
-    for (int j = 0; j < c; ++j) {
-        const float d = leaf_dist_sq(t, s0 + j, px, py, pz);
-        if (!(d > top.worst())) top.offer(d, __ldg(t.leaf_obj + s0 + j));
-    }
-}
 
 // Search-radius seed for one query: the kk-th smallest distance^2 among the
 // 2*kk leaves that neighbour the query's Morton code in leaf order (a real
@@ -324,7 +282,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         int32_t next = -1;
         if (!(fd > top.worst())) {  // NaN worst = list not full yet
             if (fl < 0) {
-                offer_link(top, t, fl, fd, px, py, pz);
+                top.offer(fd, fl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
@@ -335,7 +293,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         }
         if (!(ndist > top.worst())) {
             if (nl < 0) {
-                offer_link(top, t, nl, ndist, px, py, pz);
+                top.offer(ndist, nl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
@@ -493,7 +451,7 @@ knn_persistent_kernel(const lbvh_tree t, const float *__restrict__ centers,
         bool done = false;
         if (!(fd > top.worst())) {
             if (fl < 0) {
-                offer_link(top, t, fl, fd, px, py, pz);
+                top.offer(fd, fl & 0x7FFFFFFF);
             } else if (sp >= kStack) {
                 fail = LBVH_FLAG_STACK_EXHAUSTED;
                 done = true;
@@ -503,7 +461,7 @@ knn_persistent_kernel(const lbvh_tree t, const float *__restrict__ centers,
         }
         if (!done && !(ndist > top.worst())) {
             if (nl < 0) {
-                offer_link(top, t, nl, ndist, px, py, pz);
+                top.offer(ndist, nl & 0x7FFFFFFF);
             } else if (sp >= kStack) {
                 fail = LBVH_FLAG_STACK_EXHAUSTED;
                 done = true;
@@ -615,30 +573,16 @@ knn_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
             const float cd = pick == 0 ? fd : ndist;
             if (size == kk && cd > hd[0]) continue;
             if (link < 0) {
-                const bool bucket = is_bucket(link);
-                const int c = bucket ? bucket_count(link) : 1;
-                for (int j = 0; j < c; ++j) {
-                    int32_t obj;
-                    float dj;
-                    if (bucket) {
-                        const int64_t p = bucket_start(link) + j;
-                        dj = leaf_dist_sq(t, p, px, py, pz);
-                        if (size == kk && dj > hd[0]) continue;
-                        obj = __ldg(t.leaf_obj + p);
-                    } else {
-                        dj = cd;
-                        obj = link & 0x7FFFFFFF;
-                    }
-                    if (size < kk) {
-                        hd[size] = dj;
-                        hi[size] = obj;
-                        ++size;
-                        sift_up(hd, hi, size - 1);
-                    } else if (worse(hd[0], hi[0], dj, obj)) {
-                        hd[0] = dj;
-                        hi[0] = obj;
-                        sift_down(hd, hi, kk, 0);
-                    }
+                const int32_t obj = link & 0x7FFFFFFF;
+                if (size < kk) {
+                    hd[size] = cd;
+                    hi[size] = obj;
+                    ++size;
+                    sift_up(hd, hi, size - 1);
+                } else if (worse(hd[0], hi[0], cd, obj)) {
+                    hd[0] = cd;
+                    hi[0] = obj;
+                    sift_down(hd, hi, kk, 0);
                 }
             } else {
                 if (sp >= kStack) {
