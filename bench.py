@@ -73,6 +73,8 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--cpu-sample", type=int, default=1_000_000,
                    help="queries in the CPU baseline sample")
+    p.add_argument("--sweep-max", type=int, default=100_000_000,
+                   help="largest n of the C5 construction sweep")
     p.add_argument("--profile", action="store_true",
                    help="short run for ncu: no clocks/cpu/e2e/extra legs")
     return p.parse_args(argv)
@@ -462,7 +464,29 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
     tot, _, _ = timed_loop(c3_step, steps, warm)
     ex["c3_hollow_radius_2p_queries_per_sec"] = round(world * nq * steps / (tot / 1e3), 1)
     ex["c3_mean_hits"] = round(float(counts_box["h"]) / nq, 3)
+
+    # kNN against the hollow sphere (the reference replay needs ~6,000 box
+    # tests per query here): a stress case for the search bound
+    def c3_knn_step():
+        return lb.query_knn(htree, (qs_d, args.k))
+
+    tot, _, _ = timed_loop(c3_knn_step, 2, 1)
+    ex["c3_hollow_knn_queries_per_sec"] = round(world * nq * 2 / (tot / 1e3), 1)
     del htree, hs_d
+
+    # C5: construction-only sweep, filled cube seed 0 (device-resident input)
+    sweep = {}
+    for n_b in (10_000, 100_000, 1_000_000, 10_000_000, 100_000_000):
+        if n_b > args.sweep_max:
+            break
+        p_b = torch.from_numpy(lb.generate(lb.CloudSpec("cube", "filled", n_b, 0))).to(dev)
+        reps = 10 if n_b <= 1_000_000 else 3
+        tot, _, _ = timed_loop(lambda: lb.build(p_b), reps, 2)
+        sweep[str(n_b)] = {"ms": round(tot / reps, 4),
+                           "prims_per_sec": round(n_b * reps / (tot / 1e3), 1)}
+        del p_b
+        torch.cuda.empty_cache()
+    ex["c5_build_sweep"] = sweep
     return ex
 
 
