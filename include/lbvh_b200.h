@@ -95,12 +95,16 @@ size_t lbvh_sort_workspace_bytes(int64_t n);
  * mins, maxs: n x 3 f32 (maxs may equal mins for point input).
  * Outputs: node_mins/node_maxs (2n-1)x3, left/right (n-1), leaf_obj n,
  * root_box 6 floats (== scene box), nodes (n-1) x 64 B, status word.
- * sorted_codes (optional, may be NULL): n u32 Morton codes in leaf order.
+ * sorted_codes (optional, may be NULL): n u32 30-bit Morton codes in leaf order.
+ * morton_bits: 30 = the reference's codes (bit-exact tree); 63 = 21 bits per
+ * axis, the same recipe (north_star "30/63-bit"; not in the reference, so
+ * its parity is pinned only by the oracle restatement).  Leaves are then
+ * ordered by (63-bit code, index), finer for very large clouds.
  */
-int lbvh_build(const float *mins, const float *maxs, int64_t n, void *workspace,
-               size_t workspace_bytes, float *node_mins, float *node_maxs, int32_t *left,
-               int32_t *right, int32_t *leaf_obj, float *root_box, void *nodes,
-               uint32_t *sorted_codes, uint32_t *status, void *stream);
+int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
+               void *workspace, size_t workspace_bytes, float *node_mins, float *node_maxs,
+               int32_t *left, int32_t *right, int32_t *leaf_obj, float *root_box,
+               void *nodes, uint32_t *sorted_codes, uint32_t *status, void *stream);
 
 /* morton_codes(points, scene_min, scene_max)   replaces morton.py:68-91
  * points n x 3 f64 (device); scene bounds host doubles (smin[3], smax[3]). */

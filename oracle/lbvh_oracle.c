@@ -461,3 +461,138 @@ int orc_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------ */
+/* 63-bit Morton build (north_star "30/63-bit"; NOT in the reference,  */
+/* which is 30-bit only).  Same recipe at 21 bits/axis:   */
+/* f64 normalise, clip, floor(t * 2^21) clamped to 2^21 - 1, x-major   */
+/* interleave; Karras topology over (code, position) keys.  Parity of  */
+/* this path is pinned only by this restatement (no reference output). */
+/* ------------------------------------------------------------------ */
+
+static inline uint64_t spread21(uint64_t v) {
+    v &= 0x1FFFFFull;
+    v = (v | (v << 32)) & 0x1F00000000FFFFull;
+    v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+    v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+    v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+static inline uint64_t grid21(double c, double lo, double ext) {
+    double t = 0.0;
+    if (ext > 0.0) t = (c - lo) / ext;
+    if (t < 0.0) t = 0.0;
+    if (t > 1.0) t = 1.0;
+    uint64_t g = (uint64_t)(t * 2097152.0);
+    return g < 2097151ull ? g : 2097151ull;
+}
+
+void orc_morton63_codes(const double *pts, int64_t n, const double *smin, const double *smax,
+                        uint64_t *codes, int threads) {
+    double ext[3] = {smax[0] - smin[0], smax[1] - smin[1], smax[2] - smin[2]};
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        codes[i] = (spread21(grid21(pts[3 * i], smin[0], ext[0])) << 2) |
+                   (spread21(grid21(pts[3 * i + 1], smin[1], ext[1])) << 1) |
+                   spread21(grid21(pts[3 * i + 2], smin[2], ext[2]));
+}
+
+static int cmp_code64(const void *a, const void *b) {
+    const uint64_t *x = (const uint64_t *)a, *y = (const uint64_t *)b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return x[1] < y[1] ? -1 : (x[1] > y[1]);
+}
+
+/* stable argsort of 64-bit codes == sort of (code, index) pairs */
+void orc_sort_perm64(const uint64_t *codes, int64_t n, int64_t *perm) {
+    uint64_t *kv = (uint64_t *)malloc(sizeof(uint64_t) * 2 * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) { kv[2 * i] = codes[i]; kv[2 * i + 1] = (uint64_t)i; }
+    qsort(kv, (size_t)n, 2 * sizeof(uint64_t), cmp_code64);
+    for (int64_t i = 0; i < n; ++i) perm[i] = (int64_t)kv[2 * i + 1];
+    free(kv);
+}
+
+static inline int prefix64(const uint64_t *c, int64_t n, int64_t i, int64_t j) {
+    if (j < 0 || j >= n) return -1;
+    if (c[i] != c[j]) return __builtin_clzll(c[i] ^ c[j]);
+    return 64 + __builtin_clz((uint32_t)(i ^ j));
+}
+
+static int64_t find_split64(const uint64_t *c, int64_t n, int64_t first, int64_t last) {
+    int common = prefix64(c, n, first, last);
+    int64_t split = first, step = last - first;
+    for (;;) {
+        step = (step + 1) >> 1;
+        int64_t cand = split + step;
+        if (cand < last && prefix64(c, n, first, cand) > common) split = cand;
+        if (step <= 1) break;
+    }
+    return split;
+}
+
+void orc_generate_topology64(const uint64_t *c, int64_t n, int32_t *left, int32_t *right,
+                             int32_t *parent, int threads) {
+    for (int64_t i = 0; i < n - 1; ++i) left[i] = right[i] = -1;
+    for (int64_t i = 0; i < 2 * n - 1; ++i) parent[i] = -1;
+    if (n < 2) return;
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n - 1; ++i) {
+        int64_t d = prefix64(c, n, i, i + 1) > prefix64(c, n, i, i - 1) ? 1 : -1;
+        int floor_ = prefix64(c, n, i, i - d);
+        int64_t span_max = 2;
+        while (prefix64(c, n, i, i + span_max * d) > floor_) span_max <<= 1;
+        int64_t span = 0;
+        for (int64_t t = span_max >> 1; t >= 1; t >>= 1)
+            if (prefix64(c, n, i, i + (span + t) * d) > floor_) span += t;
+        int64_t j = i + span * d;
+        int64_t first = i < j ? i : j, last = i < j ? j : i;
+        int64_t g = find_split64(c, n, first, last);
+        int64_t lc = (g == first) ? (n - 1) + g : g;
+        int64_t rc = (g + 1 == last) ? (n - 1) + (g + 1) : g + 1;
+        left[i] = (int32_t)lc;
+        right[i] = (int32_t)rc;
+        parent[lc] = (int32_t)i;
+        parent[rc] = (int32_t)i;
+    }
+}
+
+int orc_build63(const float *mins, const float *maxs, int64_t n, float *node_mins,
+                float *node_maxs, int32_t *left, int32_t *right, int32_t *leaf_obj,
+                float *scene_min, float *scene_max, int threads) {
+    if (n < 1) return 1;
+    for (int a = 0; a < 3; ++a) { scene_min[a] = mins[a]; scene_max[a] = maxs[a]; }
+    for (int64_t i = 1; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            if (mins[3 * i + a] < scene_min[a]) scene_min[a] = mins[3 * i + a];
+            if (maxs[3 * i + a] > scene_max[a]) scene_max[a] = maxs[3 * i + a];
+        }
+    double *cent = (double *)malloc(sizeof(double) * 3 * (size_t)n);
+    for (int64_t i = 0; i < 3 * n; ++i) cent[i] = ((double)mins[i] + (double)maxs[i]) * 0.5;
+    double smin[3] = {scene_min[0], scene_min[1], scene_min[2]};
+    double smax[3] = {scene_max[0], scene_max[1], scene_max[2]};
+    uint64_t *codes = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n);
+    orc_morton63_codes(cent, n, smin, smax, codes, threads);
+    free(cent);
+    int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    orc_sort_perm64(codes, n, perm);
+    uint64_t *sorted = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n);
+    for (int64_t p = 0; p < n; ++p) {
+        int64_t o = perm[p];
+        sorted[p] = codes[o];
+        leaf_obj[p] = (int32_t)o;
+        for (int a = 0; a < 3; ++a) {
+            node_mins[3 * ((n - 1) + p) + a] = mins[3 * o + a];
+            node_maxs[3 * ((n - 1) + p) + a] = maxs[3 * o + a];
+        }
+    }
+    free(codes);
+    free(perm);
+    int32_t *parent = (int32_t *)malloc(sizeof(int32_t) * (size_t)(2 * n - 1));
+    orc_generate_topology64(sorted, n, left, right, parent, threads);
+    orc_refit(node_mins, node_maxs, left, right, parent, n);
+    free(parent);
+    free(sorted);
+    return 0;
+}

@@ -57,8 +57,8 @@ _SIGS = {
     "lbvh_topology_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_query_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_scan_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
-    "lbvh_build": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
-                    ctypes.c_size_t] + [ctypes.c_void_p] * 10, ctypes.c_int),
+    "lbvh_build": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                    ctypes.c_void_p, ctypes.c_size_t] + [ctypes.c_void_p] * 10, ctypes.c_int),
     "lbvh_morton_codes": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_sort_pairs": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,

@@ -92,10 +92,21 @@ scene_reduce_kernel(const float *__restrict__ mins, const float *__restrict__ ma
     }
 }
 
+__device__ __forceinline__ void encode(double x, double y, double z, const double *lo,
+                                       const double *ext, uint32_t &out) {
+    out = morton3(x, y, z, lo, ext);
+}
+__device__ __forceinline__ void encode(double x, double y, double z, const double *lo,
+                                       const double *ext, uint64_t &out) {
+    out = morton63(x, y, z, lo, ext);
+}
+
 // K2: codes of the f64 box centroids on the scene grid, plus iota values.
+// CodeT = uint32_t: the reference's 30-bit codes; uint64_t: 63-bit codes.
+template <typename CodeT>
 __global__ void __launch_bounds__(256)
 morton_kernel(const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
-              const float *__restrict__ scene, uint32_t *__restrict__ codes,
+              const float *__restrict__ scene, CodeT *__restrict__ codes,
               uint32_t *__restrict__ iota) {
     double lo[3], ext[3];
 #pragma unroll
@@ -113,7 +124,9 @@ morton_kernel(const float *__restrict__ mins, const float *__restrict__ maxs, in
                                        (double)__ldg(maxs + 3 * i + a)),
                              0.5);
         }
-        codes[i] = morton3(c[0], c[1], c[2], lo, ext);
+        CodeT code;
+        encode(c[0], c[1], c[2], lo, ext, code);
+        codes[i] = code;
         if (iota) iota[i] = (uint32_t)i;
     }
 }
@@ -126,8 +139,16 @@ __device__ __forceinline__ int delta(const uint32_t *__restrict__ codes, int64_t
     return 32 + __clz((uint32_t)i ^ (uint32_t)(i + 1));
 }
 
+// 63-bit codes: keys (code, position) compare on 64 code bits first.
+__device__ __forceinline__ int delta(const uint64_t *__restrict__ codes, int64_t i) {
+    uint64_t a = __ldg(codes + i), b = __ldg(codes + i + 1);
+    if (a != b) return __clzll(a ^ b);
+    return 64 + __clz((uint32_t)i ^ (uint32_t)(i + 1));
+}
+
 // Is [l, r] the left child of its parent?  Boundary prefixes are never equal.
-__device__ __forceinline__ bool is_left_child(const uint32_t *__restrict__ codes, int64_t n,
+template <typename CodeT>
+__device__ __forceinline__ bool is_left_child(const CodeT *__restrict__ codes, int64_t n,
                                               int64_t l, int64_t r) {
     if (l == 0) return true;
     if (r == n - 1) return false;
@@ -162,19 +183,25 @@ __device__ __forceinline__ void store_packed(PackedNode *nodes, int64_t id, cons
 
 // K4 + K5.  WITH_BOXES=false is the topology-only variant behind
 // lbvh_generate_topology (sorted codes in, left/right/parent out).
-template <bool WITH_BOXES, bool ROWS_LATE = false>
+// leaf_codes (optional): the 30-bit code of every leaf in leaf order (for
+// 63-bit codes the top 30 bits, which are exactly the 30-bit code).
+__device__ __forceinline__ uint32_t code30(uint32_t c) { return c; }
+__device__ __forceinline__ uint32_t code30(uint64_t c) { return (uint32_t)(c >> 33); }
+
+template <bool WITH_BOXES, bool ROWS_LATE = false, typename CodeT = uint32_t>
 __global__ void __launch_bounds__(256)
-hierarchy_kernel(const uint32_t *__restrict__ codes, const uint32_t *__restrict__ perm,
+hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
                  const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
                  uint32_t *slots, float *node_mins, float *node_maxs, int32_t *__restrict__ left,
                  int32_t *__restrict__ right, int32_t *__restrict__ parent,
                  int32_t *__restrict__ leaf_obj, PackedNode *__restrict__ nodes,
-                 float *__restrict__ root_box) {
+                 float *__restrict__ root_box, uint32_t *__restrict__ leaf_codes) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int64_t internal = n - 1;
     Box mine;
     int32_t my_link = 0;  // packed-layout link of the current node
+    if (leaf_codes) leaf_codes[p] = code30(__ldg(codes + p));
     if (WITH_BOXES) {
         const uint32_t obj = __ldg(perm + p);
         leaf_obj[p] = (int32_t)obj;
@@ -402,65 +429,88 @@ unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
 // ----------------------------------------------------------------- host API
 
 size_t build_workspace_bytes(int64_t n) {
+    // sized for the wider (63-bit) pipeline so one size serves both
     size_t b = 0;
-    b += align_up(sizeof(uint32_t) * (size_t)n) * 2;             // codes + perm
+    b += align_up(sizeof(uint64_t) * (size_t)n) + align_up(sizeof(uint32_t) * (size_t)n);
     b += align_up(sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1));  // handshake slots
     b += align_up(sizeof(float) * 6 * kNumSMs * 8);              // reduce partials
     b += align_up(sizeof(uint32_t) * 4);                         // reduce counter
-    b += sort_workspace_bytes(n);
+    size_t s32 = sort_workspace_bytes(n), s64 = sort64_workspace_bytes(n);
+    b += s32 > s64 ? s32 : s64;
     return b + 1024;
 }
 
-int build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
-          float *node_mins, float *node_maxs, int32_t *left, int32_t *right, int32_t *leaf_obj,
-          float *root_box, void *nodes, uint32_t *sorted_codes, uint32_t *status,
-          cudaStream_t stream) {
-    if (n == 0) return LBVH_ERR_EMPTY_SCENE;
-    if (n < 0 || !mins || !maxs || !node_mins || !node_maxs || !leaf_obj || !root_box ||
-        !status)
-        return LBVH_ERR_INVALID_ARG;
-    if (n > 1 && (!left || !right || !nodes)) return LBVH_ERR_INVALID_ARG;
-    if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
-    if (ws_bytes < build_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+namespace {
+int sort_codes(uint32_t *codes, uint32_t *perm, int64_t n, void *ws, cudaStream_t st) {
+    return sort_pairs(codes, perm, n, 30, ws, sort_workspace_bytes(n), st);
+}
+int sort_codes(uint64_t *codes, uint32_t *perm, int64_t n, void *ws, cudaStream_t st) {
+    return sort_pairs64(codes, perm, n, 63, ws, sort64_workspace_bytes(n), st);
+}
+
+template <typename CodeT>
+int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
+               float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
+               int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
+               uint32_t *status, cudaStream_t stream) {
     Carve c(ws, ws_bytes);
-    uint32_t *codes = c.take<uint32_t>(n);
+    CodeT *codes = c.take<CodeT>(n);
     uint32_t *perm = c.take<uint32_t>(n);
     size_t zero_begin = align_up(c.off);
     uint32_t *slots = c.take<uint32_t>(n > 1 ? n - 1 : 1);
     uint32_t *counter = c.take<uint32_t>(4);
     size_t zero_end = c.off;
     float *partials = c.take<float>(6 * kNumSMs * 8);
-    void *sort_ws = c.take<char>(sort_workspace_bytes(n));
+    void *sort_ws = c.take<char>(sizeof(CodeT) == 4 ? sort_workspace_bytes(n)
+                                                    : sort64_workspace_bytes(n));
     if (!c.ok()) return LBVH_ERR_WORKSPACE;
     cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned rg = grid_for(n, kReduceThreads, 4);
     scene_reduce_kernel<<<rg, kReduceThreads, 0, stream>>>(mins, maxs, n, partials, counter,
-                                                           root_box, status); count_launches(1);
+                                                           root_box, status);
     unsigned mg = grid_for(n, 256, 16);
-    morton_kernel<<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm); count_launches(1);
-    int rc = sort_pairs(codes, perm, n, 30, sort_ws, sort_workspace_bytes(n), stream);
+    morton_kernel<CodeT><<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm);
+    count_launches(2);
+    int rc = sort_codes(codes, perm, n, sort_ws, stream);
     if (rc != LBVH_OK) return rc;
     // 1 (measured 15% faster at 1e7): sibling boxes from packed records,
     // internal reference rows in a separate coalesced pass.
     static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 1);
     if (rows_late && n > 1) {
-        hierarchy_kernel<true, true><<<div_up(n, 256), 256, 0, stream>>>(
+        hierarchy_kernel<true, true, CodeT><<<div_up(n, 256), 256, 0, stream>>>(
             codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-            leaf_obj, (PackedNode *)nodes, root_box);
+            leaf_obj, (PackedNode *)nodes, root_box, sorted_codes);
         internal_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
             (const PackedNode *)nodes, n - 1, node_mins, node_maxs);
         count_launches(2);
     } else {
-        hierarchy_kernel<true><<<div_up(n, 256), 256, 0, stream>>>(
+        hierarchy_kernel<true, false, CodeT><<<div_up(n, 256), 256, 0, stream>>>(
             codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-            leaf_obj, (PackedNode *)nodes, root_box);
+            leaf_obj, (PackedNode *)nodes, root_box, sorted_codes);
         count_launches(1);
     }
-    if (sorted_codes)
-        cudaMemcpyAsync(sorted_codes, codes, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
-                        stream);
     return check_launch();
+}
+}  // namespace
+
+int build(const float *mins, const float *maxs, int64_t n, int morton_bits, void *ws,
+          size_t ws_bytes, float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
+          int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
+          uint32_t *status, cudaStream_t stream) {
+    if (n == 0) return LBVH_ERR_EMPTY_SCENE;
+    if (n < 0 || !mins || !maxs || !node_mins || !node_maxs || !leaf_obj || !root_box ||
+        !status || (morton_bits != 30 && morton_bits != 63))
+        return LBVH_ERR_INVALID_ARG;
+    if (n > 1 && (!left || !right || !nodes)) return LBVH_ERR_INVALID_ARG;
+    if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    if (ws_bytes < build_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+    if (morton_bits == 63)
+        return build_impl<uint64_t>(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left,
+                                    right, leaf_obj, root_box, nodes, sorted_codes, status,
+                                    stream);
+    return build_impl<uint32_t>(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left, right,
+                                leaf_obj, root_box, nodes, sorted_codes, status, stream);
 }
 
 size_t topology_workspace_bytes(int64_t n) {
@@ -477,7 +527,7 @@ int generate_topology(const uint32_t *codes, int64_t n, int32_t *left, int32_t *
     cudaMemsetAsync(slots, 0, sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1), stream);
     hierarchy_kernel<false><<<div_up(n, 256), 256, 0, stream>>>(
         codes, nullptr, nullptr, nullptr, n, slots, nullptr, nullptr, left, right, parent,
-        nullptr, nullptr, nullptr); count_launches(1);
+        nullptr, nullptr, nullptr, nullptr); count_launches(1);
     return check_launch();
 }
 
@@ -538,8 +588,9 @@ int query_order(const float *centers, int64_t nq, const float *scene, int order_
     Carve c(ws, ws_bytes);
     uint32_t *codes = sorted_codes ? sorted_codes : c.take<uint32_t>(nq);
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
-    morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq, scene, codes,
-                                                             order); count_launches(1);
+    morton_kernel<uint32_t><<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq,
+                                                                       scene, codes, order);
+    count_launches(1);
     int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
                         30 - order_bits);
     if (rc != LBVH_OK) return rc;

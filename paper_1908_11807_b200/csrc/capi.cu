@@ -32,8 +32,9 @@ int check_launch() {
 
 // defined in build.cu / traverse.cu / scan.cu
 size_t build_workspace_bytes(int64_t n);
-int build(const float *, const float *, int64_t, void *, size_t, float *, float *, int32_t *,
-          int32_t *, int32_t *, float *, void *, uint32_t *, uint32_t *, cudaStream_t);
+int build(const float *, const float *, int64_t, int, void *, size_t, float *, float *,
+          int32_t *, int32_t *, int32_t *, float *, void *, uint32_t *, uint32_t *,
+          cudaStream_t);
 size_t topology_workspace_bytes(int64_t n);
 int generate_topology(const uint32_t *, int64_t, int32_t *, int32_t *, int32_t *, void *, size_t,
                       cudaStream_t);
@@ -102,12 +103,12 @@ size_t lbvh_topology_workspace_bytes(int64_t n) { return topology_workspace_byte
 size_t lbvh_query_workspace_bytes(int64_t nq) { return query_workspace_bytes(nq); }
 size_t lbvh_scan_workspace_bytes(int64_t nq) { return scan_workspace_bytes(nq); }
 
-int lbvh_build(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
-               float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
-               int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
-               uint32_t *status, void *stream) {
-    return build(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left, right, leaf_obj,
-                 root_box, nodes, sorted_codes, status, S(stream));
+int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits, void *ws,
+               size_t ws_bytes, float *node_mins, float *node_maxs, int32_t *left,
+               int32_t *right, int32_t *leaf_obj, float *root_box, void *nodes,
+               uint32_t *sorted_codes, uint32_t *status, void *stream) {
+    return build(mins, maxs, n, morton_bits, ws, ws_bytes, node_mins, node_maxs, left, right,
+                 leaf_obj, root_box, nodes, sorted_codes, status, S(stream));
 }
 
 int lbvh_morton_codes(const double *pts, int64_t n, const double *lo, const double *hi,

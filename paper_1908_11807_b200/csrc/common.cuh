@@ -83,6 +83,33 @@ __device__ __forceinline__ uint32_t morton3(double x, double y, double z, const 
            spread_bits(grid_cell(z, lo[2], ext[2]));
 }
 
+// 63-bit codes (north_star "30/63-bit"; not in the reference):
+// the same recipe at 21 bits per axis, so code63 >> 33 == the 30-bit code.
+__device__ __forceinline__ uint64_t spread21(uint64_t v) {
+    v &= 0x1FFFFFull;
+    v = (v | (v << 32)) & 0x1F00000000FFFFull;
+    v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+    v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+    v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+__device__ __forceinline__ uint64_t grid21(double c, double lo, double ext) {
+    double t = 0.0;
+    if (ext > 0.0) t = __ddiv_rn(__dsub_rn(c, lo), ext);
+    t = t < 0.0 ? 0.0 : t;
+    t = t > 1.0 ? 1.0 : t;
+    uint64_t g = __double2ull_rz(__dmul_rn(t, 2097152.0));
+    return g < 2097151ull ? g : 2097151ull;
+}
+
+__device__ __forceinline__ uint64_t morton63(double x, double y, double z, const double *lo,
+                                             const double *ext) {
+    return (spread21(grid21(x, lo[0], ext[0])) << 2) | (spread21(grid21(y, lo[1], ext[1])) << 1) |
+           spread21(grid21(z, lo[2], ext[2]));
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // GPU-scope release+acquire read-modify-writes (no full membar).

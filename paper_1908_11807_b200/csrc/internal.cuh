@@ -18,6 +18,9 @@ size_t sort_workspace_bytes(int64_t n);
 // Stable LSD sort on key bits [first_bit, key_bits).
 int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                size_t ws_bytes, cudaStream_t stream, int first_bit = 0);
+size_t sort64_workspace_bytes(int64_t n);
+int sort_pairs64(uint64_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+                 size_t ws_bytes, cudaStream_t stream);
 
 size_t scan_workspace_bytes(int64_t n);
 // offsets[0] = 0, offsets[i+1] = offsets[i] + f(i); f reads counts (i32) or

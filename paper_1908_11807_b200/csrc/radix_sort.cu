@@ -1,14 +1,15 @@
-// radix_sort.cu -- stable LSD radix sort of (u32 key, u32 value) pairs.
+// radix_sort.cu -- stable LSD radix sort of (key, u32 value) pairs.
 //
 // Replaces np.argsort(codes, kind="stable") (reference tree.py:194,
 // traversal.py:159): sorting (code, index) pairs with a stable LSD sort gives
 // exactly the stable argsort.  One-sweep design (Adinets & Merrill): one
 // upfront pass builds the digit histograms of every digit position, then each
-// digit pass is a single kernel that ranks a 4096-key tile in shared memory,
-// resolves its global offsets with a decoupled look-back over preceding tiles
-// and scatters.  8-bit digits; the 30-bit Morton keys take 4 passes.
+// digit pass is a single kernel that ranks a tile in shared memory, resolves
+// its global offsets with a decoupled look-back over preceding tiles and
+// scatters.  8-bit digits: 30-bit Morton keys take 4 passes (u32 keys,
+// 4096-key tiles), 63-bit keys 8 passes (u64 keys, 2048-key tiles).
 //
-// HBM traffic per pass: 8 B read + 8 B written per pair; histogram pass 4 B.
+// HBM traffic per pass: (sizeof key + 4) B read + the same written per pair.
 
 #include "common.cuh"
 #include "internal.cuh"
@@ -23,9 +24,13 @@ constexpr int kSortWarps = kSortThreads / 32;
 #ifndef LBVH_SORT_ITEMS
 #define LBVH_SORT_ITEMS 16
 #endif
-constexpr int kItems = LBVH_SORT_ITEMS;
-constexpr int kTile = kSortThreads * kItems;  // 4096
-constexpr int kMaxPasses = 4;
+
+template <typename KeyT>
+struct SortCfg {
+    static constexpr int kItems = sizeof(KeyT) == 4 ? LBVH_SORT_ITEMS : 8;
+    static constexpr int kTile = kSortThreads * kItems;
+    static constexpr int kMaxPasses = sizeof(KeyT) == 4 ? 4 : 8;
+};
 
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
@@ -35,20 +40,23 @@ constexpr int kHistThreads = 512;
 constexpr int kHistItems = 16;
 
 // Digit histograms of every pass in one read of the keys.
+template <typename KeyT>
 __global__ void __launch_bounds__(kHistThreads)
-histogram_kernel(const uint32_t *__restrict__ keys, int64_t n, int passes, int first_bit,
+histogram_kernel(const KeyT *__restrict__ keys, int64_t n, int passes, int first_bit,
                  uint32_t *__restrict__ hist) {
-    __shared__ uint32_t s_hist[kMaxPasses][kRadix];
-    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x)
-        (&s_hist[0][0])[i] = 0;
+    constexpr int P = SortCfg<KeyT>::kMaxPasses;
+    __shared__ uint32_t s_hist[P][kRadix];
+    for (int i = threadIdx.x; i < P * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     int64_t base = (int64_t)blockIdx.x * kHistThreads * kHistItems;
     for (int j = 0; j < kHistItems; ++j) {
         int64_t i = base + (int64_t)j * kHistThreads + threadIdx.x;
         if (i < n) {
-            uint32_t k = __ldcs(keys + i);
+            const KeyT k = __ldcs(keys + i);
             for (int p = 0; p < passes; ++p)
-                atomicAdd(&s_hist[p][(k >> (first_bit + p * kRadixBits)) & (kRadix - 1)], 1u);
+                atomicAdd(&s_hist[p][(uint32_t)(k >> (first_bit + p * kRadixBits)) &
+                                     (kRadix - 1)],
+                          1u);
         }
     }
     __syncthreads();
@@ -66,12 +74,15 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // One digit pass.  Tiles are claimed in order through `tile_counter`, so a
 // tile only ever waits on tiles already owned by running CTAs.
+template <typename KeyT>
 __global__ void __launch_bounds__(kSortThreads)
-onesweep_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t n,
+onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                KeyT *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t n,
                 int shift, const uint32_t *__restrict__ hist, uint32_t *lookback,
                 uint32_t *tile_counter) {
-    __shared__ uint32_t s_keys[kTile];
+    constexpr int kItems = SortCfg<KeyT>::kItems;
+    constexpr int kTile = SortCfg<KeyT>::kTile;
+    __shared__ KeyT s_keys[kTile];
     __shared__ uint32_t s_vals[kTile];
     __shared__ uint32_t s_warp[kSortWarps][kRadix];  // counts -> warp exclusive offsets
     __shared__ uint32_t s_local[kRadix];             // digit start within the tile
@@ -92,18 +103,19 @@ onesweep_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict
 
     // Warp-striped load: item j of a lane sits at warp_base + j*32 + lane, so
     // (j, lane) order is position order and the ranking below is stable.
-    uint32_t key[kItems], val[kItems], rank[kItems];
+    KeyT key[kItems];
+    uint32_t val[kItems], rank[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         int64_t i = warp_base + j * 32 + lane;
         bool ok = i < n;
-        key[j] = ok ? __ldcs(keys_in + i) : 0xFFFFFFFFu;  // pads sort last
+        key[j] = ok ? __ldcs(keys_in + i) : ~(KeyT)0;  // pads sort last
         val[j] = ok ? __ldcs(vals_in + i) : 0u;
     }
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-        uint32_t d = (key[j] >> shift) & (kRadix - 1);
+        uint32_t d = (uint32_t)(key[j] >> shift) & (kRadix - 1);
         uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
         int leader = __ffs(peers) - 1;
         uint32_t before = 0;
@@ -167,20 +179,20 @@ onesweep_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict
     // Scatter into shared memory in tile-sorted order.
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-        uint32_t dj = (key[j] >> shift) & (kRadix - 1);
+        uint32_t dj = (uint32_t)(key[j] >> shift) & (kRadix - 1);
         uint32_t pos = s_local[dj] + s_warp[warp][dj] + rank[j];
         s_keys[pos] = key[j];
         s_vals[pos] = val[j];
     }
     __syncthreads();
 
-    // Pads (key 0xFFFFFFFF, positions >= n) are last in tile order.
+    // Pads (all-ones keys, positions >= n) are last in tile order.
     const int64_t valid = (n - tile_base) < kTile ? (n - tile_base) : kTile;
 #pragma unroll 4
     for (int i = tid; i < kTile; i += kSortThreads) {
         if (i < valid) {
-            uint32_t k = s_keys[i];
-            int64_t dst = s_global[(k >> shift) & (kRadix - 1)] + i;
+            const KeyT k = s_keys[i];
+            int64_t dst = s_global[(uint32_t)(k >> shift) & (kRadix - 1)] + i;
             keys_out[dst] = k;
             vals_out[dst] = s_vals[i];
         }
@@ -214,56 +226,77 @@ __global__ void exclusive_hist_kernel(uint32_t *hist, int passes) {
     }
 }
 
-}  // namespace
-
-size_t sort_workspace_bytes(int64_t n) {
-    int64_t tiles = (n + kTile - 1) / kTile;
+template <typename KeyT>
+size_t sort_ws_bytes(int64_t n) {
+    using C = SortCfg<KeyT>;
+    int64_t tiles = (n + C::kTile - 1) / C::kTile;
     size_t b = 0;
-    b += align_up(sizeof(uint32_t) * (size_t)n) * 2;                  // ping-pong
-    b += align_up(sizeof(uint32_t) * kMaxPasses * kRadix);           // hist
-    b += align_up(sizeof(uint32_t) * kMaxPasses * (size_t)tiles * kRadix);  // look-back
-    b += align_up(sizeof(uint32_t) * kMaxPasses);                    // tile counters
+    b += align_up(sizeof(KeyT) * (size_t)n) + align_up(sizeof(uint32_t) * (size_t)n);
+    b += align_up(sizeof(uint32_t) * C::kMaxPasses * kRadix);                // hist
+    b += align_up(sizeof(uint32_t) * C::kMaxPasses * (size_t)tiles * kRadix);  // look-back
+    b += align_up(sizeof(uint32_t) * C::kMaxPasses);                         // counters
     return b + 256;
 }
 
-int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
-               size_t ws_bytes, cudaStream_t stream, int first_bit) {
+template <typename KeyT>
+int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, size_t ws_bytes,
+              cudaStream_t stream, int first_bit) {
+    using C = SortCfg<KeyT>;
     if (n <= 1) return LBVH_OK;
     if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
-    if (key_bits < 1 || key_bits > 32 || first_bit < 0 || first_bit >= key_bits)
+    if (key_bits < 1 || key_bits > (int)(8 * sizeof(KeyT)) || first_bit < 0 ||
+        first_bit >= key_bits)
         return LBVH_ERR_INVALID_ARG;
-    if (ws_bytes < sort_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
+    if (ws_bytes < sort_ws_bytes<KeyT>(n)) return LBVH_ERR_WORKSPACE;
     const int passes = (key_bits - first_bit + kRadixBits - 1) / kRadixBits;
-    const int64_t tiles = (n + kTile - 1) / kTile;
+    const int64_t tiles = (n + C::kTile - 1) / C::kTile;
     Carve c(ws, ws_bytes);
-    uint32_t *k_alt = c.take<uint32_t>(n);
+    KeyT *k_alt = c.take<KeyT>(n);
     uint32_t *v_alt = c.take<uint32_t>(n);
     // hist, look-back and counters are contiguous so one memset clears them.
     size_t zero_begin = align_up(c.off);
-    uint32_t *hist = c.take<uint32_t>(kMaxPasses * kRadix);
-    uint32_t *lookback = c.take<uint32_t>((size_t)kMaxPasses * tiles * kRadix);
-    uint32_t *counters = c.take<uint32_t>(kMaxPasses);
+    uint32_t *hist = c.take<uint32_t>(C::kMaxPasses * kRadix);
+    uint32_t *lookback = c.take<uint32_t>((size_t)C::kMaxPasses * tiles * kRadix);
+    uint32_t *counters = c.take<uint32_t>(C::kMaxPasses);
     size_t zero_end = c.off;
     cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
-    histogram_kernel<<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, first_bit, hist);
-    count_launches(1);
-    exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes); count_launches(1);
+    histogram_kernel<KeyT><<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, first_bit,
+                                                                      hist);
+    exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes);
+    count_launches(2);
 
-    uint32_t *ks = keys, *vs = vals, *kd = k_alt, *vd = v_alt;
+    KeyT *ks = keys, *kd = k_alt;
+    uint32_t *vs = vals, *vd = v_alt;
     for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, stream>>>(
+        onesweep_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, stream>>>(
             ks, vs, kd, vd, n, first_bit + p * kRadixBits, hist + p * kRadix,
-            lookback + (size_t)p * tiles * kRadix, counters + p); count_launches(1);
-        uint32_t *t = ks; ks = kd; kd = t;
-        t = vs; vs = vd; vd = t;
+            lookback + (size_t)p * tiles * kRadix, counters + p);
+        count_launches(1);
+        KeyT *tk = ks; ks = kd; kd = tk;
+        uint32_t *tv = vs; vs = vd; vd = tv;
     }
     if (ks != keys) {
-        cudaMemcpyAsync(keys, ks, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream);
+        cudaMemcpyAsync(keys, ks, sizeof(KeyT) * n, cudaMemcpyDeviceToDevice, stream);
         cudaMemcpyAsync(vals, vs, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream);
     }
     return check_launch();
+}
+
+}  // namespace
+
+size_t sort_workspace_bytes(int64_t n) { return sort_ws_bytes<uint32_t>(n); }
+size_t sort64_workspace_bytes(int64_t n) { return sort_ws_bytes<uint64_t>(n); }
+
+int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+               size_t ws_bytes, cudaStream_t stream, int first_bit) {
+    return sort_impl<uint32_t>(keys, vals, n, key_bits, ws, ws_bytes, stream, first_bit);
+}
+
+int sort_pairs64(uint64_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+                 size_t ws_bytes, cudaStream_t stream) {
+    return sort_impl<uint64_t>(keys, vals, n, key_bits, ws, ws_bytes, stream, 0);
 }
 
 }  // namespace lbvh

@@ -184,7 +184,8 @@ def _device_boxes(boxes):
     return t[:, :3].contiguous(), t[:, 3:].contiguous()
 
 
-def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> Bvh:
+def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
+                 morton_bits: int = 30) -> Bvh:
     """Build from device-resident (n, 3) f32 ``mins``/``maxs`` (``maxs`` may
     be ``mins`` for point input).  The device-resident entry of :func:`build`."""
     n = int(mins.shape[0])
@@ -192,6 +193,8 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> 
         raise ValueError("empty scene")
     if n > _lib.MAX_ITEMS:
         raise ValueError(f"at most {_lib.MAX_ITEMS} primitives per tree")
+    if morton_bits not in (30, 63):
+        raise ValueError(f"morton_bits must be 30 or 63, got {morton_bits}")
     l = _lib.lib()
     f32, i32 = torch.float32, torch.int32
     d = {
@@ -206,7 +209,8 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> 
     }
     ws = dv.workspace(l.lbvh_build_workspace_bytes(n))
     status = dv.Status()
-    _lib.check(_launch("build", lambda: l.lbvh_build(dv.ptr(mins), dv.ptr(maxs), n, dv.ptr(ws), ws.numel(),
+    _lib.check(_launch("build", lambda: l.lbvh_build(
+                            dv.ptr(mins), dv.ptr(maxs), n, morton_bits, dv.ptr(ws), ws.numel(),
                             dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]), dv.ptr(d["left"]),
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
                             dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), status.ptr,
@@ -220,17 +224,22 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True) -> 
     return Bvh._from_device(d, n)
 
 
-def build(boxes, threads: int = 1) -> Bvh:
+def build(boxes, threads: int = 1, morton_bits: int = 30) -> Bvh:
     """Build a linear BVH over a non-empty collection of boxes (tree.py:177-209).
 
     Accepts (n, 3) points, (n, 6) corner rows, a ``(mins, maxs)`` pair,
     Box/Point sequences -- or a CUDA tensor of shape (n, 3)/(n, 6), which
     skips the host round trip.  ``threads`` is accepted and ignored.
     Deterministic: identical input gives bit-identical arrays.
+
+    ``morton_bits=63`` (an extension; the reference is 30-bit only) orders the
+    leaves by 63-bit codes, 21 bits per axis, for very large clouds.  Queries
+    on such a tree return exactly the same results (they are independent of
+    the tree shape); only the tree arrays differ from the reference's.
     """
     if dv.is_cuda_tensor(boxes):
         mins, maxs = _device_boxes(boxes)
-        return build_device(mins, maxs)
+        return build_device(mins, maxs, morton_bits=morton_bits)
     # Large ndarray inputs are value-checked on the device; pairs and
     # sequences on the host (exact reference messages either way).
     device_checks = isinstance(boxes, np.ndarray)
@@ -239,7 +248,7 @@ def build(boxes, threads: int = 1) -> Bvh:
         raise ValueError("empty scene")
     dmins = dv.h2d(mins)
     dmaxs = dmins if maxs is mins else dv.h2d(maxs)
-    return build_device(dmins, dmaxs)
+    return build_device(dmins, dmaxs, morton_bits=morton_bits)
 
 
 # ---------------------------------------------------------------------------
