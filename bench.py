@@ -418,6 +418,8 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
     tot, launches, bms = timed_loop(build_step, steps, warm, "build")
     ex["build_prims_per_sec"] = round(world * m * steps / (tot / 1e3), 1)
     ex["build_ms"] = round(tot / steps, 3)
+    t63, _, _ = timed_loop(lambda: lb.build(pts_d, morton_bits=63), steps, warm)
+    ex["build63_prims_per_sec"] = round(world * m * steps / (t63 / 1e3), 1)
     ex["build_roofline_frac"] = round(m * BUILD_BYTES_PER_PRIM / (bms / 1e3) / 1e9 / peak_gbs, 4)
     ex["build_launches_per_step"] = launches / steps
 
