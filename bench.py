@@ -214,7 +214,10 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # BENCH_FORCE_SHARDED=1 runs the sharded protocol (and its NCCL calls) even
+    # at N=1, to exercise it on a one-GPU box
+    dist_mode = world > 1 or os.environ.get("BENCH_FORCE_SHARDED") == "1"
+    if dist_mode:
         backend = os.environ.get("BENCH_BACKEND", "nccl")
         if backend == "nccl":
             tdist.init_process_group("nccl", device_id=dev)
@@ -225,11 +228,11 @@ def run_ours(args):
             _D.set_comm_device("cpu")
 
     def barrier():
-        if world > 1:
+        if dist_mode:
             tdist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
+        if not dist_mode:
             return x
         on_gpu = tdist.get_backend() == "nccl"
         t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
@@ -290,7 +293,7 @@ def run_ours(args):
 
     # -- build the index once (its own timed leg below) ----------------------
     sharded = None
-    if world == 1:
+    if not dist_mode:
         tree = lb.build(pts_d)
 
         def knn_step():
@@ -397,7 +400,7 @@ def run_ours(args):
 
     traversal.KERNEL_TIMER = None
     tree_mod.KERNEL_TIMER = None
-    if world > 1:
+    if dist_mode:
         tdist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
