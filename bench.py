@@ -367,11 +367,20 @@ def run_ours(args):
         pin = torch.empty((nq, 3), dtype=torch.float32, pin_memory=True)
         pin.numpy()[:] = qs
         host_q = pin.numpy()
+        if sharded is not None:
+            span_s = min(k, world * m)
+            h_off = torch.empty(nq + 1, dtype=torch.int64, pin_memory=True)
+            h_gid = torch.empty(nq * span_s, dtype=torch.int64, pin_memory=True)
+            h_dd = torch.empty(nq * span_s, dtype=torch.float32, pin_memory=True)
 
         def e2e_step():
             if sharded is not None:
                 off, gid, dd = D.query_knn_distributed(sharded["t"], pin.to(dev, non_blocking=True), k)
-                return off.cpu(), gid.cpu(), dd.cpu()
+                h_off.copy_(off, non_blocking=True)
+                h_gid[:gid.numel()].copy_(gid.reshape(-1), non_blocking=True)
+                h_dd[:dd.numel()].copy_(dd.reshape(-1), non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return h_off, h_gid, h_dd
             rs = lb.query_knn(tree, (host_q, k))
             assert rs.indices.shape[0] == nq * min(k, m)
             return rs

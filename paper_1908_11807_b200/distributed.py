@@ -293,14 +293,17 @@ def query_knn_distributed(t: DistributedBvh, centers, k: int):
     c = torch.as_tensor(centers, dtype=torch.float32).to(dev).reshape(-1, 3)
     nq = int(c.shape[0])
     kk = min(k, t.total)
+    # Payload rows are 32-bit words: f32 coordinates / d^2 and i32 indices
+    # (bit-cast), so every exchange moves 16 B per query and 4 B per candidate.
     # 1. to the home rank
     codes = t.engine.morton(c, t.scene_lo, t.scene_hi)
     home = torch.searchsorted(t.split_codes, codes, right=True)
-    q_id = torch.arange(nq, dtype=torch.float64, device=dev)
-    rows = torch.cat([c.to(torch.float64), q_id[:, None]], dim=1)
+    rows = torch.empty((nq, 4), dtype=torch.float32, device=dev)
+    rows[:, :3] = c
+    rows[:, 3] = torch.arange(nq, dtype=torch.int32, device=dev).view(torch.float32)
     hq, hcounts = _alltoallv(rows, home, world, g)
     origin = _source_ranks(hcounts, dev)
-    hc = hq[:, :3].to(torch.float32).contiguous()
+    hc = hq[:, :3].contiguous()
     mh = int(hc.shape[0])
     own_gid, own_d2 = _local_knn(t, hc, k)
     if t.tree is not None and t.counts[t.rank] >= k:
@@ -312,11 +315,14 @@ def query_knn_distributed(t: DistributedBvh, centers, k: int):
     need = (bd <= bound[:, None]) & (torch.tensor(t.counts, device=dev) > 0)[None, :]
     need[:, t.rank] = False
     qi, rr = torch.nonzero(need, as_tuple=True)
-    frows = torch.cat([hc[qi].to(torch.float64), qi.to(torch.float64)[:, None]], dim=1)
+    frows = torch.empty((qi.numel(), 4), dtype=torch.float32, device=dev)
+    frows[:, :3] = hc[qi]
+    frows[:, 3] = qi.to(torch.int32).view(torch.float32)
     fq, fcounts = _alltoallv(frows, rr, world, g)
     fsrc = _source_ranks(fcounts, dev)
-    f_gid, f_d2 = _local_knn(t, fq[:, :3].to(torch.float32).contiguous(), k)
-    back = torch.cat([fq[:, 3:4], f_d2.to(torch.float64), f_gid.to(torch.float64)], dim=1)
+    f_gid, f_d2 = _local_knn(t, fq[:, :3].contiguous(), k)
+    back = torch.cat([fq[:, 3:4].contiguous().view(torch.int32), f_d2.view(torch.int32),
+                      f_gid.to(torch.int32)], dim=1)
     bq, _ = _alltoallv(back, fsrc, world, g)
     # 3. merge at home: own candidates + every responder's
     brow = bq[:, 0].to(torch.int64)
@@ -346,19 +352,22 @@ def query_knn_distributed(t: DistributedBvh, centers, k: int):
             slot = torch.arange(brow_s.numel(), device=dev) - starts[brow_s]
             cols = (1 + slot)[:, None] * k + torch.arange(k, device=dev)[None, :]
             cand[pos[brow_s][:, None], cols] = _merge_keys(
-                bq[o, 1 + k:1 + 2 * k].to(torch.int64), bq[o, 1:1 + k].to(torch.float32))
+                bq[o, 1 + k:1 + 2 * k].to(torch.int64),
+                bq[o, 1:1 + k].contiguous().view(torch.float32))
         top[rows] = torch.sort(cand, dim=1).values[:, :kk]
     # ordinals and correctly rounded sqrt(d^2) (torch's CPU sqrt is not)
     res_gid, res_dist = t.engine.unpack_keys(top.contiguous())
-    # 4. back to the origin rank, in query order
-    ret = torch.cat([hq[:, 3:4], res_dist.to(torch.float64), res_gid.to(torch.float64)], dim=1)
+    # 4. back to the origin rank, scattered straight into query order
+    ret = torch.cat([hq[:, 3:4].contiguous().view(torch.int32), res_dist.view(torch.int32),
+                     res_gid.to(torch.int32)], dim=1)
     got, _ = _alltoallv(ret, origin, world, g)
     qix = got[:, 0].to(torch.int64)
-    o = torch.argsort(qix)
-    dist_out = got[o, 1:1 + kk].to(torch.float32).reshape(-1)
-    gid_out = got[o, 1 + kk:1 + 2 * kk].to(torch.int64).reshape(-1)
+    dist_out = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+    gid_out = torch.empty((nq, kk), dtype=torch.int64, device=dev)
+    dist_out[qix] = got[:, 1:1 + kk].contiguous().view(torch.float32)
+    gid_out[qix] = got[:, 1 + kk:1 + 2 * kk].to(torch.int64)
     offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
-    return offsets, gid_out, dist_out
+    return offsets, gid_out.reshape(-1), dist_out.reshape(-1)
 
 
 def query_spatial_distributed(t: DistributedBvh, centers, radius):
@@ -373,20 +382,22 @@ def query_spatial_distributed(t: DistributedBvh, centers, radius):
     bd = _box_dist_sq(c, t.boxes)
     need = (bd <= r2[:, None]) & (torch.tensor(t.counts, device=dev) > 0)[None, :]
     qi, rr = torch.nonzero(need, as_tuple=True)
-    rows = torch.cat([c[qi].to(torch.float64), r[qi].to(torch.float64)[:, None],
-                      qi.to(torch.float64)[:, None]], dim=1)
+    rows = torch.empty((qi.numel(), 5), dtype=torch.float32, device=dev)
+    rows[:, :3] = c[qi]
+    rows[:, 3] = r[qi]
+    rows[:, 4] = qi.to(torch.int32).view(torch.float32)
     rq, rcounts = _alltoallv(rows, rr, world, g)
     src = _source_ranks(rcounts, dev)
     m = int(rq.shape[0])
     if m and t.tree is not None:
-        off, idx = t.engine.radius(t.tree, rq[:, :3].to(torch.float32).contiguous(),
-                                   rq[:, 3].to(torch.float32).contiguous())
+        off, idx = t.engine.radius(t.tree, rq[:, :3].contiguous(), rq[:, 3].contiguous())
         cnt = off[1:] - off[:-1]
         owner = torch.repeat_interleave(torch.arange(m, device=dev), cnt)
-        hit_rows = torch.stack([rq[owner, 4], t.gids[idx].to(torch.float64)], dim=1)
+        qcol = rq[:, 4].contiguous().view(torch.int32)
+        hit_rows = torch.stack([qcol[owner], t.gids[idx].to(torch.int32)], dim=1)
         hit_dest = src[owner]
     else:
-        hit_rows = torch.empty((0, 2), dtype=torch.float64, device=dev)
+        hit_rows = torch.empty((0, 2), dtype=torch.int32, device=dev)
         hit_dest = torch.empty(0, dtype=torch.int64, device=dev)
     got, _ = _alltoallv(hit_rows, hit_dest, world, g)
     qix = got[:, 0].to(torch.int64)
