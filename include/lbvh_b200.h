@@ -68,6 +68,13 @@ typedef struct lbvh_tree {
     const void *nodes;
     const float *root_box;
     const uint32_t *leaf_codes;
+    /* Optional (with leaf_codes): (1 << leaf_dir_bits) + 1 u32 entries;
+     * entry p = first leaf whose code >> (30 - leaf_dir_bits) >= p
+     * (lbvh_leaf_directory).  Turns the kNN seed's lower_bound over
+     * leaf_codes into one directory lookup plus a search within a bucket. */
+    const uint32_t *leaf_dir;
+    int32_t leaf_dir_bits;
+    int32_t reserved;
 } lbvh_tree;
 
 #define LBVH_NODE_BYTES 64
@@ -105,6 +112,13 @@ int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
                void *workspace, size_t workspace_bytes, float *node_mins, float *node_maxs,
                int32_t *left, int32_t *right, int32_t *leaf_obj, float *root_box,
                void *nodes, uint32_t *sorted_codes, uint32_t *status, void *stream);
+
+/* Leaf directory over the build's sorted 30-bit leaf codes (kNN seed index;
+ * no reference counterpart).  lbvh_leaf_directory_bits(n) is the bucket
+ * count exponent used by the Python layer (n/8 leaves per bucket, <= 24). */
+int lbvh_leaf_directory_bits(int64_t n);
+int lbvh_leaf_directory(const uint32_t *leaf_codes, int64_t n, int bits, uint32_t *dir,
+                        void *stream);
 
 /* morton_codes(points, scene_min, scene_max)   replaces morton.py:68-91
  * points n x 3 f64 (device); scene bounds host doubles (smin[3], smax[3]). */

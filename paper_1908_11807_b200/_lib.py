@@ -44,13 +44,18 @@ class CTree(ctypes.Structure):
                 ("node_mins", ctypes.c_void_p), ("node_maxs", ctypes.c_void_p),
                 ("left", ctypes.c_void_p), ("right", ctypes.c_void_p),
                 ("leaf_obj", ctypes.c_void_p), ("nodes", ctypes.c_void_p),
-                ("root_box", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p)]
+                ("root_box", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p),
+                ("leaf_dir", ctypes.c_void_p), ("leaf_dir_bits", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 _SIGS = {
     "lbvh_strerror": ([ctypes.c_int], ctypes.c_char_p),
     "lbvh_last_cuda_error": ([], ctypes.c_char_p),
     "lbvh_abi_version": ([], ctypes.c_int),
+    "lbvh_leaf_directory_bits": ([ctypes.c_int64], ctypes.c_int),
+    "lbvh_leaf_directory": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                             ctypes.c_void_p], ctypes.c_int),
     "lbvh_launch_count": ([], ctypes.c_uint64),
     "lbvh_build_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_sort_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),

@@ -58,6 +58,7 @@ int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t,
             cudaStream_t);
 int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
                 void *, size_t, cudaStream_t);
+int leaf_directory(const uint32_t *, int64_t, int, uint32_t *, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
         const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
         cudaStream_t);
@@ -93,7 +94,7 @@ const char *lbvh_strerror(int code) {
 
 const char *lbvh_last_cuda_error(void) { return g_cuda_err; }
 
-int lbvh_abi_version(void) { return 1; }
+int lbvh_abi_version(void) { return 2; }
 
 uint64_t lbvh_launch_count(void) { return launch_count(); }
 
@@ -140,6 +141,17 @@ int lbvh_pack(const lbvh_tree *tree, void *nodes, float *root_box, uint32_t *sta
 int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
                       void *stream) {
     return unpack_boxes(tree, node_mins, node_maxs, S(stream));
+}
+
+int lbvh_leaf_directory_bits(int64_t n) {
+    int b = 0;
+    while (b < 24 && ((int64_t)8 << (b + 1)) <= n) ++b;
+    return b;
+}
+
+int lbvh_leaf_directory(const uint32_t *leaf_codes, int64_t n, int bits, uint32_t *dir,
+                        void *stream) {
+    return leaf_directory(leaf_codes, n, bits, dir, S(stream));
 }
 
 int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box, int order_bits,

@@ -44,8 +44,8 @@ struct TopK {
 
     // Keep the candidate iff it beats the current k-th best
     // (_kernels.py:387-395); branch-free sorted insertion dropping slot K-1.
-    __device__ __forceinline__ void offer(float cd, int32_t obj) {
-        const uint64_t c = make(cd, obj);
+    __device__ __forceinline__ void offer(float cd, int32_t obj) { offer_key(make(cd, obj)); }
+    __device__ __forceinline__ void offer_key(const uint64_t c) {
         if (!(c < key[K - 1])) return;
         bool lt[K];
 #pragma unroll

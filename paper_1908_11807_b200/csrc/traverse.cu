@@ -181,6 +181,12 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
     const int64_t n = t.n;
     const uint32_t *__restrict__ codes = t.leaf_codes;
     int64_t lo = 0, hi = n;
+    if (t.leaf_dir) {
+        // lower_bound(qcode) lies in the bucket of its top leaf_dir_bits
+        const uint32_t p = qcode >> (30 - t.leaf_dir_bits);
+        lo = __ldg(t.leaf_dir + p);
+        hi = __ldg(t.leaf_dir + p + 1);
+    }
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (__ldg(codes + mid) < qcode)
@@ -214,19 +220,35 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
     return best[K - 1];
 }
 
-// 6 resident CTAs per SM (<= 40 registers) measured 1.4% faster at K=10;
-// K=32 would spill, so it keeps the compiler's choice.
+// 5 resident CTAs per SM (<= 48 registers, no spills) with the 12-entry
+// shared-memory stack measured fastest at K=10 (8.75 vs 8.89 ms for 6 CTAs
+// and a local-memory stack, C2); K=32 keeps the compiler's choice.
 #ifndef LBVH_KNN_MINBLOCKS
-#define LBVH_KNN_MINBLOCKS 6
+#define LBVH_KNN_MINBLOCKS 5
 #endif
+#ifndef LBVH_KNN_STACKTOP
+#define LBVH_KNN_STACKTOP 0
+#endif
+#ifndef LBVH_KNN_DEFER
+#define LBVH_KNN_DEFER 0
+#endif
+#ifndef LBVH_KNN_SMEMSTACK
+#define LBVH_KNN_SMEMSTACK 12
+#endif
+// Threads per CTA of knn_kernel (resident threads per SM stay
+// LBVH_KNN_MINBLOCKS * 256 for K <= 16).
+#ifndef LBVH_KNN_BLOCK
+#define LBVH_KNN_BLOCK 256
+#endif
+// One query slot s of a kNN batch (s < nq).
 template <int K, bool REGNEXT>
-__global__ void __launch_bounds__(256, (K <= 16 ? LBVH_KNN_MINBLOCKS : 1))
-knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
-           const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
-           const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-           float *__restrict__ out_dist, bool squared, uint32_t *status) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nq) return;
+__device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__restrict__ centers,
+                                          const uint32_t *__restrict__ order,
+                                          const uint32_t *__restrict__ qcodes, int64_t s,
+                                          const int64_t *__restrict__ offsets,
+                                          int32_t *__restrict__ out_idx,
+                                          float *__restrict__ out_dist, bool squared,
+                                          uint32_t *status) {
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
     const int64_t base = __ldg(offsets + q);
     const int kk = (int)(__ldg(offsets + q + 1) - base);
@@ -253,6 +275,42 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     // and pop) and the capacity test still counts it, so node order and
     // stack exhaustion are the reference's either way.
     uint64_t stack[kStack];
+    // LBVH_KNN_STACKTOP: the top entry lives in a register (`stop`) and the
+    // local array holds the entries below it, so a pop never waits on a
+    // local-memory load (the next top is loaded while the popped node is
+    // processed).
+    constexpr bool STACKTOP = REGNEXT && LBVH_KNN_STACKTOP;
+    // LBVH_KNN_SMEMSTACK = D > 0: the first D entries live in shared memory
+    // as bare node ids (lane-interleaved, conflict-free), deeper ones in
+    // local memory.  Popped entries are not re-tested (a pruned entry costs
+    // one node visit whose children are then pruned), so pushes -- and the
+    // capacity test -- are exactly as above.
+    constexpr int SMS = REGNEXT ? LBVH_KNN_SMEMSTACK : 0;
+    __shared__ int32_t sst[(SMS > 0 ? SMS : 1) * LBVH_KNN_BLOCK];
+    int32_t *const sbase = sst + (threadIdx.x % LBVH_KNN_BLOCK);
+    uint64_t stop = 0;
+    // LBVH_KNN_DEFER: leaf candidates wait in a 4-entry per-lane buffer and
+    // are offered when some lane's buffer reaches 3 -- by every lane of the
+    // warp at once, so the k-best insertions run on many lanes together.
+    // Pruning meanwhile uses the not-yet-updated k-th distance, which is
+    // only less tight; the final list is the same.
+    constexpr bool DEFER = REGNEXT && LBVH_KNN_DEFER;
+    uint64_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0;
+    int np = 0;
+    auto pend = [&](float d, int32_t obj) {
+        pk3 = pk2;
+        pk2 = pk1;
+        pk1 = pk0;
+        pk0 = TopK<K>::make(d, obj);
+        ++np;
+    };
+    auto flush = [&]() {
+        if (np > 0) top.offer_key(pk0);
+        if (np > 1) top.offer_key(pk1);
+        if (np > 2) top.offer_key(pk2);
+        if (np > 3) top.offer_key(pk3);
+        np = 0;
+    };
     uint32_t fail = 0;
     int sp;
     int32_t node = 0;  // the root; never pruned (the list is empty)
@@ -282,18 +340,37 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
         int32_t next = -1;
         if (!(fd > top.worst())) {  // NaN worst = list not full yet
             if (fl < 0) {
-                top.offer(fd, fl & 0x7FFFFFFF);
+                if (DEFER)
+                    pend(fd, fl & 0x7FFFFFFF);
+                else
+                    top.offer(fd, fl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
+                const uint64_t e = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
+                if (SMS > 0) {
+                    if (sp < SMS)
+                        sbase[sp * LBVH_KNN_BLOCK] = fl;
+                    else
+                        reinterpret_cast<int32_t *>(stack)[sp] = fl;
+                    ++sp;
+                } else if (STACKTOP) {
+                    if (sp > 0) stack[sp - 1] = stop;
+                    stop = e;
+                    ++sp;
+                } else {
+                    stack[sp++] = e;
+                }
             }
         }
         if (!(ndist > top.worst())) {
             if (nl < 0) {
-                top.offer(ndist, nl & 0x7FFFFFFF);
+                if (DEFER)
+                    pend(ndist, nl & 0x7FFFFFFF);
+                else
+                    top.offer(ndist, nl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
@@ -306,22 +383,209 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
             }
         }
         if (REGNEXT) {
+            if (DEFER) {
+                const unsigned am = __activemask();
+                if (__any_sync(am, np >= 3)) flush();
+            }
             if (next < 0) {
                 // pop until an entry survives the prune test (_kernels.py:364-368)
-                while (sp > 0) {
-                    const uint64_t e = stack[--sp];
+                if (SMS > 0) {
+                    if (sp > 0) {
+                        --sp;
+                        next = sp < SMS ? sbase[sp * LBVH_KNN_BLOCK]
+                                        : reinterpret_cast<int32_t *>(stack)[sp];
+                    }
+                }
+                while (SMS == 0 && sp > 0) {
+                    uint64_t e;
+                    if (STACKTOP) {
+                        e = stop;
+                        --sp;
+                        if (sp > 0) stop = stack[sp - 1];
+                    } else {
+                        e = stack[--sp];
+                    }
                     if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
                         next = (int32_t)(uint32_t)e;
                         break;
                     }
                 }
-                if (next < 0) break;
+                if (next < 0) {
+                    if (DEFER) flush();
+                    break;
+                }
             }
             node = next;
         }
     }
     if (fail) atomicOr(status, fail);
     // Spans are written even after a failure; the driver raises anyway.
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        if (j >= K - kk) {
+            const int64_t o = base + (j - (K - kk));
+            out_idx[o] = top.ordinal(j);
+            out_dist[o] = squared ? top.dist(j) : __fsqrt_rn(top.dist(j));
+        }
+    }
+}
+
+template <int K, bool REGNEXT>
+__global__ void __launch_bounds__(LBVH_KNN_BLOCK,
+                                  (K <= 16 ? LBVH_KNN_MINBLOCKS * 256 / LBVH_KNN_BLOCK : 1))
+knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
+           const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
+           const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
+           float *__restrict__ out_dist, bool squared, uint32_t *status) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    knn_query<K, REGNEXT>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
+                          status);
+}
+
+// Persistent warps: each warp takes the next 32 Morton-consecutive query
+// slots from a global counter when all its lanes are done, so SM slots are
+// never held by a CTA waiting for its slowest warp (per-lane work is
+// exactly knn_kernel's).
+template <int K>
+__global__ void __launch_bounds__(LBVH_KNN_BLOCK,
+                                  (K <= 16 ? LBVH_KNN_MINBLOCKS * 256 / LBVH_KNN_BLOCK : 1))
+knn_warpq_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                 const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
+                 int64_t nq, const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
+                 float *__restrict__ out_dist, bool squared, uint32_t *status,
+                 unsigned long long *counter) {
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned long long s0 = 0;
+        if (lane == 0) s0 = atomicAdd(counter, 32ull);
+        s0 = __shfl_sync(0xFFFFFFFFu, s0, 0);
+        if ((int64_t)s0 >= nq) break;
+        const int64_t s = (int64_t)s0 + lane;
+        if (s < nq)
+            knn_query<K, true>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
+                               status);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-packet kNN.
+//
+// A warp holds 32 Morton-consecutive queries and walks ONE depth-first path
+// through the tree for all of them: every step loads one node record (the
+// same address in every lane, so one L1 transaction serves the warp), each
+// lane tests the two child boxes against its own query and k-th distance,
+// and the warp descends into a child if any lane still needs it (nearer
+// child of the lane majority first, the other pushed on a warp-uniform
+// stack that keeps each lane's own distance for the pop-time prune test).
+// Lanes offer leaves only within their own current k-th distance, so each
+// query's result is exactly the k smallest (dist^2, ordinal) pairs -- the
+// visiting order changes nothing.  The stack holds at most one entry per
+// level, so on trees of depth <= 63 neither this nor the reference's
+// per-query stack can overflow; the launcher only picks this kernel for
+// such trees (stack exhaustion elsewhere keeps the reference's behaviour).
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(LBVH_KNN_BLOCK, (K <= 16 ? LBVH_KNN_MINBLOCKS * 256 / LBVH_KNN_BLOCK : 1))
+knn_packet_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                  const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
+                  int64_t nq, const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
+                  float *__restrict__ out_dist, bool squared, uint32_t *status) {
+    const unsigned kFull = 0xFFFFFFFFu;
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= nq) return;  // whole warp idle
+    bool active = s < nq;
+    int64_t q = 0, base = 0;
+    int kk = 0;
+    float px = 0.f, py = 0.f, pz = 0.f;
+    if (active) {
+        q = order ? (int64_t)__ldg(order + s) : s;
+        base = __ldg(offsets + q);
+        kk = (int)(__ldg(offsets + q + 1) - base);
+        px = __ldg(centers + 3 * q);
+        py = __ldg(centers + 3 * q + 1);
+        pz = __ldg(centers + 3 * q + 2);
+        active = kk > 0;
+    }
+    if (t.n == 1) {
+        if (active) {
+            const float *bx = t.root_box;
+            const float d2 = box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]);
+            out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
+            out_idx[base] = __ldg(t.leaf_obj);
+        }
+        return;
+    }
+    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    TopK<K> top;
+    float bound = __int_as_float(0x7FFFFFFF);
+    if (active && qcodes && t.leaf_codes) bound = seed_bound<K>(t, __ldg(qcodes + s), kk, px, py, pz);
+    top.init(active ? kk : K, bound);
+    // An idle lane needs nothing: worst = -inf makes every distance "farther".
+    const float kIdle = -INFINITY;
+    uint64_t stack[kStack];
+    int sp = 0;  // warp-uniform
+    int32_t node = 0;
+    uint32_t fail = 0;
+    while (true) {
+        float4 a, b, c;
+        int4 dd;
+        load_node(nodes, node, a, b, c, dd);
+        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
+        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        float w = active ? top.worst() : kIdle;
+        bool nl = !(dl > w), nr = !(dr > w);
+        // leaves: offered by the lanes that still need them, nearer one first
+        if ((dd.x < 0) | (dd.y < 0)) {
+            const bool left_near = dl <= dr;
+            if (left_near) {
+                if (dd.x < 0 && nl) top.offer(dl, dd.x & 0x7FFFFFFF);
+                if (dd.y < 0 && !(dr > (active ? top.worst() : kIdle))) top.offer(dr, dd.y & 0x7FFFFFFF);
+            } else {
+                if (dd.y < 0 && nr) top.offer(dr, dd.y & 0x7FFFFFFF);
+                if (dd.x < 0 && !(dl > (active ? top.worst() : kIdle))) top.offer(dl, dd.x & 0x7FFFFFFF);
+            }
+            if (dd.x < 0) nl = false;
+            if (dd.y < 0) nr = false;
+            w = active ? top.worst() : kIdle;
+            nl = nl && !(dl > w);
+            nr = nr && !(dr > w);
+        }
+        const unsigned bl = __ballot_sync(kFull, nl), br = __ballot_sync(kFull, nr);
+        int32_t next = -1;
+        if (bl && br) {
+            // lanes for which the left child is the nearer one
+            const unsigned pl = __ballot_sync(kFull, nl && (!nr || dl <= dr));
+            const bool left_first = 2 * __popc(pl) >= __popc(bl | br);
+            if (sp >= kStack) {
+                fail = LBVH_FLAG_STACK_EXHAUSTED;
+                break;
+            }
+            const float pd = left_first ? dr : dl;
+            const int32_t pn = left_first ? dd.y : dd.x;
+            stack[sp++] = ((uint64_t)__float_as_uint(active ? pd : INFINITY) << 32) | (uint32_t)pn;
+            next = left_first ? dd.x : dd.y;
+        } else if (bl) {
+            next = dd.x;
+        } else if (br) {
+            next = dd.y;
+        } else {
+            while (sp > 0) {
+                const uint64_t e = stack[--sp];
+                const bool need = !(__uint_as_float((uint32_t)(e >> 32)) >
+                                    (active ? top.worst() : kIdle));
+                if (__any_sync(kFull, need)) {
+                    next = (int32_t)(uint32_t)e;
+                    break;
+                }
+            }
+            if (next < 0) break;
+        }
+        node = next;
+    }
+    if (fail && (threadIdx.x & 31) == 0) atomicOr(status, fail);
+    if (!active) return;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         if (j >= K - kk) {
@@ -721,6 +985,62 @@ int launch_knn_persistent(const lbvh_tree *t, const float *centers, const uint32
     return check_launch();
 }
 
+template <int K>
+int launch_knn_warpq(const lbvh_tree *t, const float *centers, const uint32_t *order,
+                     const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int32_t *out_idx,
+                     float *out_dist, bool squared, uint32_t *status, void *ws,
+                     cudaStream_t stream) {
+    unsigned long long *counter =
+        (unsigned long long *)((char *)ws + knn_workspace_bytes(nq) - 64);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_warpq_kernel<K>,
+                                                      LBVH_KNN_BLOCK, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    unsigned g = div_up(nq, LBVH_KNN_BLOCK);
+    const unsigned cap = (unsigned)(sms * per_sm);
+    g = g < cap ? g : cap;
+    knn_warpq_kernel<K><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq, offsets,
+                                                          out_idx, out_dist, squared, status,
+                                                          counter);
+    count_launches(1);
+    return check_launch();
+}
+
+namespace {
+__global__ void __launch_bounds__(256)
+leaf_directory_kernel(const uint32_t *__restrict__ codes, int64_t n, int bits,
+                      uint32_t *__restrict__ dir) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > ((int64_t)1 << bits)) return;
+    const uint64_t target = (uint64_t)p << (30 - bits);
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(codes + mid) < target)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    dir[p] = (uint32_t)lo;
+}
+}  // namespace
+
+int leaf_directory(const uint32_t *codes, int64_t n, int bits, uint32_t *dir,
+                   cudaStream_t stream) {
+    if (n < 1 || bits < 0 || bits > 30 || !codes || !dir) return LBVH_ERR_INVALID_ARG;
+    if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
+    const int64_t entries = ((int64_t)1 << bits) + 1;
+    leaf_directory_kernel<<<div_up(entries, 256), 256, 0, stream>>>(codes, n, bits, dir);
+    count_launches(1);
+    return check_launch();
+}
+
 int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
         int32_t *out_idx, float *out_dist, int flags, void *ws, size_t ws_bytes,
@@ -729,7 +1049,7 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     if (nq == 0 || max_span <= 0) return LBVH_OK;
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
-    const unsigned g = div_up(nq, 256);
+    const unsigned g = div_up(nq, LBVH_KNN_BLOCK);
     // 1 = nearer child kept in a register (measured faster with the seed),
     // 0 = reference push/pop per node.  Same results either way.
     static const int variant = env_int("LBVH_KNN_VARIANT", 1);
@@ -739,18 +1059,28 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     static const int persistent = env_int("LBVH_KNN_PERSISTENT", 0);
     if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
     const bool use_persistent = persistent && ws && ws_bytes >= knn_workspace_bytes(nq);
+    static const int packet = env_int("LBVH_KNN_PACKET", 0);
+    static const int warpq = env_int("LBVH_KNN_WARPQ", 0);
+    const bool use_warpq = warpq && ws && ws_bytes >= knn_workspace_bytes(nq);
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
         if (use_persistent)                                                                 \
             return launch_knn_persistent<KV>(t, centers, order, qcodes, nq, offsets,        \
                                              out_idx, out_dist, squared, status, ws,        \
                                              stream);                                       \
-        if (variant == 1)                                                                   \
-            knn_kernel<KV, true><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,     \
+        if (use_warpq)                                                                      \
+            return launch_knn_warpq<KV>(t, centers, order, qcodes, nq, offsets, out_idx,     \
+                                        out_dist, squared, status, ws, stream);             \
+        if (packet)                                                                         \
+            knn_packet_kernel<KV><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, \
+                                                                 nq, offsets, out_idx,       \
+                                                                 out_dist, squared, status); \
+        else if (variant == 1)                                                              \
+            knn_kernel<KV, true><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,     \
                                                         offsets, out_idx, out_dist, squared, \
                                                         status);                            \
         else                                                                                \
-            knn_kernel<KV, false><<<g, 256, 0, stream>>>(*t, centers, order, qcodes, nq,    \
+            knn_kernel<KV, false><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,    \
                                                          offsets, out_idx, out_dist,        \
                                                          squared, status);                  \
         count_launches(1);                                                                  \

@@ -168,9 +168,12 @@ class Bvh:
 
 
 def _ctree(d: dict, n: int) -> _lib.CTree:
+    ld = d.get("leaf_dir")
+    bits = (int(ld.numel()) - 1).bit_length() - 1 if ld is not None else 0
     return _lib.CTree(n, dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]),
                       dv.ptr(d.get("left")), dv.ptr(d.get("right")), dv.ptr(d["leaf_obj"]),
-                      dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), dv.ptr(d.get("leaf_codes")))
+                      dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), dv.ptr(d.get("leaf_codes")),
+                      dv.ptr(ld), bits, 0)
 
 
 def _device_boxes(boxes):
@@ -215,6 +218,11 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
                             dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), status.ptr,
                             dv.stream())))
+    # kNN seed index over the sorted leaf codes (2^bits + 1 bucket starts)
+    bits = l.lbvh_leaf_directory_bits(n)
+    d["leaf_dir"] = dv.empty((1 << bits) + 1, i32)
+    _lib.check(l.lbvh_leaf_directory(dv.ptr(d["leaf_codes"]), n, bits, dv.ptr(d["leaf_dir"]),
+                                     dv.stream()))
     if check:
         flags = status.read()
         if flags & _lib.FLAG_NONFINITE:

@@ -164,6 +164,35 @@ def test_device_resident_inputs_and_outputs():
     assert np.array_equal(rs.to_host().offsets, lb.query_spatial_2p(th, (q, 2.0)).offsets)
 
 
+@pytest.mark.parametrize("kind", ["cube:filled", "sphere:hollow", "clustered"])
+def test_leaf_directory_is_lower_bound_of_bucket_starts(kind):
+    """The kNN seed's leaf directory: entry p = lower_bound(p << (30 - bits))
+    over the sorted leaf codes, including empty buckets; kNN with and
+    without it returns identical results (equal to the oracle)."""
+    if kind == "clustered":
+        rng = np.random.default_rng(5)
+        pts = np.concatenate([rng.normal(c, 0.01, size=(4000, 3)) for c in (-50, 0, 3, 70)])
+        pts = pts.astype(np.float32)
+    else:
+        src, k = kind.split(":")
+        pts = datasets.generate(datasets.CloudSpec(src, k, 30_000, 0))
+    tree = lb.build(pts)
+    d = tree.device_arrays()
+    codes = d["leaf_codes"].cpu().numpy().view(np.uint32).astype(np.int64)
+    ld = d["leaf_dir"].cpu().numpy().view(np.uint32).astype(np.int64)
+    bits = (ld.shape[0] - 1).bit_length() - 1
+    assert ld.shape[0] == (1 << bits) + 1
+    targets = np.arange((1 << bits) + 1, dtype=np.int64) << (30 - bits)
+    assert np.array_equal(ld, np.searchsorted(codes, targets, side="left"))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 5_000, 1)) * 0.5
+    ko, ki, kd = oracle.query_knn(oracle.build(pts), q, 10)
+    rk = lb.query_knn(tree, (q, 10))
+    assert np.array_equal(rk.indices, ki) and rk.distances.tobytes() == kd.tobytes()
+    del d["leaf_dir"]  # seed falls back to the full binary search
+    rk2 = lb.query_knn(tree, (q, 10))
+    assert np.array_equal(rk2.indices, ki) and rk2.distances.tobytes() == kd.tobytes()
+
+
 def test_large_scale_properties_1e7():
     """Full C2 size: size-independent properties (sortedness of leaf codes,
     containment, root box == scene box), plus oracle parity on a query sample."""

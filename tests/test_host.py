@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     lib = _lib.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.lbvh_abi_version() == 1
+    assert lib.lbvh_abi_version() == 2
     assert set(_lib.exported_symbols()) == set(header_functions())
 
 
@@ -38,6 +38,13 @@ def test_library_strerror_and_workspace_sizes():
         assert lib.lbvh_build_workspace_bytes(n) >= 20 * n
         assert lib.lbvh_query_workspace_bytes(n) >= 12 * n
         assert lib.lbvh_scan_workspace_bytes(n) > 0
+
+
+def test_leaf_directory_bits():
+    lib = _lib.load_library()
+    assert [lib.lbvh_leaf_directory_bits(n) for n in (1, 15, 16, 17, 10**7, 2**40)] == \
+        [0, 0, 1, 1, 20, 24]
+    assert lib.lbvh_leaf_directory(None, 0, 3, None, None) == 1
 
 
 def test_library_rejects_bad_arguments_without_touching_the_device():
