@@ -74,8 +74,15 @@ typedef struct lbvh_tree {
      * leaf_codes into one directory lookup plus a search within a bucket. */
     const uint32_t *leaf_dir;
     int32_t leaf_dir_bits;
-    int32_t reserved;
+    /* LBVH_TREE_* bits describing how the tree was built (0 = unknown). */
+    int32_t flags;
 } lbvh_tree;
+
+/* Every leaf box is a point (built from (n, 3) input: maxs == mins). */
+#define LBVH_TREE_POINT_LEAVES 0x1
+/* Leaves ordered by (30-bit code, index) -- the reference's build -- so the
+ * Karras node covering any code prefix can be located from leaf_codes. */
+#define LBVH_TREE_CODES30 0x2
 
 #define LBVH_NODE_BYTES 64
 

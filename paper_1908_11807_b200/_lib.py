@@ -46,7 +46,10 @@ class CTree(ctypes.Structure):
                 ("leaf_obj", ctypes.c_void_p), ("nodes", ctypes.c_void_p),
                 ("root_box", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p),
                 ("leaf_dir", ctypes.c_void_p), ("leaf_dir_bits", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("flags", ctypes.c_int32)]
+
+TREE_POINT_LEAVES = 0x1
+TREE_CODES30 = 0x2
 
 
 _SIGS = {

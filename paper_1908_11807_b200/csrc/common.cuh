@@ -120,6 +120,28 @@ __device__ __forceinline__ uint32_t atomic_exch_acq_rel(uint32_t *p, uint32_t v)
     return old;
 }
 
+__device__ __forceinline__ uint32_t atomic_exch_release(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// Strong (relaxed, gpu-scope) loads: read at the point of coherence, never a
+// stale L1 line.
+__device__ __forceinline__ float ld_relaxed(const float *p) {
+    float v;
+    asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ float4 ld_relaxed(const float4 *p) {
+    float4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t atomic_add_acq_rel(uint32_t *p, uint32_t v) {
     uint32_t old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"

