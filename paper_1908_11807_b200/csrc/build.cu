@@ -344,6 +344,222 @@ hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ p
     }
 }
 
+// ---------------------------------------------------------------------------
+// Two-level hierarchy (K4+K5, default): the same bottom-up construction and
+// Karras ordinals as hierarchy_kernel, split by where the two children of a
+// node meet.
+//
+// hierarchy_local_kernel: CTA c owns leaves [B, E].  A thread climbs while the
+// split slot g of its node satisfies B <= g < E, i.e. both children of the
+// parent start or end inside the CTA; the handshake is then a shared-memory
+// exchange and the sibling's box and link come from shared memory -- no
+// global atomics, no fences.  A node whose slot leaves the CTA is appended to
+// the frontier list; a first arrival whose partner never came (the sibling
+// subtree crosses the CTA edge) is copied to the global slot array at the end.
+//
+// hierarchy_frontier_kernel: the frontier nodes continue with the global
+// release handshake of hierarchy_kernel.  A kernel-A first arrival is then
+// indistinguishable from a global one, so the meeting rule is unchanged.
+// ---------------------------------------------------------------------------
+constexpr int kHierT = 256;
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kHierT)
+hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
+                       const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
+                       uint32_t *__restrict__ slots, float *__restrict__ node_mins,
+                       float *__restrict__ node_maxs, int32_t *__restrict__ left,
+                       int32_t *__restrict__ right, int32_t *__restrict__ leaf_obj,
+                       PackedNode *__restrict__ nodes, float *__restrict__ root_box,
+                       uint32_t *__restrict__ leaf_codes, uint2 *__restrict__ frontier,
+                       uint32_t *frontier_count) {
+    __shared__ uint32_t s_slot[kHierT];
+    __shared__ float s_box[2][6][kHierT];
+    __shared__ int32_t s_link[2][kHierT];
+    const int tid = threadIdx.x;
+    const int64_t B = (int64_t)blockIdx.x * kHierT;
+    const int64_t E = (B + kHierT < n ? B + kHierT : n) - 1;
+    const int64_t p = B + tid;
+    const int64_t internal = n - 1;
+    s_slot[tid] = 0;
+    __syncthreads();
+    bool active = p < n;
+    Box mine;
+    int32_t my_link = 0;
+    int64_t l = p, r = p;
+    if (active) {
+        if (leaf_codes) leaf_codes[p] = code30(__ldg(codes + p));
+        const uint32_t obj = __ldg(perm + p);
+        leaf_obj[p] = (int32_t)obj;
+        const bool same = (mins == maxs);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mine.lo[a] = __ldg(mins + 3 * (int64_t)obj + a);
+            mine.hi[a] = same ? mine.lo[a] : __ldg(maxs + 3 * (int64_t)obj + a);
+        }
+        store_box(node_mins, node_maxs, internal + p, mine);
+        my_link = (int32_t)(obj | kLeafTag);
+    }
+    while (active) {
+        const bool left_side = is_left_child(codes, n, l, r);
+        const int64_t g = left_side ? r : l - 1;
+        if (g < B || g >= E) {  // the parent's other child may lie outside the CTA
+            const uint32_t at = atomicAdd(frontier_count, 1u);
+            frontier[at] = make_uint2((uint32_t)l, (uint32_t)r);
+            break;
+        }
+        const int s = (int)(g - B);
+        const int side = left_side ? 0 : 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s_box[side][a][s] = mine.lo[a];
+            s_box[side][3 + a][s] = mine.hi[a];
+        }
+        s_link[side][s] = my_link;
+        __threadfence_block();
+        const uint32_t known = (uint32_t)(left_side ? l : r);
+        const uint32_t other = atomicExch(&s_slot[s], known + 1u);
+        if (other == 0) break;  // first arrival: the sibling continues
+        __threadfence_block();
+        s_slot[s] = 0;  // consumed (only the two children meet here)
+        const int64_t pl = left_side ? l : (int64_t)(other - 1u);
+        const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
+        const int64_t lc = (pl == g) ? internal + g : g;
+        const int64_t rc = (g + 1 == pr) ? internal + g + 1 : g + 1;
+        const bool root = (pl == 0 && pr == n - 1);
+        const int64_t pid = root ? 0 : (is_left_child(codes, n, pl, pr) ? pr : pl);
+        left[pid] = (int32_t)lc;
+        right[pid] = (int32_t)rc;
+        Box sb;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            sb.lo[a] = s_box[1 - side][a][s];
+            sb.hi[a] = s_box[1 - side][3 + a][s];
+        }
+        const int32_t sib_link = s_link[1 - side][s];
+        const Box &L = left_side ? mine : sb;
+        const Box &R = left_side ? sb : mine;
+        Box P;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            P.lo[a] = min_left(L.lo[a], R.lo[a]);
+            P.hi[a] = max_left(L.hi[a], R.hi[a]);
+        }
+        store_packed(nodes, pid, L, R, left_side ? my_link : sib_link,
+                     left_side ? sib_link : my_link);
+        mine = P;
+        my_link = (int32_t)pid;
+        if (root) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                root_box[a] = P.lo[a];
+                root_box[3 + a] = P.hi[a];
+            }
+            break;
+        }
+        l = pl;
+        r = pr;
+    }
+    __syncthreads();
+    // first arrivals still waiting for a partner from outside the CTA
+    const uint32_t v = s_slot[tid];
+    if (v) slots[B + tid] = v;
+}
+
+template <typename CodeT>
+__global__ void __launch_bounds__(256)
+hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
+                          int64_t n, uint32_t *slots, float *node_mins, float *node_maxs,
+                          int32_t *__restrict__ left, int32_t *__restrict__ right,
+                          PackedNode *__restrict__ nodes, float *__restrict__ root_box,
+                          const uint2 *__restrict__ frontier, const uint32_t *frontier_count) {
+    const int64_t internal = n - 1;
+    const int64_t count = (int64_t)*frontier_count;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint2 e = frontier[i];
+        int64_t l = e.x, r = e.y;
+        Box mine;
+        int32_t my_link;
+        if (l == r) {  // a leaf (row written by the local kernel)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                mine.lo[a] = ld_relaxed(node_mins + 3 * (internal + l) + a);
+                mine.hi[a] = ld_relaxed(node_maxs + 3 * (internal + l) + a);
+            }
+            my_link = (int32_t)(__ldg(perm + l) | kLeafTag);
+        } else {       // an internal node built by the local kernel
+            const int64_t id = is_left_child(codes, n, l, r) ? r : l;
+            const PackedNode *pn = nodes + id;
+            const float4 a = ld_relaxed(&pn->a), b = ld_relaxed(&pn->b), c = ld_relaxed(&pn->c);
+            mine.lo[0] = min_left(a.x, b.z); mine.lo[1] = min_left(a.y, b.w);
+            mine.lo[2] = min_left(a.z, c.x);
+            mine.hi[0] = max_left(a.w, c.y); mine.hi[1] = max_left(b.x, c.z);
+            mine.hi[2] = max_left(b.y, c.w);
+            my_link = (int32_t)id;
+        }
+        bool left_side = is_left_child(codes, n, l, r);
+        while (true) {
+            const int64_t g = left_side ? r : l - 1;
+            const uint32_t known = (uint32_t)(left_side ? l : r);
+            const uint32_t other = atomic_exch_release(slots + g, known + 1u);
+            if (other == 0) break;  // first arrival: sibling subtree not done
+            const int64_t pl = left_side ? l : (int64_t)(other - 1u);
+            const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
+            const int64_t lc = (pl == g) ? internal + g : g;
+            const int64_t rc = (g + 1 == pr) ? internal + g + 1 : g + 1;
+            const bool root = (pl == 0 && pr == n - 1);
+            const bool parent_left = root ? false : is_left_child(codes, n, pl, pr);
+            const int64_t pid = root ? 0 : (parent_left ? pr : pl);
+            left[pid] = (int32_t)lc;
+            right[pid] = (int32_t)rc;
+            const int64_t sib = left_side ? rc : lc;
+            Box sb;
+            int32_t sib_link;
+            if (sib < internal) {
+                const PackedNode *sp = nodes + sib;
+                const float4 a = ld_relaxed(&sp->a), b = ld_relaxed(&sp->b),
+                             c = ld_relaxed(&sp->c);
+                sb.lo[0] = min_left(a.x, b.z); sb.lo[1] = min_left(a.y, b.w);
+                sb.lo[2] = min_left(a.z, c.x);
+                sb.hi[0] = max_left(a.w, c.y); sb.hi[1] = max_left(b.x, c.z);
+                sb.hi[2] = max_left(b.y, c.w);
+                sib_link = (int32_t)sib;
+            } else {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    sb.lo[a] = ld_relaxed(node_mins + 3 * sib + a);
+                    sb.hi[a] = ld_relaxed(node_maxs + 3 * sib + a);
+                }
+                sib_link = (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
+            }
+            const Box &L = left_side ? mine : sb;
+            const Box &R = left_side ? sb : mine;
+            Box P;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                P.lo[a] = min_left(L.lo[a], R.lo[a]);
+                P.hi[a] = max_left(L.hi[a], R.hi[a]);
+            }
+            store_packed(nodes, pid, L, R, left_side ? my_link : sib_link,
+                         left_side ? sib_link : my_link);
+            mine = P;
+            my_link = (int32_t)pid;
+            if (root) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    root_box[a] = P.lo[a];
+                    root_box[3 + a] = P.hi[a];
+                }
+                break;
+            }
+            l = pl;
+            r = pr;
+            left_side = parent_left;
+        }
+    }
+}
+
 // Reference-layout rows of the internal nodes, written after the hierarchy
 // pass: row i = union of the two child boxes in packed record i, folded with
 // the refit's left-first rule (identical bits to an in-pass write).  Thread i
@@ -525,7 +741,21 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
     // 1 (measured 15% faster at 1e7): sibling boxes from packed records,
     // internal reference rows in a separate coalesced pass.
     static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 1);
-    if (rows_late && n > 1) {
+    static const int two_level = env_int("LBVH_BUILD_TWO_LEVEL", 1);
+    if (two_level && n > 1) {
+        // the sort's ping-pong buffers are dead now: frontier list lives there
+        uint2 *frontier = reinterpret_cast<uint2 *>(sort_ws);
+        uint32_t *fcount = counter + 2;
+        hierarchy_local_kernel<CodeT><<<div_up(n, kHierT), kHierT, 0, stream>>>(
+            codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, leaf_obj,
+            (PackedNode *)nodes, root_box, sorted_codes, frontier, fcount);
+        hierarchy_frontier_kernel<CodeT><<<grid_for(n / 64 + 1, 256, 8), 256, 0, stream>>>(
+            codes, perm, n, slots, node_mins, node_maxs, left, right, (PackedNode *)nodes,
+            root_box, frontier, fcount);
+        internal_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
+            (const PackedNode *)nodes, n - 1, node_mins, node_maxs);
+        count_launches(3);
+    } else if (rows_late && n > 1) {
         hierarchy_kernel<true, true, CodeT><<<div_up(n, 256), 256, 0, stream>>>(
             codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
             leaf_obj, (PackedNode *)nodes, root_box, sorted_codes);
