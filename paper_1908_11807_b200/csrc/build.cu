@@ -361,10 +361,16 @@ hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ p
 // release handshake of hierarchy_kernel.  A kernel-A first arrival is then
 // indistinguishable from a global one, so the meeting rule is unchanged.
 // ---------------------------------------------------------------------------
-constexpr int kHierT = 256;
+#ifndef LBVH_HIER_T
+#define LBVH_HIER_T 256
+#endif
+#ifndef LBVH_HIER_MINBLOCKS
+#define LBVH_HIER_MINBLOCKS 1
+#endif
+constexpr int kHierT = LBVH_HIER_T;
 
 template <typename CodeT>
-__global__ void __launch_bounds__(kHierT)
+__global__ void __launch_bounds__(kHierT, LBVH_HIER_MINBLOCKS)
 hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
                        const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
                        uint32_t *__restrict__ slots, float *__restrict__ node_mins,

@@ -173,17 +173,28 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
 __global__ void __launch_bounds__(256)
 compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__restrict__ counts,
                const int64_t *__restrict__ offsets, int64_t nq, int32_t *__restrict__ out) {
-    // One warp per query row: lanes copy the row's prefix.
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= nq) return;
-    const int32_t cnt = __ldg(counts + warp);
-    if (cnt > cap) return;  // did not fit its row: written by the overflow fill pass
-    const int64_t dst = __ldg(offsets + warp);
-    const int32_t *row = buf + warp * cap;
-    for (int j = lane; j < cnt; j += 32) out[dst + j] = __ldcs(row + j);
+    // One thread per query row: consecutive threads read consecutive rows
+    // (16-byte vector loads when rows are 16-byte aligned) and write
+    // consecutive output segments.
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t cnt = __ldg(counts + q);
+        if (cnt > cap) continue;  // did not fit its row: written by the overflow fill pass
+        const int64_t dst = __ldg(offsets + q);
+        const int32_t *row = buf + q * cap;
+        if ((cap & 3) == 0) {
+            for (int32_t j = 0; j < cnt; j += 4) {
+                const int4 v = __ldcs(reinterpret_cast<const int4 *>(row + j));
+                out[dst + j] = v.x;
+                if (j + 1 < cnt) out[dst + j + 1] = v.y;
+                if (j + 2 < cnt) out[dst + j + 2] = v.z;
+                if (j + 3 < cnt) out[dst + j + 3] = v.w;
+            }
+        } else {
+            for (int32_t j = 0; j < cnt; ++j) out[dst + j] = __ldcs(row + j);
+        }
+    }
 }
-
 
 // Search-radius seed for one query: the kk-th smallest distance^2 among the
 // 2*kk leaves that neighbour the query's Morton code in leaf order (a real
@@ -1031,7 +1042,10 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
     if (nq < 0 || cap < 1) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (!buf || !counts || !offsets) return LBVH_ERR_INVALID_ARG;
-    compact_kernel<<<div_up(nq * 32, 256), 256, 0, stream>>>(buf, cap, counts, offsets, nq, out); count_launches(1);
+    unsigned g = div_up(nq, 256);
+    g = g < kNumSMs * 8 ? g : kNumSMs * 8;
+    compact_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
+    count_launches(1);
     return check_launch();
 }
 

@@ -309,7 +309,7 @@ def _finish(host: bool, status: dv.Status, *arrays):
 # the count pass (in traversal order, so bytes are the reference's fill
 # order); the fill pass then revisits only queries with more hits.  The row
 # buffer is skipped when it would exceed _ROW_BUDGET bytes.
-_ROW_HITS = 16
+_ROW_HITS = int(os.environ.get("LBVH_ROW_HITS", "24"))
 _ROW_BUDGET = 4 << 30
 
 
@@ -319,7 +319,7 @@ def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     st = dv.stream()
     nq = b.nq
     counts = dv.empty(nq, torch.int32)
-    rows = next((r for r in (2 * _ROW_HITS, _ROW_HITS) if nq * r * 4 <= _ROW_BUDGET), 0)
+    rows = next((r for r in (_ROW_HITS, _ROW_HITS // 2) if r and nq * r * 4 <= _ROW_BUDGET), 0)
     buf = dv.empty((nq, rows), torch.int32) if rows else None
     _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
         ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq, dv.ptr(counts),
