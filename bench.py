@@ -370,7 +370,8 @@ def run_ours(args):
         if sharded is not None:
             span_s = min(k, world * m)
             h_off = torch.empty(nq + 1, dtype=torch.int64, pin_memory=True)
-            h_gid = torch.empty(nq * span_s, dtype=torch.int64, pin_memory=True)
+            gid_dtype = torch.int32 if world * m < 2 ** 31 else torch.int64
+            h_gid = torch.empty(nq * span_s, dtype=gid_dtype, pin_memory=True)
             h_dd = torch.empty(nq * span_s, dtype=torch.float32, pin_memory=True)
 
         def e2e_step():
@@ -392,9 +393,13 @@ def run_ours(args):
                       "unit": "queries/s",
                       "h2d_bytes_per_step": nq * 12,
                       "d2h_bytes_per_step": ((nq + 1) * 8 + nq * span * 8 + 4 if sharded is None
-                                             else (nq + 1) * 8 + nq * span * 12),
+                                             else (nq + 1) * 8
+                                             + nq * min(k, world * m) * (4 + h_gid.element_size())),
                       "ms_per_step": round(e2e_tot / e2e_steps, 3),
-                      "api": "paper_1908_11807_b200.query_knn(tree, (pinned numpy centers, k))"}
+                      "api": ("paper_1908_11807_b200.query_knn(tree, (pinned numpy centers, k))"
+                              if sharded is None else
+                              "paper_1908_11807_b200.distributed.query_knn_distributed("
+                              "sharded tree, pinned centers, k) -> pinned host arrays")}
 
     if sharded is not None:
         out["extra"] = {"sharded_build_ms": round(sharded["build_ms"], 3),

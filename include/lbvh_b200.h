@@ -267,6 +267,40 @@ int lbvh_brute_radius(const float *points, int64_t n, const float *centers, cons
                       float radius, int64_t nq, int32_t *counts, const int64_t *offsets,
                       int32_t *out, void *stream);
 
+/* ------------------------------------------- sharded search (multi-GPU) */
+
+/* Sharded kNN / radius helpers (distributed.py; no reference counterpart --
+ * the reference is single-process).  world <= 32 ranks.
+ * rank_forward_mask: mask[q] bit r set iff rank r is in `candidates` and its
+ * box (boxes: world x 6 f32) has fp32 distance^2 <= bound[q] (or radius2 when
+ * bound is NULL), the traversal's box-distance recipe. */
+int lbvh_rank_forward_mask(const float *centers, const float *bound, float radius2, int64_t m,
+                           const float *boxes, int world, uint32_t candidates, uint32_t *mask,
+                           void *stream);
+/* Renumber a local tree's leaves with global ordinals (map[local] ->
+ * global, < 2^31) in leaf_obj and in the packed leaf links, so its queries
+ * report -- and break distance ties by -- global ordinals. */
+int lbvh_remap_leaves(const lbvh_tree *tree, int32_t *leaf_obj, void *nodes, const int64_t *map,
+                      void *stream);
+/* Home kNN lists -> return arrays out_dist = sqrt(d^2) (f32) and out_gid
+ * (i32 global ordinal), m x kk, in row order; rows with merged_pos[q] >= 0
+ * take merged[merged_pos[q]] (kk sorted (d^2 bits << 32 | ordinal) keys).
+ * gids NULL: local_idx are global already.  merged_pos may be NULL. */
+int lbvh_knn_finalize(int64_t m, int kk, const int32_t *local_idx, const float *d2,
+                      const int64_t *gids, const int64_t *merged_pos, const uint64_t *merged,
+                      float *out_dist, int32_t *out_gid, void *stream);
+/* Home kNN results -> return rows of 1 + 2*kk i32: [qid, sqrt(d^2) bits x kk,
+ * global ordinal x kk].  Row q takes merged[merged_pos[q]] (kk sorted
+ * (d^2 bits << 32 | global ordinal) keys) when merged_pos[q] >= 0, else its
+ * local list (local_idx -> gids, d2; gids NULL = local_idx are global
+ * already).  merged_pos may be NULL. */
+int lbvh_knn_result_rows(int64_t m, int kk, const int32_t *qid, const int32_t *local_idx,
+                         const float *d2, const int64_t *gids, const int64_t *merged_pos,
+                         const uint64_t *merged, int32_t *rows, void *stream);
+/* Received return rows -> dist_out / gid_out (nq x kk) at row qid. */
+int lbvh_scatter_knn_rows(const int32_t *rows, int64_t m, int kk, float *dist_out,
+                          int64_t *gid_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,15 @@ _SIGS = {
                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_unpack_knn_keys": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.c_void_p], ctypes.c_int),
+    "lbvh_rank_forward_mask": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float, ctypes.c_int64,
+                                ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p,
+                                ctypes.c_void_p], ctypes.c_int),
+    "lbvh_knn_finalize": ([ctypes.c_int64, ctypes.c_int] + [ctypes.c_void_p] * 8, ctypes.c_int),
+    "lbvh_remap_leaves": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 4, ctypes.c_int),
+    "lbvh_knn_result_rows": ([ctypes.c_int64, ctypes.c_int] + [ctypes.c_void_p] * 8,
+                             ctypes.c_int),
+    "lbvh_scatter_knn_rows": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_brute_knn": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
                        ctypes.c_int),

@@ -93,6 +93,27 @@ class GpuEngine:
         rs = query_knn_squared(tree, (centers.contiguous(), k))
         return (rs.indices.to(torch.int64).reshape(m, kk), rs.distances.reshape(m, kk))
 
+    def knn_sq_raw(self, tree, centers: torch.Tensor, k: int):
+        """(m, min(k, n)) local ordinals (i32) and exact fp32 d^2, on device."""
+        from .traversal import query_knn_squared
+
+        m = int(centers.shape[0])
+        kk = min(k, tree.leaf_count)
+        rs = query_knn_squared(tree, (centers.contiguous(), k))
+        return rs.indices.reshape(m, kk), rs.distances.reshape(m, kk)
+
+    def globalize(self, tree, gids: torch.Tensor) -> None:
+        """Renumber the local tree's leaves with global ordinals (< 2^31): its
+        queries then report them and break distance ties by them."""
+        from . import _device as dv
+        from . import _lib
+
+        d = tree.device_arrays()
+        g = gids.to(torch.int64).contiguous()
+        _lib.check(_lib.lib().lbvh_remap_leaves(tree.ctree(), dv.ptr(d["leaf_obj"]),
+                                                dv.ptr(d["nodes"]), dv.ptr(g), dv.stream()))
+        tree._host.clear()  # host views are re-read on access
+
     def radius(self, tree, centers: torch.Tensor, radii: torch.Tensor):
         from .traversal import query_spatial_2p
 
@@ -123,13 +144,45 @@ def _comm_device(group, data_dev):
     return _COMM.get(group, data_dev)
 
 
-def _alltoallv(rows: torch.Tensor, dest: torch.Tensor, world: int, group=None):
-    """Send row i of ``rows`` to rank ``dest[i]``; returns (received rows,
-    per-source counts).  Counts are exchanged first, then the payload."""
-    cdev = _comm_device(group, rows.device)
+def _partition(dest: torch.Tensor, world: int):
+    """Stable partition of row indices by destination rank -> (order, counts
+    tensor).  On CUDA one radix pass of the library's sort over
+    ceil(log2 world) key bits; elsewhere torch."""
+    if dest.is_cuda and dest.numel() > 1 and world > 1:
+        from . import _device as dv
+        from . import _lib
+
+        n = int(dest.numel())
+        keys = dest.to(torch.int32).contiguous()
+        order = torch.arange(n, dtype=torch.int32, device=dest.device)
+        l = _lib.lib()
+        ws = dv.workspace(l.lbvh_sort_workspace_bytes(n))
+        bits = max(1, (world - 1).bit_length())
+        _lib.check(l.lbvh_sort_pairs(dv.ptr(keys), dv.ptr(order), n, bits, dv.ptr(ws),
+                                     ws.numel(), dv.stream()))
+        edges = torch.searchsorted(keys, torch.arange(world + 1, dtype=torch.int32,
+                                                      device=dest.device))
+        return order.to(torch.int64), (edges[1:] - edges[:-1]).to(torch.int64)
     order = torch.argsort(dest, stable=True)
-    send = rows[order].contiguous().to(cdev)
-    counts = torch.bincount(dest, minlength=world).to(torch.int64).to(cdev)
+    return order, torch.bincount(dest, minlength=world).to(torch.int64)
+
+
+def _alltoallv(rows: torch.Tensor, dest: torch.Tensor, world: int, group=None,
+               grouped_counts=None):
+    """Send row i of ``rows`` to rank ``dest[i]``; returns (received rows,
+    per-source counts).  Counts are exchanged first, then the payload.
+    ``grouped_counts`` (list): rows are already grouped by destination with
+    these counts (``dest`` is then ignored)."""
+    if world == 1:
+        return rows, [int(rows.shape[0])]
+    cdev = _comm_device(group, rows.device)
+    if grouped_counts is not None:
+        send = rows.contiguous().to(cdev)
+        counts = torch.tensor(grouped_counts, dtype=torch.int64, device=cdev)
+    else:
+        order, counts = _partition(dest, world)
+        send = rows[order].contiguous().to(cdev)
+        counts = counts.to(cdev)
     recv_counts = torch.empty_like(counts)
     dist.all_to_all_single(recv_counts, counts, group=group)
     sc, rc = counts.tolist(), recv_counts.tolist()
@@ -197,6 +250,7 @@ class DistributedBvh:
     rank: int
     group: object = None
     monotone: bool = True        # local ordinal order == global ordinal order
+    global_leaves: bool = False  # the local tree's leaves carry global ordinals
 
     @property
     def total(self) -> int:
@@ -258,8 +312,14 @@ def build_distributed(local_points, global_offset: int, engine=None, group=None,
     boxes = _all_gather(box.to(torch.float32), world, group)
     cnts = _all_gather(torch.tensor([m], dtype=torch.int64, device=dev), world, group)
     monotone = bool((rgids[1:] > rgids[:-1]).all().item()) if m > 1 else True
-    return DistributedBvh(engine, tree, rgids, torch.stack(boxes), [int(c.item()) for c in cnts],
-                          splitters >> 32, scene_lo, scene_hi, world, rank, group, monotone)
+    counts = [int(c.item()) for c in cnts]
+    global_leaves = False
+    if hasattr(engine, "globalize") and sum(counts) < 2 ** 31:
+        if tree is not None:
+            engine.globalize(tree, rgids)
+        global_leaves = True
+    return DistributedBvh(engine, tree, rgids, torch.stack(boxes), counts, splitters >> 32,
+                          scene_lo, scene_hi, world, rank, group, monotone, global_leaves)
 
 
 def _local_knn(t: DistributedBvh, centers: torch.Tensor, k: int):
@@ -271,7 +331,7 @@ def _local_knn(t: DistributedBvh, centers: torch.Tensor, k: int):
     if m and t.tree is not None:
         idx, dd = t.engine.knn_sq(t.tree, centers, k)
         kk = idx.shape[1]
-        gid[:, :kk] = t.gids[idx]
+        gid[:, :kk] = idx if t.global_leaves else t.gids[idx]
         d2[:, :kk] = dd
     return gid, d2
 
@@ -283,14 +343,132 @@ def _merge_keys(gid: torch.Tensor, d2: torch.Tensor) -> torch.Tensor:
     return torch.where(gid < 0, torch.full_like(key, torch.iinfo(torch.int64).max), key)
 
 
+def _merge_remote(own_keys_rows: torch.Tensor, brow: torch.Tensor, bq: torch.Tensor, k: int,
+                  kk: int, nresp: torch.Tensor, rows: torch.Tensor, mh: int):
+    """k smallest (d^2, global ordinal) keys of each listed row over its own
+    candidates and every responder's (bq rows: [row, d^2 x k, ordinal x k])."""
+    dev = own_keys_rows.device
+    nr = rows.numel()
+    pos = torch.full((mh,), -1, dtype=torch.int64, device=dev)
+    pos[rows] = torch.arange(nr, device=dev)
+    width = k * (1 + int(nresp[rows].max().item()))
+    cand = torch.full((nr, width), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    cand[:, :own_keys_rows.shape[1]] = own_keys_rows
+    if brow.numel():
+        o = torch.argsort(brow, stable=True)
+        brow_s = brow[o]
+        starts = torch.cumsum(nresp, 0) - nresp
+        slot = torch.arange(brow_s.numel(), device=dev) - starts[brow_s]
+        cols = (1 + slot)[:, None] * k + torch.arange(k, device=dev)[None, :]
+        cand[pos[brow_s][:, None], cols] = _merge_keys(
+            bq[o, 1 + k:1 + 2 * k].to(torch.int64),
+            bq[o, 1:1 + k].contiguous().view(torch.float32))
+    return torch.sort(cand, dim=1).values[:, :kk].contiguous(), pos
+
+
+def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
+    """query_knn_distributed on CUDA.  Results come back in the order the
+    queries were sent, so the origin scatters them with its own partition
+    permutation; library kernels compute the forwarding masks and the return
+    arrays, tensor ops touch only the forwarded minority (queries near a
+    rank boundary)."""
+    from . import _device as dv
+    from . import _lib
+
+    l = _lib.lib()
+    dev, world, g = t.engine.device, t.world, t.group
+    nq = int(c.shape[0])
+    kk = min(k, t.total)
+    # 1. to the home rank (its Morton range)
+    if world > 1:
+        codes = t.engine.morton(c, t.scene_lo, t.scene_hi)
+        home = torch.searchsorted(t.split_codes, codes, right=True)
+        order, counts = _partition(home, world)
+        hc, hcounts = _alltoallv(c[order], None, world, g, grouped_counts=counts.tolist())
+        hc = hc.contiguous()
+    else:
+        order, hc, hcounts = None, c.contiguous(), [nq]
+    mh = int(hc.shape[0])
+    nloc = t.counts[t.rank] if t.tree is not None else 0
+    if nloc:
+        lidx, ld2 = t.engine.knn_sq_raw(t.tree, hc, k)
+    else:
+        lidx = torch.empty((mh, 0), dtype=torch.int32, device=dev)
+        ld2 = torch.empty((mh, 0), dtype=torch.float32, device=dev)
+    if nloc >= k:
+        bound = ld2[:, k - 1].contiguous()
+    else:
+        bound = torch.full((mh,), math.inf, dtype=torch.float32, device=dev)
+    # 2. forward to the other ranks within the bound
+    cand_ranks = 0
+    for r in range(world):
+        if t.counts[r] > 0 and r != t.rank:
+            cand_ranks |= 1 << r
+    merged_pos = top = None
+    if cand_ranks:
+        mask = torch.zeros(mh, dtype=torch.int32, device=dev)
+        boxes = t.boxes.to(torch.float32).contiguous()
+        _lib.check(l.lbvh_rank_forward_mask(dv.ptr(hc), dv.ptr(bound), 0.0, mh, dv.ptr(boxes),
+                                            world, cand_ranks, dv.ptr(mask), dv.stream()))
+        sel = torch.nonzero(mask, as_tuple=True)[0]
+        shifts = torch.arange(world, dtype=torch.int32, device=dev)[None, :]
+        si, rr = torch.nonzero((mask[sel, None] >> shifts) & 1, as_tuple=True)
+        qi = sel[si]
+        frows = torch.empty((qi.numel(), 4), dtype=torch.float32, device=dev)
+        frows[:, :3] = hc[qi]
+        frows[:, 3] = qi.to(torch.int32).view(torch.float32)
+        fq, fcounts = _alltoallv(frows, rr, world, g)
+        f_gid, f_d2 = _local_knn(t, fq[:, :3].contiguous(), k)
+        back = torch.cat([fq[:, 3:4].contiguous().view(torch.int32), f_d2.view(torch.int32),
+                          f_gid.to(torch.int32)], dim=1)
+        bq, _ = _alltoallv(back, None, world, g, grouped_counts=fcounts)
+        # 3. merge at home, only for queries that got remote candidates
+        brow = bq[:, 0].to(torch.int64)
+        nresp = torch.bincount(brow, minlength=mh) if brow.numel() else torch.zeros(
+            mh, dtype=torch.int64, device=dev)
+        if nloc < kk:  # the home alone cannot fill a span: every query merges
+            mrows = torch.arange(mh, device=dev)
+        else:
+            mrows = torch.nonzero(nresp > 0, as_tuple=True)[0]
+        if mrows.numel():
+            if nloc:
+                lm = lidx[mrows].to(torch.int64)
+                own = _merge_keys(lm if t.global_leaves else t.gids[lm], ld2[mrows])
+            else:
+                own = torch.empty((mrows.numel(), 0), dtype=torch.int64, device=dev)
+            top, merged_pos = _merge_remote(own, brow, bq, k, kk, nresp, mrows, mh)
+    # 4. return arrays (sqrt(d^2), global ordinal), rows in arrival order
+    if nloc < kk:  # every row is merged; the local lists are not read
+        lidx = torch.zeros((mh, kk), dtype=torch.int32, device=dev)
+        ld2 = torch.zeros((mh, kk), dtype=torch.float32, device=dev)
+    rd = torch.empty((mh, kk), dtype=torch.float32, device=dev)
+    rg = torch.empty((mh, kk), dtype=torch.int32, device=dev)
+    _lib.check(l.lbvh_knn_finalize(mh, kk, dv.ptr(lidx.contiguous()), dv.ptr(ld2.contiguous()),
+                                   None if t.global_leaves else dv.ptr(t.gids),
+                                   dv.ptr(merged_pos), dv.ptr(top), dv.ptr(rd), dv.ptr(rg),
+                                   dv.stream()))
+    if world > 1:
+        gd, _ = _alltoallv(rd, None, world, g, grouped_counts=hcounts)
+        gg, _ = _alltoallv(rg, None, world, g, grouped_counts=hcounts)
+        rd = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+        rg = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+        rd[order] = gd
+        rg[order] = gg
+    offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
+    return offsets, rg.reshape(-1), rd.reshape(-1)
+
+
 def query_knn_distributed(t: DistributedBvh, centers, k: int):
     """Collective kNN over the sharded cloud.  Returns (offsets int64,
-    global ordinals int64, distances f32) for this rank's queries, in order;
-    spans are min(k, total) long, sorted by (distance, ordinal)."""
+    global ordinals, distances f32) for this rank's queries, in order; spans
+    are min(k, total) long, sorted by (distance, ordinal).  Ordinals are
+    int32 on the CUDA path (clouds below 2^31 points), int64 otherwise."""
     if k < 1:
         raise ValueError("k must be >= 1")
     dev, world, g = t.engine.device, t.world, t.group
     c = torch.as_tensor(centers, dtype=torch.float32).to(dev).reshape(-1, 3)
+    if c.is_cuda and isinstance(t.engine, GpuEngine) and world <= 32 and t.total < 2 ** 31:
+        return _query_knn_gpu(t, c, k)
     nq = int(c.shape[0])
     kk = min(k, t.total)
     # Payload rows are 32-bit words: f32 coordinates / d^2 and i32 indices
@@ -394,7 +572,8 @@ def query_spatial_distributed(t: DistributedBvh, centers, radius):
         cnt = off[1:] - off[:-1]
         owner = torch.repeat_interleave(torch.arange(m, device=dev), cnt)
         qcol = rq[:, 4].contiguous().view(torch.int32)
-        hit_rows = torch.stack([qcol[owner], t.gids[idx].to(torch.int32)], dim=1)
+        hit = idx if t.global_leaves else t.gids[idx]
+        hit_rows = torch.stack([qcol[owner], hit.to(torch.int32)], dim=1)
         hit_dest = src[owner]
     else:
         hit_rows = torch.empty((0, 2), dtype=torch.int32, device=dev)

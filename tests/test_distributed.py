@@ -156,5 +156,6 @@ def test_sharded_search_equals_single_process_gloo(split):
 
 
 @pytest.mark.gpu
-def test_sharded_search_gpu_engine():
-    _run("gpu", 20000, 0.5)
+@pytest.mark.parametrize("split", [0.5, 0.97, -1])
+def test_sharded_search_gpu_engine(split):
+    _run("gpu", 20000, split)
