@@ -376,12 +376,10 @@ def run_ours(args):
 
         def e2e_step():
             if sharded is not None:
-                off, gid, dd = D.query_knn_distributed(sharded["t"], pin.to(dev, non_blocking=True), k)
-                h_off.copy_(off, non_blocking=True)
-                h_gid[:gid.numel()].copy_(gid.reshape(-1), non_blocking=True)
-                h_dd[:dd.numel()].copy_(dd.reshape(-1), non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                return h_off, h_gid, h_dd
+                # pinned host queries in, pinned host results out, pipelined
+                # over chunks (H2D / sharded search / D2H overlap)
+                return D.query_knn_distributed_host(sharded["t"], pin, k,
+                                                    out=(h_off, h_gid, h_dd))
             rs = lb.query_knn(tree, (host_q, k))
             assert rs.indices.shape[0] == nq * min(k, m)
             return rs

@@ -49,7 +49,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["GpuEngine", "DistributedBvh", "build_distributed", "query_knn_distributed",
-           "query_spatial_distributed"]
+           "query_knn_distributed_host", "query_spatial_distributed"]
 
 
 # ---------------------------------------------------------------------------
@@ -546,6 +546,64 @@ def query_knn_distributed(t: DistributedBvh, centers, k: int):
     gid_out[qix] = got[:, 1 + kk:1 + 2 * kk].to(torch.int64)
     offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
     return offsets, gid_out.reshape(-1), dist_out.reshape(-1)
+
+
+def query_knn_distributed_host(t: DistributedBvh, centers, k: int, chunk: int = 1 << 21,
+                               out=None):
+    """Collective kNN for host (pinned or pageable numpy / CPU tensor) queries,
+    pipelined over chunks: the H2D copy of chunk i+1 and the D2H copy of
+    chunk i-1 overlap the sharded search of chunk i.  Every rank must pass
+    the same number of chunks (the chunk count is agreed with an all-reduce).
+    Returns numpy (offsets int64, ordinals, distances f32) -- views of pinned
+    buffers, or of ``out`` = (offsets, ordinals, distances) pinned tensors when
+    given.  Results are identical to :func:`query_knn_distributed`."""
+    dev, world, g = t.engine.device, t.world, t.group
+    host = torch.as_tensor(centers, dtype=torch.float32).reshape(-1, 3)
+    if not host.is_pinned():
+        host = host.pin_memory()
+    nq = int(host.shape[0])
+    kk = min(k, t.total)
+    nchunks = torch.tensor([max(1, -(-nq // chunk))], dtype=torch.int64, device=dev)
+    if world > 1:
+        nchunks = _all_reduce(nchunks, dist.ReduceOp.MAX, g)
+    nchunks = int(nchunks.item())
+    gid_dtype = torch.int32 if t.total < 2 ** 31 and dev.type == "cuda" else torch.int64
+    if out is None:
+        h_off = torch.empty(nq + 1, dtype=torch.int64, pin_memory=True)
+        h_gid = torch.empty(nq * kk, dtype=gid_dtype, pin_memory=True)
+        h_dd = torch.empty(nq * kk, dtype=torch.float32, pin_memory=True)
+    else:
+        h_off, h_gid, h_dd = out
+    comp = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    dev_c = torch.empty((nq, 3), dtype=torch.float32, device=dev)
+    d_off = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
+    e0 = torch.cuda.Event()
+    e0.record(comp)
+    s_out.wait_event(e0)
+    with torch.cuda.stream(s_out):
+        h_off.copy_(d_off, non_blocking=True)
+        d_off.record_stream(s_out)
+    per = -(-nq // nchunks) if nq else 0
+    for i in range(nchunks):
+        c0, c1 = min(nq, i * per), min(nq, (i + 1) * per)
+        e_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            dev_c[c0:c1].copy_(host[c0:c1], non_blocking=True)
+            e_in.record(s_in)
+        comp.wait_event(e_in)
+        off, gid, dd = query_knn_distributed(t, dev_c[c0:c1], k)
+        e_c = torch.cuda.Event()
+        e_c.record(comp)
+        s_out.wait_event(e_c)
+        with torch.cuda.stream(s_out):
+            h_gid[c0 * kk:c1 * kk].copy_(gid, non_blocking=True)
+            h_dd[c0 * kk:c1 * kk].copy_(dd, non_blocking=True)
+            gid.record_stream(s_out)
+            dd.record_stream(s_out)
+    s_out.synchronize()
+    comp.wait_stream(s_out)
+    return h_off.numpy(), h_gid.numpy(), h_dd.numpy()
 
 
 def query_spatial_distributed(t: DistributedBvh, centers, radius):

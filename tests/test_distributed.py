@@ -122,6 +122,12 @@ def _worker(rank, world, port, engine_kind, n_total, split, queue):
             for i in range(q.shape[0]):
                 assert np.array_equal(gid.cpu().numpy()[off[i]:off[i + 1]],
                                       np.sort(si[so[i]:so[i + 1]])), (r, i)
+        if engine_kind == "gpu":
+            # pipelined host entry point: chunk counts differ per rank
+            qh = q[:300 - 50 * rank]
+            ho, hg, hd = D.query_knn_distributed_host(t, qh, 10, chunk=64)
+            ko, ki, kd = oracle.query_knn(ref, qh, 10, threads=1)
+            assert np.array_equal(ho, ko) and np.array_equal(hg, ki) and hd.tobytes() == kd.tobytes()
         # k beyond the whole cloud
         off, gid, dd = D.query_knn_distributed(t, q[:5], n_total + 3)
         assert int(off[-1]) == 5 * n_total
