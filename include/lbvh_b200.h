@@ -76,6 +76,9 @@ typedef struct lbvh_tree {
     int32_t leaf_dir_bits;
     /* LBVH_TREE_* bits describing how the tree was built (0 = unknown). */
     int32_t flags;
+    /* Optional (n-1) x 128 B 4-wide records (lbvh_wide_records); used by
+     * lbvh_knn on LBVH_TREE_CODES30 trees. */
+    const void *nodes4;
 } lbvh_tree;
 
 /* Every leaf box is a point (built from (n, 3) input: maxs == mins). */
@@ -126,6 +129,12 @@ int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
 int lbvh_leaf_directory_bits(int64_t n);
 int lbvh_leaf_directory(const uint32_t *leaf_codes, int64_t n, int bits, uint32_t *dir,
                         void *stream);
+
+/* 4-wide kNN records of a built tree (n >= 2): record X holds, for each
+ * child C of internal node X, C itself if it is a leaf, else C's two
+ * children (boxes SoA + links), 128 B per internal node.  Layout only: kNN
+ * results are unchanged (no reference counterpart). */
+int lbvh_wide_records(const lbvh_tree *tree, void *nodes4, void *stream);
 
 /* morton_codes(points, scene_min, scene_max)   replaces morton.py:68-91
  * points n x 3 f64 (device); scene bounds host doubles (smin[3], smax[3]). */

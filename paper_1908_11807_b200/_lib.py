@@ -46,7 +46,7 @@ class CTree(ctypes.Structure):
                 ("leaf_obj", ctypes.c_void_p), ("nodes", ctypes.c_void_p),
                 ("root_box", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p),
                 ("leaf_dir", ctypes.c_void_p), ("leaf_dir_bits", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("nodes4", ctypes.c_void_p)]
 
 TREE_POINT_LEAVES = 0x1
 TREE_CODES30 = 0x2
@@ -57,6 +57,8 @@ _SIGS = {
     "lbvh_last_cuda_error": ([], ctypes.c_char_p),
     "lbvh_abi_version": ([], ctypes.c_int),
     "lbvh_leaf_directory_bits": ([ctypes.c_int64], ctypes.c_int),
+    "lbvh_wide_records": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p],
+                          ctypes.c_int),
     "lbvh_leaf_directory": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                              ctypes.c_void_p], ctypes.c_int),
     "lbvh_launch_count": ([], ctypes.c_uint64),

@@ -59,6 +59,7 @@ int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t,
 int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
                 void *, size_t, cudaStream_t);
 int leaf_directory(const uint32_t *, int64_t, int, uint32_t *, cudaStream_t);
+int wide_records(const lbvh_tree *, void *, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
         const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
         cudaStream_t);
@@ -94,7 +95,7 @@ const char *lbvh_strerror(int code) {
 
 const char *lbvh_last_cuda_error(void) { return g_cuda_err; }
 
-int lbvh_abi_version(void) { return 2; }
+int lbvh_abi_version(void) { return 3; }
 
 uint64_t lbvh_launch_count(void) { return launch_count(); }
 
@@ -141,6 +142,10 @@ int lbvh_pack(const lbvh_tree *tree, void *nodes, float *root_box, uint32_t *sta
 int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
                       void *stream) {
     return unpack_boxes(tree, node_mins, node_maxs, S(stream));
+}
+
+int lbvh_wide_records(const lbvh_tree *tree, void *nodes4, void *stream) {
+    return wide_records(tree, nodes4, S(stream));
 }
 
 int lbvh_leaf_directory_bits(int64_t n) {

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "internal.cuh"
 #include "topk.cuh"
+#include "seed.cuh"
 
 namespace lbvh {
 namespace {
@@ -194,55 +195,6 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
             for (int32_t j = 0; j < cnt; ++j) out[dst + j] = __ldcs(row + j);
         }
     }
-}
-
-// Search-radius seed for one query: the kk-th smallest distance^2 among the
-// 2*kk leaves that neighbour the query's Morton code in leaf order (a real
-// upper bound of the true k-th distance).  Leaves are found by a lower_bound
-// over the build's sorted leaf codes.
-template <int K>
-__device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, int kk,
-                                            float px, float py, float pz) {
-    const int64_t n = t.n;
-    const uint32_t *__restrict__ codes = t.leaf_codes;
-    int64_t lo = 0, hi = n;
-    if (t.leaf_dir) {
-        // lower_bound(qcode) lies in the bucket of its top leaf_dir_bits
-        const uint32_t p = qcode >> (30 - t.leaf_dir_bits);
-        lo = __ldg(t.leaf_dir + p);
-        hi = __ldg(t.leaf_dir + p + 1);
-    }
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (__ldg(codes + mid) < qcode)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    const int64_t w = 2 * (int64_t)kk;
-    int64_t w0 = lo - kk;
-    w0 = w0 < 0 ? 0 : w0;
-    w0 = (w0 + w > n) ? (n - w > 0 ? n - w : 0) : w0;
-    const int64_t w1 = (w0 + w < n) ? w0 + w : n;
-    float best[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) best[j] = (j < K - kk) ? -INFINITY : INFINITY;
-    const float *__restrict__ mn = t.node_mins + 3 * (n - 1);
-    const float *__restrict__ mx = t.node_maxs + 3 * (n - 1);
-    for (int64_t p = w0; p < w1; ++p) {
-        const float d = box_dist_sq(px, py, pz, __ldg(mn + 3 * p), __ldg(mn + 3 * p + 1),
-                                    __ldg(mn + 3 * p + 2), __ldg(mx + 3 * p),
-                                    __ldg(mx + 3 * p + 1), __ldg(mx + 3 * p + 2));
-        if (d < best[K - 1]) {
-            bool lt[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) lt[j] = best[j] <= d;
-#pragma unroll
-            for (int j = K - 1; j > 0; --j) best[j] = lt[j] ? best[j] : (lt[j - 1] ? d : best[j - 1]);
-            best[0] = lt[0] ? best[0] : d;
-        }
-    }
-    return best[K - 1];
 }
 
 // lower_bound(target) over the sorted 30-bit leaf codes through the leaf
@@ -1142,6 +1094,9 @@ int leaf_directory(const uint32_t *codes, int64_t n, int bits, uint32_t *dir,
     return check_launch();
 }
 
+int knn_wide(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
+             const int64_t *, int64_t, int32_t *, float *, bool, uint32_t *, cudaStream_t);
+
 int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
         int32_t *out_idx, float *out_dist, int flags, void *ws, size_t ws_bytes,
@@ -1188,6 +1143,12 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         return check_launch();                                                              \
     }
     const bool squared = (flags & LBVH_KNN_SQUARED) != 0;
+    static const int wide = env_int("LBVH_KNN_WIDE", 1);
+    if (wide && t->nodes4 && (t->flags & LBVH_TREE_CODES30) && !use_persistent && !packet) {
+        const int rc = knn_wide(t, centers, order, qcodes, nq, offsets, max_span, out_idx,
+                                out_dist, squared, status, stream);
+        if (rc >= 0) return rc;
+    }
     LBVH_KNN_CASE(4)
     LBVH_KNN_CASE(8)
     LBVH_KNN_CASE(10)

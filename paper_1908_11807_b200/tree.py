@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from typing import NamedTuple
 
+import os
+
 import numpy as np
 import torch
 
@@ -22,6 +24,11 @@ from . import _device as dv
 from . import _lib
 from .geometry import Box
 from .validation import check_boxes
+
+# 4-wide kNN records (LBVH_WIDE=1; A/B switch).  Measured slower than the
+# binary kernel at C2 (8.89 vs 8.48 ms, +0.9 ms build): the kNN kernel is
+# issue-bound and a 4-wide step costs more than two binary ones.
+_WIDE = os.environ.get("LBVH_WIDE", "0") == "1"
 
 __all__ = ["Bvh", "Topology", "build", "common_prefix", "find_split", "node_range",
            "generate_topology", "refit_bounds"]
@@ -173,7 +180,7 @@ def _ctree(d: dict, n: int) -> _lib.CTree:
     return _lib.CTree(n, dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]),
                       dv.ptr(d.get("left")), dv.ptr(d.get("right")), dv.ptr(d["leaf_obj"]),
                       dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), dv.ptr(d.get("leaf_codes")),
-                      dv.ptr(ld), bits, int(d.get("flags", 0)))
+                      dv.ptr(ld), bits, int(d.get("flags", 0)), dv.ptr(d.get("nodes4")))
 
 
 def _device_boxes(boxes):
@@ -225,6 +232,10 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
     d["leaf_dir"] = dv.empty((1 << bits) + 1, i32)
     _lib.check(l.lbvh_leaf_directory(dv.ptr(d["leaf_codes"]), n, bits, dv.ptr(d["leaf_dir"]),
                                      dv.stream()))
+    if morton_bits == 30 and n > 1 and _WIDE:
+        # 4-wide kNN records (layout of the same tree; kNN results unchanged)
+        d["nodes4"] = dv.empty((n - 1) * 128, torch.uint8)
+        _lib.check(l.lbvh_wide_records(_ctree(d, n), dv.ptr(d["nodes4"]), dv.stream()))
     if check:
         flags = status.read()
         if flags & _lib.FLAG_NONFINITE:
