@@ -193,6 +193,29 @@ def test_leaf_directory_is_lower_bound_of_bucket_starts(kind):
     assert np.array_equal(rk2.indices, ki) and rk2.distances.tobytes() == kd.tobytes()
 
 
+@pytest.mark.parametrize("kind", ["cube:filled", "sphere:hollow"])
+def test_wide_knn_records_same_results(kind):
+    """The 4-wide kNN layout (A/B switch LBVH_WIDE=1) returns the reference's
+    indices and distance bits."""
+    from paper_1908_11807_b200 import _device as dv, _lib
+
+    src, var = kind.split(":")
+    pts = datasets.generate(datasets.CloudSpec(src, var, 40_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 6_000, 1))
+    tree = lb.build(pts)
+    d = tree.device_arrays()
+    n = tree.leaf_count
+    d["nodes4"] = torch.empty((n - 1) * 128, dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().lbvh_wide_records(tree.ctree(), dv.ptr(d["nodes4"]), dv.stream()))
+    ref = oracle.build(pts)
+    for k in (1, 10, 16, 32):
+        ko, ki, kd = oracle.query_knn(ref, q, k)
+        rk = lb.query_knn(tree, (q, k))
+        assert np.array_equal(rk.offsets, ko)
+        assert np.array_equal(rk.indices, ki), k
+        assert rk.distances.tobytes() == kd.tobytes(), k
+
+
 def test_large_scale_properties_1e7():
     """Full C2 size: size-independent properties (sortedness of leaf codes,
     containment, root box == scene box), plus oracle parity on a query sample."""
