@@ -165,3 +165,45 @@ def test_sharded_search_equals_single_process_gloo(split):
 @pytest.mark.parametrize("split", [0.5, 0.97, -1])
 def test_sharded_search_gpu_engine(split):
     _run("gpu", 20000, split)
+
+
+def _worker_single(port, queue):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        dist.init_process_group("gloo", rank=0, world_size=1)
+        from paper_1908_11807_b200 import distributed as D
+        from oracle import oracle
+
+        torch.cuda.set_device(0)
+        pts = _cloud(5000, 0)
+        t = D.build_distributed(pts, 0)
+        assert t.global_leaves and t.total == 5000
+        q = np.random.default_rng(7).uniform(-20, 20, size=(400, 3)).astype(np.float32)
+        ref = oracle.build(pts, threads=1)
+        for k in (1, 10, 5003):
+            off, gid, dd = D.query_knn_distributed(t, torch.from_numpy(q).cuda(), k)
+            ko, ki, kd = oracle.query_knn(ref, q, k, threads=1)
+            assert np.array_equal(off.cpu().numpy(), ko) and np.array_equal(gid.cpu().numpy(), ki)
+            assert dd.cpu().numpy().tobytes() == kd.tobytes()
+        ho, hg, hd = D.query_knn_distributed_host(t, q, 10, chunk=128)
+        ko, ki, kd = oracle.query_knn(ref, q, 10, threads=1)
+        assert np.array_equal(hg, ki) and hd.tobytes() == kd.tobytes()
+        dist.destroy_process_group()
+        queue.put("ok")
+    except Exception:
+        import traceback
+
+        queue.put(traceback.format_exc())
+        raise
+
+
+@pytest.mark.gpu
+def test_sharded_search_single_rank_gpu():
+    """world_size 1: the sharded protocol without exchanges (BENCH_FORCE_SHARDED)."""
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    p = ctx.Process(target=_worker_single, args=(_free_port(), queue))
+    p.start()
+    p.join(timeout=600)
+    assert queue.get(timeout=5) == "ok"
