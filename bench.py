@@ -255,10 +255,17 @@ def run_ours(args):
         pts = lb.generate(lb.CloudSpec("cube", "filled", m, 0))
         qs = lb.generate(lb.CloudSpec("cube", "filled", nq, 1))
     else:
-        pts = lb.generate(lb.CloudSpec("cube", "filled", world * m, 0))[rank * m:(rank + 1) * m].copy()
-        qs = lb.generate(lb.CloudSpec("cube", "filled", world * nq, 1))[rank * nq:(rank + 1) * nq].copy()
-    pts_d = torch.from_numpy(pts).to(dev)
-    qs_d = torch.from_numpy(qs).to(dev)
+        # the global clouds generated on each GPU (bit-identical to numpy's)
+        # and sliced; the host copies feed the e2e leg and the CPU baseline
+        pts_d = lb.datasets.generate_device(
+            lb.CloudSpec("cube", "filled", world * m, 0), dev)[rank * m:(rank + 1) * m].clone()
+        qs_d = lb.datasets.generate_device(
+            lb.CloudSpec("cube", "filled", world * nq, 1), dev)[rank * nq:(rank + 1) * nq].clone()
+        torch.cuda.empty_cache()
+        pts, qs = pts_d.cpu().numpy(), qs_d.cpu().numpy()
+    if world == 1:
+        pts_d = torch.from_numpy(pts).to(dev)
+        qs_d = torch.from_numpy(qs).to(dev)
     r = lb.default_radius(k)
 
     timer = KernelTimer()
@@ -468,10 +475,8 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
     ex["radius_1p_b64_fell_back"] = bool(fb["f"])
 
     # C3: hollow-sphere sources vs filled queries, radius 2P
-    hs = lb.generate(lb.CloudSpec("sphere", "hollow", m, 2 * rank))
-    hs_d = torch.from_numpy(hs).to(dev)
+    hs_d = lb.datasets.generate_device(lb.CloudSpec("sphere", "hollow", m, 2 * rank), dev)
     htree = lb.build(hs_d)
-    del hs
 
     def c3_step():
         rs = lb.query_spatial_2p(htree, (qs_d, r))
@@ -496,7 +501,7 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
     for n_b in (10_000, 100_000, 1_000_000, 10_000_000, 100_000_000):
         if n_b > args.sweep_max:
             break
-        p_b = torch.from_numpy(lb.generate(lb.CloudSpec("cube", "filled", n_b, 0))).to(dev)
+        p_b = lb.datasets.generate_device(lb.CloudSpec("cube", "filled", n_b, 0), dev)
         reps = 10 if n_b <= 1_000_000 else 3
         tot, _, _ = timed_loop(lambda: lb.build(p_b), reps, 2)
         sweep[str(n_b)] = {"ms": round(tot / reps, 4),

@@ -276,6 +276,17 @@ int lbvh_brute_radius(const float *points, int64_t n, const float *centers, cons
                       float radius, int64_t nq, int32_t *counts, const int64_t *offsets,
                       int32_t *out, void *stream);
 
+/* ------------------------------------------------- benchmark clouds */
+
+/* datasets.generate(CloudSpec) on the device (datasets.py:95-153), bit for
+ * bit numpy's PCG64 stream: kind 0 cube:filled, 1 cube:hollow, 2
+ * sphere:hollow; a = count^(1/3), lim = float32(a); (st, inc) = numpy's
+ * PCG64(seed).state.  out: p x 3 f32.  sphere:hollow sets
+ * LBVH_FLAG_NONFINITE when numpy would redraw a point (norm < 1e-6). */
+int lbvh_generate_cloud(int kind, int64_t p, double a, float lim, uint64_t st_hi,
+                        uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, float *out,
+                        uint32_t *status, void *stream);
+
 /* ------------------------------------------- sharded search (multi-GPU) */
 
 /* Sharded kNN / radius helpers (distributed.py; no reference counterpart --

@@ -112,6 +112,8 @@ _SIGS = {
                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_unpack_knn_keys": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.c_void_p], ctypes.c_int),
+    "lbvh_generate_cloud": ([ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float]
+                            + [ctypes.c_uint64] * 4 + [ctypes.c_void_p] * 3, ctypes.c_int),
     "lbvh_rank_forward_mask": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float, ctypes.c_int64,
                                 ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p,
                                 ctypes.c_void_p], ctypes.c_int),

@@ -216,6 +216,18 @@ def test_wide_knn_records_same_results(kind):
         assert rk.distances.tobytes() == kd.tobytes(), k
 
 
+@pytest.mark.parametrize("shape,variant,count,seed", [
+    ("cube", "filled", 100_000, 0), ("cube", "filled", 100_000, 1), ("cube", "filled", 12_345, 7),
+    ("cube", "hollow", 100_000, 0), ("cube", "hollow", 9_999, 3),
+    ("sphere", "hollow", 100_000, 0), ("sphere", "hollow", 10_001, 5),
+    ("sphere", "filled", 5_000, 2), ("cube", "filled", 1, 0)])
+def test_device_generators_match_host(shape, variant, count, seed):
+    spec = datasets.CloudSpec(shape, variant, count, seed)
+    host = datasets.generate(spec)
+    dev = datasets.generate_device(spec)
+    assert dev.is_cuda and dev.cpu().numpy().tobytes() == host.tobytes()
+
+
 def test_large_scale_properties_1e7():
     """Full C2 size: size-independent properties (sortedness of leaf codes,
     containment, root box == scene box), plus oracle parity on a query sample."""
