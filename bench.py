@@ -397,9 +397,10 @@ def run_ours(args):
         out["e2e"] = {"value": round(world * nq * e2e_steps / (e2e_tot / 1e3), 1),
                       "unit": "queries/s",
                       "h2d_bytes_per_step": nq * 12,
-                      "d2h_bytes_per_step": ((nq + 1) * 8 + nq * span * 8 + 4 if sharded is None
-                                             else (nq + 1) * 8
-                                             + nq * min(k, world * m) * (4 + h_gid.element_size())),
+                      # offsets (uniform spans) are written by host threads
+                      "d2h_bytes_per_step": (nq * span * 8 + 4 if sharded is None
+                                             else nq * min(k, world * m)
+                                             * (4 + h_gid.element_size())),
                       "ms_per_step": round(e2e_tot / e2e_steps, 3),
                       "api": ("paper_1908_11807_b200.query_knn(tree, (pinned numpy centers, k))"
                               if sharded is None else

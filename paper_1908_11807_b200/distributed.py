@@ -577,13 +577,9 @@ def query_knn_distributed_host(t: DistributedBvh, centers, k: int, chunk: int = 
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     dev_c = torch.empty((nq, 3), dtype=torch.float32, device=dev)
-    d_off = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
-    e0 = torch.cuda.Event()
-    e0.record(comp)
-    s_out.wait_event(e0)
-    with torch.cuda.stream(s_out):
-        h_off.copy_(d_off, non_blocking=True)
-        d_off.record_stream(s_out)
+    from .traversal import _host_arange_into
+
+    off_jobs = _host_arange_into(h_off.numpy(), kk)  # host threads, no D2H
     per = -(-nq // nchunks) if nq else 0
     for i in range(nchunks):
         c0, c1 = min(nq, i * per), min(nq, (i + 1) * per)
@@ -603,6 +599,8 @@ def query_knn_distributed_host(t: DistributedBvh, centers, k: int, chunk: int = 
             dd.record_stream(s_out)
     s_out.synchronize()
     comp.wait_stream(s_out)
+    for j in off_jobs:
+        j.result()
     return h_off.numpy(), h_gid.numpy(), h_dd.numpy()
 
 

@@ -472,6 +472,29 @@ def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultS
     return ResultSet._trusted(offsets, out_idx, out_dist)
 
 
+_HOST_POOL = None
+# 1 (measured 16.07 vs 16.63 ms e2e at C2): host threads write the uniform
+# offsets instead of copying them from the device
+_HOST_OFFSETS = os.environ.get("LBVH_HOST_OFFSETS", "1") == "1"
+
+
+def _host_arange_into(out: np.ndarray, step: int, parts: int = 8):
+    """out[i] = i * step, filled by ``parts`` pool threads (numpy releases the
+    GIL); returns the futures."""
+    global _HOST_POOL
+    if _HOST_POOL is None:
+        import concurrent.futures as cf
+
+        _HOST_POOL = cf.ThreadPoolExecutor(max_workers=parts, thread_name_prefix="lbvh-host")
+    n = out.shape[0]
+    per = -(-n // parts)
+
+    def fill(c0, c1):
+        np.multiply(np.arange(c0, c1, dtype=np.int64), step, out=out[c0:c1])
+
+    return [_HOST_POOL.submit(fill, c0, min(n, c0 + per)) for c0 in range(0, n, per)]
+
+
 def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> ResultSet:
     """Host kNN batch as an H2D / compute / D2H pipeline over query chunks.
 
@@ -502,11 +525,18 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> 
     kws = dv.workspace(l.lbvh_knn_workspace_bytes(chunk))
     _lib.check(l.lbvh_knn_offsets(None, b.k, n, nq, dv.ptr(offsets), None, status.ptr,
                                   dv.ptr(ws), ws.numel(), comp.cuda_stream))
-    ev = torch.cuda.Event()
-    ev.record(comp)
-    s_out.wait_event(ev)
-    with torch.cuda.stream(s_out):
-        h_off.copy_(offsets, non_blocking=True)
+    # Uniform spans: the host offsets are arange(nq + 1) * span, written by
+    # host threads while the copy engines stream the results (saves 8 B per
+    # query of D2H, the pipeline's bound).
+    if _HOST_OFFSETS:
+        off_jobs = _host_arange_into(h_off.numpy(), span)
+    else:
+        off_jobs = []
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        s_out.wait_event(ev)
+        with torch.cuda.stream(s_out):
+            h_off.copy_(offsets, non_blocking=True)
     ct = tree.ctree()
     root_box = dv.ptr(tree.device_arrays()["root_box"])
     c_ptr, o_ptr = dv.ptr(dev_c), dv.ptr(offsets)
@@ -537,6 +567,8 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> 
             h_dist[c0 * span:c1 * span].copy_(out_dist[c0 * span:c1 * span], non_blocking=True)
     comp.wait_stream(s_out)
     comp.wait_stream(s_in)
+    for j in off_jobs:
+        j.result()
     _raise_flags(status.read())  # synchronises the current stream
     return ResultSet._trusted(h_off.numpy(), h_idx.numpy(), h_dist.numpy())
 
