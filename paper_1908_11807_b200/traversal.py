@@ -201,11 +201,23 @@ def _spatial_batch(queries) -> _Batch:
     b.host = True
     b.nq = int(centers.shape[0])
     if b.nq:
-        b.centers = dv.h2d(centers)
         if ra.ndim == 0:
             b.radius = float(ra)
+            if b.nq >= _PIPELINE_MIN and dv.is_pinned(centers):
+                # large pinned batch: 2P runs as a chunked H2D/compute/D2H pipeline
+                b.host_centers = centers
+                return b
         else:
             b.radii = dv.h2d(ra)
+        b.centers = dv.h2d(centers)
+    return b
+
+
+def _staged(b: _Batch) -> _Batch:
+    """Upload a batch kept on the host for the pipelined paths."""
+    if b.centers is None and b.host_centers is not None:
+        b.centers = dv.h2d(b.host_centers)
+        b.host_centers = None
     return b
 
 
@@ -368,12 +380,121 @@ def query_spatial_2p(tree: Bvh, queries, sort_queries: bool = True,
     b = _spatial_batch(queries)
     if b.nq == 0:
         return _empty_result(b.host, knn=False)
+    if b.host_centers is not None:
+        return _spatial_2p_pipelined(tree, b, sort_queries)
     status = dv.Status()
     _check_batch(b, status, radii=True)
     order = _order(tree, b, sort_queries)
     offsets, out = _spatial_2p_device(tree, b, order, status)
     offsets, out = _finish(b.host, status, offsets, out)
     return ResultSet._trusted(offsets, out)
+
+
+def _spatial_2p_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet:
+    """Host 2P batch (scalar radius, pinned centers) as a chunked pipeline:
+    while chunk i is counted on the device, chunk i-1's rows are compacted
+    (its total is read from a pinned scalar, not a stream sync) and its
+    offsets and hits stream to the host, and chunk i+1 is uploaded.  Every
+    query's hits are computed exactly as in the one-shot path; chunk offsets
+    are shifted by the running total, so the CRS equals the one-shot one."""
+    l = _lib.lib()
+    dev = dv.device()
+    nq = b.nq
+    C = _PIPELINE_CHUNK
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    status = dv.Status()
+    host_c = dv.as_tensor(b.host_centers)
+    dev_c = torch.empty((nq, 3), dtype=torch.float32, device=dev)
+    ct = tree.ctree()
+    root_box = dv.ptr(tree.device_arrays()["root_box"])
+    rows = _ROW_HITS
+    nch = -(-nq // C)
+    ws = dv.workspace(max(l.lbvh_query_workspace_bytes(C), l.lbvh_scan_workspace_bytes(C)))
+    slots = [dict(counts=dv.empty(C, torch.int32), buf=dv.empty((C, rows), torch.int32),
+                  offs=dv.empty(C + 1, torch.int64), over=dv.empty(C, torch.int32),
+                  over_n=dv.empty(1, torch.int32), order=dv.empty(C, torch.int32),
+                  tot_h=dv.pinned(1, torch.int64), over_h=dv.pinned(1, torch.int32),
+                  ev=torch.cuda.Event()) for _ in range(2)]
+    h_off = dv.pinned(nq + 1, torch.int64)
+    h_off[0] = 0
+    cap = max(nq * 16, 1 << 20)
+    h_idx = dv.pinned(cap, torch.int32)
+    base = 0
+    c_ptr = dv.ptr(dev_c)
+
+    def span(i):
+        return i * C, min(nq, (i + 1) * C)
+
+    def stage_count(i, sl):
+        c0, c1 = span(i)
+        m = c1 - c0
+        e_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            dev_c[c0:c1].copy_(host_c[c0:c1], non_blocking=True)
+            e_in.record(s_in)
+        comp.wait_event(e_in)
+        cc = c_ptr + 12 * c0
+        st = comp.cuda_stream
+        _lib.check(l.lbvh_check_queries(cc, m, None, status.ptr, st))
+        srt = sort_queries and m > 1
+        order = dv.ptr(sl["order"]) if srt else None
+        if srt:
+            _lib.check(l.lbvh_query_order(cc, m, root_box, _ORDER_BITS, order, None,
+                                          dv.ptr(ws), ws.numel(), st))
+        _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
+            ct, cc, None, b.radius, order, m, dv.ptr(sl["counts"]), dv.ptr(sl["buf"]), rows,
+            status.ptr, st)))
+        _lib.check(l.lbvh_exclusive_scan(dv.ptr(sl["counts"]), m, dv.ptr(sl["offs"]),
+                                         dv.ptr(ws), ws.numel(), st))
+        _lib.check(l.lbvh_select_overflow(order, dv.ptr(sl["counts"]), m, rows,
+                                          dv.ptr(sl["over"]), dv.ptr(sl["over_n"]), st))
+        sl["tot_h"].copy_(sl["offs"][m:m + 1], non_blocking=True)
+        sl["over_h"].copy_(sl["over_n"], non_blocking=True)
+        sl["ev"].record(comp)
+
+    def stage_fill(i, sl):
+        nonlocal base, cap, h_idx
+        c0, c1 = span(i)
+        m = c1 - c0
+        sl["ev"].synchronize()
+        total, n_over = int(sl["tot_h"][0]), int(sl["over_h"][0])
+        st = comp.cuda_stream
+        out = dv.empty(max(total, 1), torch.int32)
+        if total:
+            _lib.check(l.lbvh_compact(dv.ptr(sl["buf"]), rows, dv.ptr(sl["counts"]),
+                                      dv.ptr(sl["offs"]), m, dv.ptr(out), st))
+            if n_over:
+                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
+                    ct, c_ptr + 12 * c0, None, b.radius, dv.ptr(sl["over"]), n_over,
+                    dv.ptr(sl["offs"]), dv.ptr(out), None, 0, status.ptr, st)))
+        goff = sl["offs"][1:m + 1] + base
+        if base + total > cap:  # grow the host hit buffer (rare)
+            s_out.synchronize()
+            cap = max(2 * cap, base + total)
+            bigger = dv.pinned(cap, torch.int32)
+            bigger[:base].copy_(h_idx[:base])
+            h_idx = bigger
+        e = torch.cuda.Event()
+        e.record(comp)
+        s_out.wait_event(e)
+        with torch.cuda.stream(s_out):
+            h_off[c0 + 1:c1 + 1].copy_(goff, non_blocking=True)
+            if total:
+                h_idx[base:base + total].copy_(out[:total], non_blocking=True)
+            goff.record_stream(s_out)
+            out.record_stream(s_out)
+        base += total
+
+    for i in range(nch + 1):
+        if i < nch:
+            stage_count(i, slots[i % 2])
+        if i >= 1:
+            stage_fill(i - 1, slots[(i - 1) % 2])
+    comp.wait_stream(s_out)
+    comp.wait_stream(s_in)
+    _raise_flags(status.read())  # synchronises the current stream
+    return ResultSet._trusted(h_off.numpy(), h_idx.numpy()[:base])
 
 
 def query_spatial_1p(tree: Bvh, queries, buffer_size: int, sort_queries: bool = True,
@@ -384,7 +505,7 @@ def query_spatial_1p(tree: Bvh, queries, buffer_size: int, sort_queries: bool = 
     buffer_size = int(buffer_size)
     if buffer_size < 1:
         raise ValueError(f"buffer_size must be >= 1, got {buffer_size}")
-    b = _spatial_batch(queries)
+    b = _staged(_spatial_batch(queries))
     if b.nq == 0:
         return _empty_result(b.host, knn=False), False
     l = _lib.lib()

@@ -262,6 +262,30 @@ def test_large_scale_properties_1e7():
     assert np.array_equal(rk.indices, ki) and rk.distances.tobytes() == kd.tobytes()
 
 
+@pytest.mark.parametrize("radius", [0.0, 2.673, 4.5])
+def test_pipelined_host_radius_equals_device_path(radius):
+    """Large pinned host 2P batches run chunked (software-pipelined count /
+    fill / D2H); the CRS must equal the one-shot device path byte for byte
+    (4.5 gives ~38 hits per query: row overflows and host buffer growth)."""
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 300_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", (1 << 20) * 2 + 777, 1)) * 0.4
+    t = lb.build(pts)
+    pin = torch.empty(q.shape, dtype=torch.float32, pin_memory=True)
+    pin.numpy()[:] = q
+    host = lb.query_spatial_2p(t, (pin.numpy(), radius))
+    dev = lb.query_spatial_2p(t, (torch.from_numpy(q).cuda(), radius)).to_host()
+    assert isinstance(host.offsets, np.ndarray)
+    assert np.array_equal(host.offsets, dev.offsets)
+    assert np.array_equal(host.indices, dev.indices)
+    ref = oracle.build(pts)
+    so, si = oracle.query_spatial_2p(ref, q[-3000:], radius)
+    base = int(host.offsets[-3001])
+    assert np.array_equal(host.offsets[-3001:] - base, so)
+    assert np.array_equal(host.indices[base:], si)
+    unsorted = lb.query_spatial_2p(t, (pin.numpy(), radius), sort_queries=False)
+    assert np.array_equal(unsorted.offsets, host.offsets)
+
+
 def test_pipelined_host_knn_equals_device_path():
     """Large pinned host batches take the chunked H2D/compute/D2H pipeline;
     results must equal the one-shot device path and the oracle."""
