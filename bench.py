@@ -463,6 +463,22 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
         ex["radius_count_kernel_frac"] = round(
             nq * radius_bytes_per_query(hits, T_RAD_FILLED_1E7) / (cms / 1e3) / 1e9 / peak_gbs, 4)
 
+    # radius 2P end to end: pinned host centers in, numpy CRS out (the
+    # reference's call), chunk-pipelined H2D / count / fill / D2H
+    pin_q = torch.empty((nq, 3), dtype=torch.float32, pin_memory=True)
+    pin_q.copy_(qs_d)
+    host_q = pin_q.numpy()
+
+    def rad_e2e_step():
+        rs = lb.query_spatial_2p(tree, (host_q, r))
+        counts_box["e2e_total"] = int(rs.offsets[-1])
+        return rs
+
+    tot, _, _ = timed_loop(rad_e2e_step, max(2, steps // 2), 2)
+    ex["radius_2p_e2e_queries_per_sec"] = round(world * nq * max(2, steps // 2) / (tot / 1e3), 1)
+    ex["radius_2p_e2e_d2h_bytes_per_step"] = (nq + 1) * 8 + counts_box["e2e_total"] * 4
+    del pin_q, host_q
+
     # radius 1P, B=64 (max count at 1e7 is 33, so B=32 would fall back)
     fb = {}
 
