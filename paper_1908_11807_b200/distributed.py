@@ -42,6 +42,7 @@ CPU engine (the oracle) to exercise the routing on ``gloo``.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -366,40 +367,29 @@ def _merge_remote(own_keys_rows: torch.Tensor, brow: torch.Tensor, bq: torch.Ten
     return torch.sort(cand, dim=1).values[:, :kk].contiguous(), pos
 
 
-def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
-    """query_knn_distributed on CUDA.  Results come back in the order the
-    queries were sent, so the origin scatters them with its own partition
-    permutation; library kernels compute the forwarding masks and the return
-    arrays, tensor ops touch only the forwarded minority (queries near a
-    rank boundary)."""
+def _home_chunk(t: DistributedBvh, hc: torch.Tensor, k: int, kk: int):
+    """Home-side kNN of received queries ``hc`` (collective: every rank calls
+    it the same number of times): local kNN, forwarding to ranks within the
+    bound, merge, and the return arrays (sqrt(d^2) f32, global ordinal i32),
+    rows in ``hc`` order."""
     from . import _device as dv
     from . import _lib
 
     l = _lib.lib()
     dev, world, g = t.engine.device, t.world, t.group
-    nq = int(c.shape[0])
-    kk = min(k, t.total)
-    # 1. to the home rank (its Morton range)
-    if world > 1:
-        codes = t.engine.morton(c, t.scene_lo, t.scene_hi)
-        home = torch.searchsorted(t.split_codes, codes, right=True)
-        order, counts = _partition(home, world)
-        hc, hcounts = _alltoallv(c[order], None, world, g, grouped_counts=counts.tolist())
-        hc = hc.contiguous()
-    else:
-        order, hc, hcounts = None, c.contiguous(), [nq]
     mh = int(hc.shape[0])
     nloc = t.counts[t.rank] if t.tree is not None else 0
-    if nloc:
+    if nloc and mh:
         lidx, ld2 = t.engine.knn_sq_raw(t.tree, hc, k)
     else:
-        lidx = torch.empty((mh, 0), dtype=torch.int32, device=dev)
-        ld2 = torch.empty((mh, 0), dtype=torch.float32, device=dev)
+        kl = min(k, nloc)
+        lidx = torch.empty((mh, kl), dtype=torch.int32, device=dev)
+        ld2 = torch.empty((mh, kl), dtype=torch.float32, device=dev)
     if nloc >= k:
         bound = ld2[:, k - 1].contiguous()
     else:
         bound = torch.full((mh,), math.inf, dtype=torch.float32, device=dev)
-    # 2. forward to the other ranks within the bound
+    # forward to the other ranks within the bound
     cand_ranks = 0
     for r in range(world):
         if t.counts[r] > 0 and r != t.rank:
@@ -422,7 +412,7 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
         back = torch.cat([fq[:, 3:4].contiguous().view(torch.int32), f_d2.view(torch.int32),
                           f_gid.to(torch.int32)], dim=1)
         bq, _ = _alltoallv(back, None, world, g, grouped_counts=fcounts)
-        # 3. merge at home, only for queries that got remote candidates
+        # merge at home, only for queries that got remote candidates
         brow = bq[:, 0].to(torch.int64)
         nresp = torch.bincount(brow, minlength=mh) if brow.numel() else torch.zeros(
             mh, dtype=torch.int64, device=dev)
@@ -437,7 +427,7 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
             else:
                 own = torch.empty((mrows.numel(), 0), dtype=torch.int64, device=dev)
             top, merged_pos = _merge_remote(own, brow, bq, k, kk, nresp, mrows, mh)
-    # 4. return arrays (sqrt(d^2), global ordinal), rows in arrival order
+    # return arrays (sqrt(d^2), global ordinal), rows in arrival order
     if nloc < kk:  # every row is merged; the local lists are not read
         lidx = torch.zeros((mh, kk), dtype=torch.int32, device=dev)
         ld2 = torch.zeros((mh, kk), dtype=torch.float32, device=dev)
@@ -447,13 +437,94 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
                                    None if t.global_leaves else dv.ptr(t.gids),
                                    dv.ptr(merged_pos), dv.ptr(top), dv.ptr(rd), dv.ptr(rg),
                                    dv.stream()))
-    if world > 1:
-        gd, _ = _alltoallv(rd, None, world, g, grouped_counts=hcounts)
-        gg, _ = _alltoallv(rg, None, world, g, grouped_counts=hcounts)
-        rd = torch.empty((nq, kk), dtype=torch.float32, device=dev)
-        rg = torch.empty((nq, kk), dtype=torch.int32, device=dev)
-        rd[order] = gd
-        rg[order] = gg
+    return rd, rg
+
+
+# Home queries are processed in this many chunks when world > 1, so the
+# all-to-all returning chunk j's results overlaps chunk j+1's search.
+_SHARD_CHUNKS = int(os.environ.get("LBVH_SHARD_CHUNKS", "4"))
+
+
+class _PendingReturn:
+    """One chunk's result exchange in flight (split sizes already agreed)."""
+
+    def __init__(self, rd, rg, splits, world, group):
+        cdev = _comm_device(group, rd.device)
+        counts = torch.tensor(splits, dtype=torch.int64, device=cdev)
+        rcounts = torch.empty_like(counts)
+        dist.all_to_all_single(rcounts, counts, group=group)
+        self.rc = rcounts.tolist()
+        self.dev = rd.device
+        self.sends = (rd.contiguous().to(cdev), rg.contiguous().to(cdev))
+        self.recvs = tuple(torch.empty((sum(self.rc),) + tuple(x.shape[1:]), dtype=x.dtype,
+                                       device=cdev) for x in self.sends)
+        self.works = [dist.all_to_all_single(r, x, output_split_sizes=self.rc,
+                                             input_split_sizes=splits, group=group,
+                                             async_op=True)
+                      for r, x in zip(self.recvs, self.sends)]
+
+    def finish(self, gd, gg, cursor):
+        """Wait, then append each source's piece at its cursor."""
+        for w in self.works:
+            w.wait()
+        rd, rg = (x.to(self.dev) for x in self.recvs)
+        off = 0
+        for src, cnt in enumerate(self.rc):
+            if cnt:
+                gd[cursor[src]:cursor[src] + cnt] = rd[off:off + cnt]
+                gg[cursor[src]:cursor[src] + cnt] = rg[off:off + cnt]
+                cursor[src] += cnt
+                off += cnt
+
+
+def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
+    """query_knn_distributed on CUDA.  Results come back in the order the
+    queries were sent, so the origin scatters them with its own partition
+    permutation; library kernels compute the forwarding masks and the return
+    arrays, tensor ops touch only the forwarded minority (queries near a
+    rank boundary).  With several ranks the home work runs in chunks and
+    chunk j's results travel (asynchronous all-to-all) while chunk j+1 is
+    searched."""
+    dev, world, g = t.engine.device, t.world, t.group
+    nq = int(c.shape[0])
+    kk = min(k, t.total)
+    if world == 1:
+        rd, rg = _home_chunk(t, c.contiguous(), k, kk)
+        offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
+        return offsets, rg.reshape(-1), rd.reshape(-1)
+    # 1. to the home rank (its Morton range)
+    codes = t.engine.morton(c, t.scene_lo, t.scene_hi)
+    home = torch.searchsorted(t.split_codes, codes, right=True)
+    order, counts = _partition(home, world)
+    sent = counts.tolist()
+    hc, hcounts = _alltoallv(c[order], None, world, g, grouped_counts=sent)
+    hc = hc.contiguous()
+    mh = int(hc.shape[0])
+    # rows of origin o occupy [hstart[o], hstart[o + 1]) of hc
+    hstart = [0]
+    for x in hcounts:
+        hstart.append(hstart[-1] + x)
+    # results land grouped by home rank in send order (this rank's c[order])
+    gd = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+    gg = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+    cursor = [0]
+    for x in sent[:-1]:
+        cursor.append(cursor[-1] + x)
+    chunks = max(1, _SHARD_CHUNKS)
+    pending = None
+    for j in range(chunks):
+        r0, r1 = j * mh // chunks, (j + 1) * mh // chunks
+        rd, rg = _home_chunk(t, hc[r0:r1], k, kk)
+        splits = [max(0, min(r1, hstart[o + 1]) - max(r0, hstart[o])) for o in range(world)]
+        nxt = _PendingReturn(rd, rg, splits, world, g)
+        if pending is not None:
+            pending.finish(gd, gg, cursor)
+        pending = nxt
+    pending.finish(gd, gg, cursor)
+    rd = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+    rg = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+    rd[order] = gd
+    rg[order] = gg
     offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
     return offsets, rg.reshape(-1), rd.reshape(-1)
 
