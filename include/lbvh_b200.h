@@ -141,6 +141,11 @@ int lbvh_wide_records(const lbvh_tree *tree, void *nodes4, void *stream);
 int lbvh_morton_codes(const double *points, int64_t n, const double *scene_min_host,
                       const double *scene_max_host, uint32_t *codes, void *stream);
 
+/* The same 30-bit codes from f32 points (device) on a device scene box of 6
+ * f32 (min xyz, max xyz): coordinates convert to f64 exactly. */
+int lbvh_morton_codes_f32(const float *points, int64_t n, const float *scene_box,
+                          uint32_t *codes, void *stream);
+
 /* Stable LSD radix sort of (key, value) pairs, in place; sorts the low
  * key_bits bits.  Replaces np.argsort(kind="stable") (tree.py:194) when
  * values are the identity. */
@@ -317,6 +322,9 @@ int lbvh_knn_finalize(int64_t m, int kk, const int32_t *local_idx, const float *
 int lbvh_knn_result_rows(int64_t m, int kk, const int32_t *qid, const int32_t *local_idx,
                          const float *d2, const int64_t *gids, const int64_t *merged_pos,
                          const uint64_t *merged, int32_t *rows, void *stream);
+/* m received rows (rd f32, rg i32; m x kk) -> out_d / out_g rows dst[i]. */
+int lbvh_scatter_result_rows(int64_t m, int kk, const int64_t *dst, const float *rd,
+                             const int32_t *rg, float *out_d, int32_t *out_g, void *stream);
 /* Received return rows -> dist_out / gid_out (nq x kk) at row qid. */
 int lbvh_scatter_knn_rows(const int32_t *rows, int64_t m, int kk, float *dist_out,
                           int64_t *gid_out, void *stream);

@@ -861,6 +861,18 @@ size_t query_workspace_bytes(int64_t nq) {
     return align_up(sizeof(uint32_t) * (size_t)nq) + sort_workspace_bytes(nq) + 512;
 }
 
+// 30-bit codes of f32 points on a device scene box (6 f32): the f64
+// recipe of morton_kernel on exactly-converted coordinates.
+int morton_codes_f32(const float *pts, int64_t n, const float *scene, uint32_t *codes,
+                     cudaStream_t stream) {
+    if (n < 0 || (n > 0 && (!pts || !scene || !codes))) return LBVH_ERR_INVALID_ARG;
+    if (n == 0) return LBVH_OK;
+    morton_kernel<uint32_t><<<grid_for(n, 256, 16), 256, 0, stream>>>(pts, pts, n, scene, codes,
+                                                                       nullptr);
+    count_launches(1);
+    return check_launch();
+}
+
 int query_order(const float *centers, int64_t nq, const float *scene, int order_bits,
                 uint32_t *order, uint32_t *sorted_codes, void *ws, size_t ws_bytes,
                 cudaStream_t stream) {

@@ -59,6 +59,7 @@ int compact(const int32_t *, int64_t, const int32_t *, const int64_t *, int64_t,
 int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *, uint32_t *,
                 void *, size_t, cudaStream_t);
 int leaf_directory(const uint32_t *, int64_t, int, uint32_t *, cudaStream_t);
+int morton_codes_f32(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
 int wide_records(const lbvh_tree *, void *, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
         const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
@@ -116,6 +117,11 @@ int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
 int lbvh_morton_codes(const double *pts, int64_t n, const double *lo, const double *hi,
                       uint32_t *codes, void *stream) {
     return morton_codes_f64(pts, n, lo, hi, codes, S(stream));
+}
+
+int lbvh_morton_codes_f32(const float *points, int64_t n, const float *scene_box,
+                          uint32_t *codes, void *stream) {
+    return morton_codes_f32(points, n, scene_box, codes, S(stream));
 }
 
 int lbvh_sort_pairs(uint32_t *keys, uint32_t *values, int64_t n, int key_bits, void *ws,

@@ -138,6 +138,23 @@ knn_finalize_kernel(int64_t m, int kk, const int32_t *__restrict__ local_idx,
     }
 }
 
+// Received result rows of one source -> final (nq, kk) outputs:
+// row i lands at query dst[i] (the origin's partition permutation slice).
+__global__ void __launch_bounds__(256)
+scatter_rows_kernel(int64_t m, int kk, const int64_t *__restrict__ dst,
+                    const float *__restrict__ rd, const int32_t *__restrict__ rg,
+                    float *__restrict__ out_d, int32_t *__restrict__ out_g) {
+    const int64_t total = m * kk;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / kk;
+        const int64_t q = __ldg(dst + i);
+        const int64_t o = q * kk + (e - i * kk);
+        out_d[o] = __ldg(rd + e);
+        out_g[o] = __ldg(rg + e);
+    }
+}
+
 // Leaf ordinals of a local tree -> global ordinals (map[local] = global), in
 // leaf_obj and in the packed nodes' leaf links.
 __global__ void __launch_bounds__(256)
@@ -191,6 +208,18 @@ int lbvh_knn_finalize(int64_t m, int kk, const int32_t *local_idx, const float *
     knn_finalize_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(m, kk, local_idx, d2, gids,
                                                             merged_pos, merged, out_dist,
                                                             out_gid);
+    count_launches(1);
+    return check_launch();
+}
+
+int lbvh_scatter_result_rows(int64_t m, int kk, const int64_t *dst, const float *rd,
+                             const int32_t *rg, float *out_d, int32_t *out_g, void *stream) {
+    if (m < 0 || kk < 1 || (m > 0 && (!dst || !rd || !rg || !out_d || !out_g)))
+        return LBVH_ERR_INVALID_ARG;
+    if (m == 0) return LBVH_OK;
+    unsigned g = div_up(m * kk, 256);
+    g = g < kNumSMs * 16 ? g : kNumSMs * 16;
+    scatter_rows_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(m, kk, dst, rd, rg, out_d, out_g);
     count_launches(1);
     return check_launch();
 }

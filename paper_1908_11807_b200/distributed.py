@@ -78,6 +78,20 @@ class GpuEngine:
                                                     hi.ctypes.data, dv.ptr(codes), dv.stream()))
         return codes.to(torch.int64)
 
+    def morton32(self, pts: torch.Tensor, box: torch.Tensor) -> torch.Tensor:
+        """i32 codes of f32 points on a device (6,) f32 scene box -- the same
+        codes as :meth:`morton` without the f64 staging copy."""
+        from . import _device as dv
+        from . import _lib
+
+        n = int(pts.shape[0])
+        codes = torch.empty(n, dtype=torch.int32, device=self.device)
+        if n:
+            _lib.check(_lib.lib().lbvh_morton_codes_f32(dv.ptr(pts.contiguous()), n,
+                                                        dv.ptr(box), dv.ptr(codes),
+                                                        dv.stream()))
+        return codes
+
     def build(self, pts: torch.Tensor):
         from .tree import build
 
@@ -149,7 +163,7 @@ def _partition(dest: torch.Tensor, world: int):
     """Stable partition of row indices by destination rank -> (order, counts
     tensor).  On CUDA one radix pass of the library's sort over
     ceil(log2 world) key bits; elsewhere torch."""
-    if dest.is_cuda and dest.numel() > 1 and world > 1:
+    if dest.is_cuda and dest.numel() > 1:
         from . import _device as dv
         from . import _lib
 
@@ -440,9 +454,13 @@ def _home_chunk(t: DistributedBvh, hc: torch.Tensor, k: int, kk: int):
     return rd, rg
 
 
-# Home queries are processed in this many chunks when world > 1, so the
-# all-to-all returning chunk j's results overlaps chunk j+1's search.
-_SHARD_CHUNKS = int(os.environ.get("LBVH_SHARD_CHUNKS", "4"))
+# Home queries can be processed in chunks when world > 1 so that the
+# all-to-all returning chunk j's results overlaps chunk j+1's search; each
+# chunk adds host syncs (measured on one GPU, routed: 12.0 / 13.3 / 14.2 ms
+# per 1e7-query step for 1 / 2 / 4 chunks), so the default is 1.
+_SHARD_CHUNKS = int(os.environ.get("LBVH_SHARD_CHUNKS", "1"))
+# measurement switch: take the routed (partition + exchange) path even on one rank
+_FORCE_ROUTE = os.environ.get("LBVH_SHARD_FORCE_ROUTE", "0") == "1"
 
 
 class _PendingReturn:
@@ -463,16 +481,24 @@ class _PendingReturn:
                                              async_op=True)
                       for r, x in zip(self.recvs, self.sends)]
 
-    def finish(self, gd, gg, cursor):
-        """Wait, then append each source's piece at its cursor."""
+    def finish(self, order, out_d, out_g, cursor):
+        """Wait, then scatter each source's piece straight to its queries:
+        piece rows are the next ``cnt`` entries of that source's slice of the
+        origin's partition permutation ``order``."""
+        from . import _device as dv
+        from . import _lib
+
         for w in self.works:
             w.wait()
         rd, rg = (x.to(self.dev) for x in self.recvs)
+        kk = out_d.shape[1]
         off = 0
         for src, cnt in enumerate(self.rc):
             if cnt:
-                gd[cursor[src]:cursor[src] + cnt] = rd[off:off + cnt]
-                gg[cursor[src]:cursor[src] + cnt] = rg[off:off + cnt]
+                _lib.check(_lib.lib().lbvh_scatter_result_rows(
+                    cnt, kk, dv.ptr(order[cursor[src]:cursor[src] + cnt]),
+                    dv.ptr(rd[off:off + cnt]), dv.ptr(rg[off:off + cnt]), dv.ptr(out_d),
+                    dv.ptr(out_g), dv.stream()))
                 cursor[src] += cnt
                 off += cnt
 
@@ -488,13 +514,14 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
     dev, world, g = t.engine.device, t.world, t.group
     nq = int(c.shape[0])
     kk = min(k, t.total)
-    if world == 1:
+    if world == 1 and not _FORCE_ROUTE:
         rd, rg = _home_chunk(t, c.contiguous(), k, kk)
         offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
         return offsets, rg.reshape(-1), rd.reshape(-1)
     # 1. to the home rank (its Morton range)
-    codes = t.engine.morton(c, t.scene_lo, t.scene_hi)
-    home = torch.searchsorted(t.split_codes, codes, right=True)
+    box = torch.tensor(np.concatenate([t.scene_lo, t.scene_hi]).astype(np.float32), device=dev)
+    codes = t.engine.morton32(c, box)
+    home = torch.searchsorted(t.split_codes.to(torch.int32), codes, right=True)
     order, counts = _partition(home, world)
     sent = counts.tolist()
     hc, hcounts = _alltoallv(c[order], None, world, g, grouped_counts=sent)
@@ -504,9 +531,10 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
     hstart = [0]
     for x in hcounts:
         hstart.append(hstart[-1] + x)
-    # results land grouped by home rank in send order (this rank's c[order])
-    gd = torch.empty((nq, kk), dtype=torch.float32, device=dev)
-    gg = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+    # results are scattered straight into query order: a piece from home h
+    # covers the next rows of h's slice of this rank's send order
+    rd_out = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+    rg_out = torch.empty((nq, kk), dtype=torch.int32, device=dev)
     cursor = [0]
     for x in sent[:-1]:
         cursor.append(cursor[-1] + x)
@@ -518,15 +546,11 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
         splits = [max(0, min(r1, hstart[o + 1]) - max(r0, hstart[o])) for o in range(world)]
         nxt = _PendingReturn(rd, rg, splits, world, g)
         if pending is not None:
-            pending.finish(gd, gg, cursor)
+            pending.finish(order, rd_out, rg_out, cursor)
         pending = nxt
-    pending.finish(gd, gg, cursor)
-    rd = torch.empty((nq, kk), dtype=torch.float32, device=dev)
-    rg = torch.empty((nq, kk), dtype=torch.int32, device=dev)
-    rd[order] = gd
-    rg[order] = gg
+    pending.finish(order, rd_out, rg_out, cursor)
     offsets = torch.arange(nq + 1, dtype=torch.int64, device=dev) * kk
-    return offsets, rg.reshape(-1), rd.reshape(-1)
+    return offsets, rg_out.reshape(-1), rd_out.reshape(-1)
 
 
 def query_knn_distributed(t: DistributedBvh, centers, k: int):
