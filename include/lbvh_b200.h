@@ -260,6 +260,15 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              int64_t max_span, int32_t *out_idx, float *out_dist, int flags,
              void *workspace, size_t workspace_bytes, uint32_t *status, void *stream);
 
+/* lbvh_knn that also writes kth_d2[q] = the exact squared distance of query
+ * q's last (k-th) neighbour -- the sharded search's forwarding bound -- so
+ * the outputs can be the final sqrt'ed lists.  max_span <= 32 only. */
+int lbvh_knn_kth(const lbvh_tree *tree, const float *centers, const uint32_t *order,
+                 const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
+                 int64_t max_span, int32_t *out_idx, float *out_dist, int flags,
+                 void *workspace, size_t workspace_bytes, uint32_t *status, float *kth_d2,
+                 void *stream);
+
 /* Distributed kNN merge epilogue (no reference counterpart):
  * merged candidate keys (dist^2 bits << 32 | global ordinal) -> ordinals and
  * correctly rounded distances sqrt(dist^2), as knn_pass's final sqrt

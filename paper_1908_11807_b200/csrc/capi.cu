@@ -63,7 +63,7 @@ int morton_codes_f32(const float *, int64_t, const float *, uint32_t *, cudaStre
 int wide_records(const lbvh_tree *, void *, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
         const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
-        cudaStream_t);
+        cudaStream_t, float *);
 size_t knn_workspace_bytes(int64_t nq);
 int select_overflow(const uint32_t *, const int32_t *, int64_t, int64_t, uint32_t *, uint32_t *,
                     cudaStream_t);
@@ -220,7 +220,17 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              int32_t *out_idx, float *out_dist, int flags, void *workspace,
              size_t workspace_bytes, uint32_t *status, void *stream) {
     return knn(tree, centers, order, query_codes, nq, offsets, max_span, out_idx, out_dist,
-               flags, workspace, workspace_bytes, status, S(stream));
+               flags, workspace, workspace_bytes, status, S(stream), nullptr);
+}
+
+int lbvh_knn_kth(const lbvh_tree *tree, const float *centers, const uint32_t *order,
+                 const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
+                 int64_t max_span, int32_t *out_idx, float *out_dist, int flags,
+                 void *workspace, size_t workspace_bytes, uint32_t *status, float *kth_d2,
+                 void *stream) {
+    if (!kth_d2) return LBVH_ERR_INVALID_ARG;
+    return knn(tree, centers, order, query_codes, nq, offsets, max_span, out_idx, out_dist,
+               flags, workspace, workspace_bytes, status, S(stream), kth_d2);
 }
 
 size_t lbvh_knn_workspace_bytes(int64_t nq) { return knn_workspace_bytes(nq); }

@@ -118,9 +118,10 @@ knn_finalize_kernel(int64_t m, int kk, const int32_t *__restrict__ local_idx,
                     const int64_t *__restrict__ merged_pos, const uint64_t *__restrict__ merged,
                     float *__restrict__ out_dist, int32_t *__restrict__ out_gid) {
     const int64_t total = m * kk;
+    const bool narrow = total < (1ll << 32);  // 32-bit row/column split
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t q = e / kk;
+        const int64_t q = narrow ? (int64_t)((uint32_t)e / (uint32_t)kk) : e / kk;
         const int64_t mp = merged_pos ? __ldg(merged_pos + q) : -1;
         float dd;
         int32_t g;
@@ -145,9 +146,10 @@ scatter_rows_kernel(int64_t m, int kk, const int64_t *__restrict__ dst,
                     const float *__restrict__ rd, const int32_t *__restrict__ rg,
                     float *__restrict__ out_d, int32_t *__restrict__ out_g) {
     const int64_t total = m * kk;
+    const bool narrow = total < (1ll << 32);
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / kk;
+        const int64_t i = narrow ? (int64_t)((uint32_t)e / (uint32_t)kk) : e / kk;
         const int64_t q = __ldg(dst + i);
         const int64_t o = q * kk + (e - i * kk);
         out_d[o] = __ldg(rd + e);

@@ -294,7 +294,7 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
                                           const int64_t *__restrict__ offsets,
                                           int32_t *__restrict__ out_idx,
                                           float *__restrict__ out_dist, bool squared,
-                                          uint32_t *status) {
+                                          uint32_t *status, float *__restrict__ kth = nullptr) {
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
     const int64_t base = __ldg(offsets + q);
     const int kk = (int)(__ldg(offsets + q + 1) - base);
@@ -469,6 +469,8 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         }
     }
     if (fail) atomicOr(status, fail);
+    // the k-th squared distance (exact; the sharded search's forwarding bound)
+    if (kth) kth[q] = top.dist(K - 1);
     // Spans are written even after a failure; the driver raises anyway.
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -486,11 +488,11 @@ __global__ void __launch_bounds__(LBVH_KNN_BLOCK,
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
            const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-           float *__restrict__ out_dist, bool squared, uint32_t *status) {
+           float *__restrict__ out_dist, bool squared, uint32_t *status, float *kth) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
     knn_query<K, REGNEXT>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
-                          status);
+                          status, kth);
 }
 
 // Persistent warps: each warp takes the next 32 Morton-consecutive query
@@ -1100,7 +1102,8 @@ int knn_wide(const lbvh_tree *, const float *, const uint32_t *, const uint32_t 
 int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
         int32_t *out_idx, float *out_dist, int flags, void *ws, size_t ws_bytes,
-        uint32_t *status, cudaStream_t stream) {
+        uint32_t *status, cudaStream_t stream, float *kth) {
+    if (kth && max_span > 32) return LBVH_ERR_INVALID_ARG;  // register-list kernels only
     if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0 || max_span <= 0) return LBVH_OK;
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
@@ -1114,10 +1117,10 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     // L1 locality), so off by default; kept as an A/B variant.
     static const int persistent = env_int("LBVH_KNN_PERSISTENT", 0);
     if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
-    const bool use_persistent = persistent && ws && ws_bytes >= knn_workspace_bytes(nq);
+    const bool use_persistent = persistent && !kth && ws && ws_bytes >= knn_workspace_bytes(nq);
     static const int packet = env_int("LBVH_KNN_PACKET", 0);
     static const int warpq = env_int("LBVH_KNN_WARPQ", 0);
-    const bool use_warpq = warpq && ws && ws_bytes >= knn_workspace_bytes(nq);
+    const bool use_warpq = warpq && !kth && ws && ws_bytes >= knn_workspace_bytes(nq);
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
         if (use_persistent)                                                                 \
@@ -1127,24 +1130,25 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         if (use_warpq)                                                                      \
             return launch_knn_warpq<KV>(t, centers, order, qcodes, nq, offsets, out_idx,     \
                                         out_dist, squared, status, ws, stream);             \
-        if (packet)                                                                         \
+        if (packet && !kth)                                                                 \
             knn_packet_kernel<KV><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, \
                                                                  nq, offsets, out_idx,       \
                                                                  out_dist, squared, status); \
         else if (variant == 1)                                                              \
             knn_kernel<KV, true><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,     \
                                                         offsets, out_idx, out_dist, squared, \
-                                                        status);                            \
+                                                        status, kth);                       \
         else                                                                                \
             knn_kernel<KV, false><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,    \
                                                          offsets, out_idx, out_dist,        \
-                                                         squared, status);                  \
+                                                         squared, status, kth);             \
         count_launches(1);                                                                  \
         return check_launch();                                                              \
     }
     const bool squared = (flags & LBVH_KNN_SQUARED) != 0;
     static const int wide = env_int("LBVH_KNN_WIDE", 1);
-    if (wide && t->nodes4 && (t->flags & LBVH_TREE_CODES30) && !use_persistent && !packet) {
+    if (wide && !kth && t->nodes4 && (t->flags & LBVH_TREE_CODES30) && !use_persistent &&
+        !packet) {
         const int rc = knn_wide(t, centers, order, qcodes, nq, offsets, max_span, out_idx,
                                 out_dist, squared, status, stream);
         if (rc >= 0) return rc;

@@ -108,6 +108,13 @@ class GpuEngine:
         rs = query_knn_squared(tree, (centers.contiguous(), k))
         return (rs.indices.to(torch.int64).reshape(m, kk), rs.distances.reshape(m, kk))
 
+    def knn_final(self, tree, centers: torch.Tensor, k: int):
+        """Final lists in one kernel: (ordinals i32 (m, kk), sqrt distances
+        f32 (m, kk), exact k-th d^2 (m,)); k <= 32."""
+        from .traversal import knn_with_kth
+
+        return knn_with_kth(tree, centers.contiguous(), k)
+
     def knn_sq_raw(self, tree, centers: torch.Tensor, k: int):
         """(m, min(k, n)) local ordinals (i32) and exact fp32 d^2, on device."""
         from .traversal import query_knn_squared
@@ -393,6 +400,8 @@ def _home_chunk(t: DistributedBvh, hc: torch.Tensor, k: int, kk: int):
     dev, world, g = t.engine.device, t.world, t.group
     mh = int(hc.shape[0])
     nloc = t.counts[t.rank] if t.tree is not None else 0
+    if (nloc and mh and k <= 32 and t.global_leaves and hasattr(t.engine, "knn_final")):
+        return _home_chunk_fused(t, hc, k, kk)
     if nloc and mh:
         lidx, ld2 = t.engine.knn_sq_raw(t.tree, hc, k)
     else:
@@ -451,6 +460,62 @@ def _home_chunk(t: DistributedBvh, hc: torch.Tensor, k: int, kk: int):
                                    None if t.global_leaves else dv.ptr(t.gids),
                                    dv.ptr(merged_pos), dv.ptr(top), dv.ptr(rd), dv.ptr(rg),
                                    dv.stream()))
+    return rd, rg
+
+
+def _home_chunk_fused(t: DistributedBvh, hc: torch.Tensor, k: int, kk: int):
+    """_home_chunk whose local kNN writes the final lists (sqrt distances,
+    global ordinals) and the exact k-th d^2 bound in one kernel; only the
+    queries that received remote candidates are searched again (squared) to
+    merge, and their rows are overwritten."""
+    from . import _device as dv
+    from . import _lib
+
+    l = _lib.lib()
+    dev, world, g = t.engine.device, t.world, t.group
+    mh = int(hc.shape[0])
+    nloc = t.counts[t.rank]
+    rg, rd, kth = t.engine.knn_final(t.tree, hc, k)
+    bound = kth if nloc >= k else torch.full((mh,), math.inf, dtype=torch.float32, device=dev)
+    if rg.shape[1] < kk:  # the home alone cannot fill a span: every row is merged below
+        rg = torch.empty((mh, kk), dtype=torch.int32, device=dev)
+        rd = torch.empty((mh, kk), dtype=torch.float32, device=dev)
+    cand_ranks = 0
+    for r in range(world):
+        if t.counts[r] > 0 and r != t.rank:
+            cand_ranks |= 1 << r
+    if not cand_ranks:
+        return rd, rg
+    mask = torch.zeros(mh, dtype=torch.int32, device=dev)
+    boxes = t.boxes.to(torch.float32).contiguous()
+    _lib.check(l.lbvh_rank_forward_mask(dv.ptr(hc), dv.ptr(bound), 0.0, mh, dv.ptr(boxes),
+                                        world, cand_ranks, dv.ptr(mask), dv.stream()))
+    sel = torch.nonzero(mask, as_tuple=True)[0]
+    shifts = torch.arange(world, dtype=torch.int32, device=dev)[None, :]
+    si, rr = torch.nonzero((mask[sel, None] >> shifts) & 1, as_tuple=True)
+    qi = sel[si]
+    frows = torch.empty((qi.numel(), 4), dtype=torch.float32, device=dev)
+    frows[:, :3] = hc[qi]
+    frows[:, 3] = qi.to(torch.int32).view(torch.float32)
+    fq, fcounts = _alltoallv(frows, rr, world, g)
+    f_gid, f_d2 = _local_knn(t, fq[:, :3].contiguous(), k)
+    back = torch.cat([fq[:, 3:4].contiguous().view(torch.int32), f_d2.view(torch.int32),
+                      f_gid.to(torch.int32)], dim=1)
+    bq, _ = _alltoallv(back, None, world, g, grouped_counts=fcounts)
+    brow = bq[:, 0].to(torch.int64)
+    nresp = torch.bincount(brow, minlength=mh) if brow.numel() else torch.zeros(
+        mh, dtype=torch.int64, device=dev)
+    if nloc < kk:
+        mrows = torch.arange(mh, device=dev)
+    else:
+        mrows = torch.nonzero(nresp > 0, as_tuple=True)[0]
+    if mrows.numel():
+        lidx, ld2 = t.engine.knn_sq_raw(t.tree, hc[mrows].contiguous(), k)
+        own = _merge_keys(lidx.to(torch.int64), ld2)
+        top, _ = _merge_remote(own, brow, bq, k, kk, nresp, mrows, mh)
+        gid, dd = t.engine.unpack_keys(top)
+        rd[mrows] = dd
+        rg[mrows] = gid.to(torch.int32)
     return rd, rg
 
 

@@ -616,6 +616,37 @@ def _host_arange_into(out: np.ndarray, step: int, parts: int = 8):
     return [_HOST_POOL.submit(fill, c0, min(n, c0 + per)) for c0 in range(0, n, per)]
 
 
+def knn_with_kth(tree: Bvh, centers: torch.Tensor, k: int):
+    """Device kNN (k <= 32) returning ``(ordinals i32 (m, kk), distances f32
+    (m, kk), kth_d2 f32 (m,))``: the final sqrt'ed lists plus each query's
+    exact squared k-th distance (the sharded search's forwarding bound), in
+    one kernel."""
+    b = _knn_batch((centers, k))
+    l = _lib.lib()
+    st = dv.stream()
+    nq, n = b.nq, tree.leaf_count
+    span = min(b.k, n)
+    out_idx = dv.empty(nq * span, torch.int32)
+    out_dist = dv.empty(nq * span, torch.float32)
+    kth = dv.empty(nq, torch.float32)
+    if nq == 0:
+        return out_idx.reshape(0, span), out_dist.reshape(0, span), kth
+    status = dv.Status()
+    _check_batch(b, status, radii=False)
+    offsets = dv.empty(nq + 1, torch.int64)
+    ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
+    _lib.check(l.lbvh_knn_offsets(None, b.k, n, nq, dv.ptr(offsets), None, status.ptr,
+                                  dv.ptr(ws), ws.numel(), st))
+    order, qcodes = _order(tree, b, True, with_codes=True)
+    kws = dv.workspace(l.lbvh_knn_workspace_bytes(nq))
+    _lib.check(_launch("knn", lambda: l.lbvh_knn_kth(
+        tree.ctree(), dv.ptr(b.centers), dv.ptr(order), dv.ptr(qcodes), nq, dv.ptr(offsets),
+        span, dv.ptr(out_idx), dv.ptr(out_dist), 0, dv.ptr(kws), kws.numel(), status.ptr,
+        dv.ptr(kth), st)))
+    _raise_flags(status.read())
+    return out_idx.reshape(nq, span), out_dist.reshape(nq, span), kth
+
+
 def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> ResultSet:
     """Host kNN batch as an H2D / compute / D2H pipeline over query chunks.
 
