@@ -323,21 +323,9 @@ int lbvh_remap_leaves(const lbvh_tree *tree, int32_t *leaf_obj, void *nodes, con
 int lbvh_knn_finalize(int64_t m, int kk, const int32_t *local_idx, const float *d2,
                       const int64_t *gids, const int64_t *merged_pos, const uint64_t *merged,
                       float *out_dist, int32_t *out_gid, void *stream);
-/* Home kNN results -> return rows of 1 + 2*kk i32: [qid, sqrt(d^2) bits x kk,
- * global ordinal x kk].  Row q takes merged[merged_pos[q]] (kk sorted
- * (d^2 bits << 32 | global ordinal) keys) when merged_pos[q] >= 0, else its
- * local list (local_idx -> gids, d2; gids NULL = local_idx are global
- * already).  merged_pos may be NULL. */
-int lbvh_knn_result_rows(int64_t m, int kk, const int32_t *qid, const int32_t *local_idx,
-                         const float *d2, const int64_t *gids, const int64_t *merged_pos,
-                         const uint64_t *merged, int32_t *rows, void *stream);
 /* m received rows (rd f32, rg i32; m x kk) -> out_d / out_g rows dst[i]. */
 int lbvh_scatter_result_rows(int64_t m, int kk, const int64_t *dst, const float *rd,
                              const int32_t *rg, float *out_d, int32_t *out_g, void *stream);
-/* Received return rows -> dist_out / gid_out (nq x kk) at row qid. */
-int lbvh_scatter_knn_rows(const int32_t *rows, int64_t m, int kk, float *dist_out,
-                          int64_t *gid_out, void *stream);
-
 #ifdef __cplusplus
 }
 #endif

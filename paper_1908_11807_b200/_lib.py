@@ -127,10 +127,6 @@ _SIGS = {
     "lbvh_morton_codes_f32": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_void_p], ctypes.c_int),
     "lbvh_remap_leaves": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 4, ctypes.c_int),
-    "lbvh_knn_result_rows": ([ctypes.c_int64, ctypes.c_int] + [ctypes.c_void_p] * 8,
-                             ctypes.c_int),
-    "lbvh_scatter_knn_rows": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
-                               ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_brute_knn": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
                        ctypes.c_int),

@@ -6,11 +6,11 @@
 //                             needed iff its box distance^2 <= the home's k-th
 //                             distance^2 (kNN) or r*r (radius); same fp32
 //                             recipe as the traversal (_kernels.py:146-176)
-//   knn_result_rows_kernel    home results -> return rows [query id, sqrt(d^2)
-//                             x kk, global ordinal x kk]; merged rows (queries
-//                             that had remote candidates) come as sorted
-//                             (d^2 bits << 32 | global ordinal) keys
-//   scatter_knn_rows_kernel   received rows -> (nq, kk) outputs in query order
+//   knn_finalize_kernel       home lists -> return arrays (sqrt(d^2), global
+//                             ordinal), merged rows from sorted (d^2 bits << 32
+//                             | global ordinal) keys (paths without lbvh_knn_kth)
+//   scatter_rows_kernel       received rows -> (nq, kk) outputs in query order
+//   remap_leaves_kernel       local tree leaves -> global ordinals
 
 #include "common.cuh"
 #include "internal.cuh"
@@ -38,74 +38,6 @@ rank_forward_mask_kernel(const float *__restrict__ centers, const float *__restr
             if (d <= b) bits |= 1u << r;
         }
         mask[q] = bits;
-    }
-}
-
-// Both row kernels give a warp 32 consecutive rows and let its lanes walk
-// the rows' words in order, so row writes (and the contiguous per-query
-// inputs) are coalesced.
-__global__ void __launch_bounds__(256)
-knn_result_rows_kernel(int64_t m, int kk, const int32_t *__restrict__ qid,
-                       const int32_t *__restrict__ local_idx, const float *__restrict__ d2,
-                       const int64_t *__restrict__ gids, const int64_t *__restrict__ merged_pos,
-                       const uint64_t *__restrict__ merged, int32_t *__restrict__ rows) {
-    const int64_t w = 1 + 2 * (int64_t)kk;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < m;
-         r0 += warps * 32) {
-        const int64_t nr = (m - r0) < 32 ? (m - r0) : 32;
-        // (row, column) of word e = lane, lane + 32, ... without divisions
-        int64_t q = r0 + lane / w, c = lane % w;
-        for (int64_t e = lane; e < nr * w; e += 32) {
-            int32_t v;
-            if (c == 0) {
-                v = __ldg(qid + q);
-            } else {
-                const int64_t j = (c - 1) % kk;
-                const int64_t mp = merged_pos ? __ldg(merged_pos + q) : -1;
-                if (mp >= 0) {
-                    const uint64_t key = __ldg(merged + mp * kk + j);
-                    v = (c <= kk) ? __float_as_int(__fsqrt_rn(__uint_as_float((uint32_t)(key >> 32))))
-                                  : (int32_t)(uint32_t)key;
-                } else if (c <= kk) {
-                    v = __float_as_int(__fsqrt_rn(__ldg(d2 + q * kk + j)));
-                } else {
-                    const int32_t li = __ldg(local_idx + q * kk + j);
-                    v = gids ? (int32_t)__ldg(gids + li) : li;
-                }
-            }
-            rows[r0 * w + e] = v;
-            c += 32;
-            while (c >= w) {
-                c -= w;
-                ++q;
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256)
-scatter_knn_rows_kernel(const int32_t *__restrict__ rows, int64_t m, int kk,
-                        float *__restrict__ dist_out, int64_t *__restrict__ gid_out) {
-    const int64_t w = 1 + 2 * (int64_t)kk;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < m;
-         r0 += warps * 32) {
-        const int64_t nr = (m - r0) < 32 ? (m - r0) : 32;
-        int64_t r = r0 + lane / kk, j = lane % kk;
-        for (int64_t e = lane; e < nr * kk; e += 32) {
-            const int32_t *row = rows + r * w;
-            const int64_t q = __ldg(row);
-            dist_out[q * kk + j] = __int_as_float(__ldg(row + 1 + j));
-            gid_out[q * kk + j] = (int64_t)(uint32_t)__ldg(row + 1 + kk + j);
-            j += 32;
-            while (j >= kk) {
-                j -= kk;
-                ++r;
-            }
-        }
     }
 }
 
@@ -232,30 +164,6 @@ int lbvh_remap_leaves(const lbvh_tree *tree, int32_t *leaf_obj, void *nodes, con
         return LBVH_ERR_INVALID_ARG;
     remap_leaves_kernel<<<grid_of(tree->n), 256, 0, (cudaStream_t)stream>>>(
         tree->n, leaf_obj, (PackedNode *)nodes, map);
-    count_launches(1);
-    return check_launch();
-}
-
-int lbvh_knn_result_rows(int64_t m, int kk, const int32_t *qid, const int32_t *local_idx,
-                         const float *d2, const int64_t *gids, const int64_t *merged_pos,
-                         const uint64_t *merged, int32_t *rows, void *stream) {
-    if (m < 0 || kk < 1 || (m > 0 && (!qid || !local_idx || !d2 || !rows)) ||
-        (merged_pos && !merged))
-        return LBVH_ERR_INVALID_ARG;
-    if (m == 0) return LBVH_OK;
-    knn_result_rows_kernel<<<grid_of(m), 256, 0, (cudaStream_t)stream>>>(
-        m, kk, qid, local_idx, d2, gids, merged_pos, merged, rows);
-    count_launches(1);
-    return check_launch();
-}
-
-int lbvh_scatter_knn_rows(const int32_t *rows, int64_t m, int kk, float *dist_out,
-                          int64_t *gid_out, void *stream) {
-    if (m < 0 || kk < 1 || (m > 0 && (!rows || !dist_out || !gid_out)))
-        return LBVH_ERR_INVALID_ARG;
-    if (m == 0) return LBVH_OK;
-    scatter_knn_rows_kernel<<<grid_of(m), 256, 0, (cudaStream_t)stream>>>(rows, m, kk,
-                                                                          dist_out, gid_out);
     count_launches(1);
     return check_launch();
 }
