@@ -162,3 +162,16 @@ def test_query_value_types():
         lb.SpatialQuery(Point(0, 0, 0), -1.0)
     with pytest.raises(ValueError):
         lb.KnnQuery(Point(0, 0, 0), 0)
+
+
+def test_reference_module_names():
+    """``lbvh.oracle`` / ``lbvh.parallel`` exist under the same names."""
+    import paper_1908_11807_b200 as lb
+    from paper_1908_11807_b200.oracle import brute_knn_batch, brute_radius_sets  # noqa: F401
+    from paper_1908_11807_b200.parallel import run_chunked
+
+    assert lb.oracle.brute_knn is lb.brute_knn
+    seen = []
+    run_chunked(lambda a, b: seen.append((a, b)), 10, 8)
+    run_chunked(lambda a, b: seen.append((a, b)), 0, 8)
+    assert seen == [(0, 10)]
