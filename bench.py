@@ -186,6 +186,17 @@ class KernelTimer:
         self.events.setdefault(name, []).append((s, e))
         return rc
 
+    def pair(self, name):
+        """Events for a kernel the library brackets itself (fused calls)."""
+        if not self.enabled:
+            return None
+        t = self.torch
+        s, e = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        s.record()  # materialise the handles; the library re-records them
+        e.record()
+        self.events.setdefault(name, []).append((s, e))
+        return s, e
+
     def mean_ms(self, name):
         ev = self.events.get(name, [])
         if not ev:

@@ -223,6 +223,52 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
                flags, workspace, workspace_bytes, status, S(stream), nullptr);
 }
 
+/* One device kNN batch with a uniform k in a single call: value checks,
+ * CRS offsets, Morton query order on the tree's grid and the search (the
+ * drop-in query_knn for device-resident centers without per-call host
+ * round trips between the launches). */
+size_t lbvh_knn_batch_workspace_bytes(int64_t nq) {
+    const size_t n = (size_t)(nq > 0 ? nq : 1);
+    size_t a = align_up(4 * n) * 2;  // order + sorted query codes
+    size_t q = query_workspace_bytes(nq), sc = scan_workspace_bytes(nq),
+           kw = knn_workspace_bytes(nq);
+    size_t m = q > sc ? q : sc;
+    m = m > kw ? m : kw;
+    return a + m + 1024;
+}
+
+int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int64_t k,
+                   int order_bits, int64_t *offsets, int32_t *out_idx, float *out_dist,
+                   int flags, void *ws, size_t ws_bytes, uint32_t *status, void *ev_before,
+                   void *ev_after, void *stream) {
+    if (!tree || nq < 0 || k < 1 || !status) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0) return LBVH_OK;
+    if (!centers || !offsets || !out_idx || !out_dist || !ws) return LBVH_ERR_INVALID_ARG;
+    if (ws_bytes < lbvh_knn_batch_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
+    cudaStream_t st = S(stream);
+    Carve c(ws, ws_bytes);
+    uint32_t *order = c.take<uint32_t>(nq);
+    uint32_t *codes = c.take<uint32_t>(nq);
+    void *rest = c.take<char>(1);
+    const size_t rest_bytes = ws_bytes - ((char *)rest - (char *)ws);
+    int rc = check_queries(centers, nq, nullptr, status, st);
+    if (rc) return rc;
+    rc = knn_offsets(nullptr, k, tree->n, nq, offsets, nullptr, status, rest, rest_bytes, st);
+    if (rc) return rc;
+    const bool sorted = order_bits > 0 && nq > 1;
+    if (sorted) {
+        rc = query_order(centers, nq, tree->root_box, order_bits, order, codes, rest,
+                         rest_bytes, st);
+        if (rc) return rc;
+    }
+    const int64_t span = k < tree->n ? k : tree->n;
+    if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
+    rc = knn(tree, centers, sorted ? order : nullptr, sorted ? codes : nullptr, nq, offsets,
+             span, out_idx, out_dist, flags, rest, rest_bytes, status, st, nullptr);
+    if (ev_after) cudaEventRecord((cudaEvent_t)ev_after, st);
+    return rc;
+}
+
 int lbvh_knn_kth(const lbvh_tree *tree, const float *centers, const uint32_t *order,
                  const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
                  int64_t max_span, int32_t *out_idx, float *out_dist, int flags,

@@ -59,6 +59,16 @@ def _launch(name: str, call) -> int:
     return call() if t is None else t.wrap(name, call)
 
 
+def _kernel_events(name: str):
+    """(before, after) raw cudaEvent_t handles for a kernel timed inside a
+    fused C call, or (None, None) when no timer is installed."""
+    t = KERNEL_TIMER
+    pair = t.pair(name) if t is not None and hasattr(t, "pair") else None
+    if pair is None:
+        return None, None
+    return pair[0].cuda_event, pair[1].cuda_event
+
+
 @dataclass(frozen=True)
 class SpatialQuery:
     """All objects within ``radius`` of ``center``, inclusive (traversal.py:46-55)."""
@@ -565,8 +575,21 @@ def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultS
     st = dv.stream()
     nq, n = b.nq, tree.leaf_count
     status = dv.Status()
-    _check_batch(b, status, radii=False)
     offsets = dv.empty(nq + 1, torch.int64)
+    if b.ks is None:
+        # uniform k: checks, offsets, query order and search in one C call
+        span = min(b.k, n)
+        out_idx = dv.empty(span * nq, torch.int32)
+        out_dist = dv.empty(span * nq, torch.float32)
+        ws = dv.workspace(l.lbvh_knn_batch_workspace_bytes(nq))
+        evs = _kernel_events("knn")
+        _lib.check(l.lbvh_knn_batch(
+            tree.ctree(), dv.ptr(b.centers), nq, b.k, _ORDER_BITS if sort_queries else 0,
+            dv.ptr(offsets), dv.ptr(out_idx), dv.ptr(out_dist), flags, dv.ptr(ws), ws.numel(),
+            status.ptr, evs[0], evs[1], st))
+        offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
+        return ResultSet._trusted(offsets, out_idx, out_dist)
+    _check_batch(b, status, radii=False)
     ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
     if b.ks is None:
         # uniform k: spans, total and the kernel variant are known on the host

@@ -16,6 +16,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:knn_kernel -s 1 -c 1 \
     -o $OUT/${TAG}_knn python bench.py --profile --steps 2 --warmup 1 > $OUT/${TAG}_ncu_knn.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on \
-    -k regex:"spatial_kernel|hierarchy_kernel|onesweep_kernel|internal_rows" -s 4 -c 8 \
+    -k regex:"spatial_kernel|hierarchy_|onesweep_kernel|internal_rows" -s 4 -c 9 \
     -o $OUT/${TAG}_other python tools/prof_radius.py > $OUT/${TAG}_ncu_other.log 2>&1
 echo done
