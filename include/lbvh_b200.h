@@ -260,6 +260,20 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              int64_t max_span, int32_t *out_idx, float *out_dist, int flags,
              void *workspace, size_t workspace_bytes, uint32_t *status, void *stream);
 
+/* query_spatial_2p's count stage for device-resident centers in one call:
+ * value checks, Morton query order (order_bits; 0 = unsorted, `order` then
+ * unused), the count pass keeping the first `rows` hits of every query in
+ * buf (rows 0: no row buffer), the exclusive scan into offsets (nq+1) and
+ * the list of queries whose hits overflowed their row (over_list, over_n).
+ * ev_before / ev_after (optional) bracket the count kernel. */
+size_t lbvh_spatial_count_batch_workspace_bytes(int64_t nq);
+int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const float *radii,
+                             float radius, int64_t nq, int order_bits, int64_t rows,
+                             uint32_t *order, int32_t *counts, int32_t *buf, int64_t *offsets,
+                             uint32_t *over_list, uint32_t *over_n, void *workspace,
+                             size_t workspace_bytes, uint32_t *status, void *ev_before,
+                             void *ev_after, void *stream);
+
 /* query_knn for device-resident centers and a uniform k in one call: value
  * checks (LBVH_FLAG_NONFINITE), uniform CRS offsets (nq+1), Morton query
  * order on the tree's grid (order_bits of the 30-bit code; 0 = unsorted) and

@@ -108,6 +108,11 @@ _SIGS = {
                   ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                   ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn_batch_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_spatial_count_batch_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_spatial_count_batch": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_float, ctypes.c_int64, ctypes.c_int, ctypes.c_int64]
+                                 + [ctypes.c_void_p] * 7 + [ctypes.c_size_t]
+                                 + [ctypes.c_void_p] * 4, ctypes.c_int),
     "lbvh_knn_batch": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                         ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,

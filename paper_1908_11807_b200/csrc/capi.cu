@@ -269,6 +269,43 @@ int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int6
     return rc;
 }
 
+size_t lbvh_spatial_count_batch_workspace_bytes(int64_t nq) {
+    size_t q = query_workspace_bytes(nq), sc = scan_workspace_bytes(nq);
+    return (q > sc ? q : sc) + 1024;
+}
+
+int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const float *radii,
+                             float radius, int64_t nq, int order_bits, int64_t rows,
+                             uint32_t *order, int32_t *counts, int32_t *buf, int64_t *offsets,
+                             uint32_t *over_list, uint32_t *over_n, void *ws, size_t ws_bytes,
+                             uint32_t *status, void *ev_before, void *ev_after, void *stream) {
+    if (!tree || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
+    if (nq == 0) return LBVH_OK;
+    if (!centers || !counts || !offsets || !order || !ws ||
+        (rows > 0 && (!buf || !over_list || !over_n)))
+        return LBVH_ERR_INVALID_ARG;
+    if (ws_bytes < lbvh_spatial_count_batch_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
+    cudaStream_t st = S(stream);
+    int rc = check_queries(centers, nq, radii, status, st);
+    if (rc) return rc;
+    const bool sorted = order_bits > 0 && nq > 1;
+    if (sorted) {
+        rc = query_order(centers, nq, tree->root_box, order_bits, order, nullptr, ws, ws_bytes,
+                         st);
+        if (rc) return rc;
+    }
+    const uint32_t *ord = sorted ? order : nullptr;
+    if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
+    rc = spatial_count(tree, centers, radii, radius, ord, nq, counts, rows > 0 ? buf : nullptr,
+                       rows, status, st);
+    if (ev_after) cudaEventRecord((cudaEvent_t)ev_after, st);
+    if (rc) return rc;
+    rc = scan_counts(counts, nq, offsets, ws, ws_bytes, st);
+    if (rc) return rc;
+    if (rows > 0) return select_overflow(ord, counts, nq, rows, over_list, over_n, st);
+    return LBVH_OK;
+}
+
 int lbvh_knn_kth(const lbvh_tree *tree, const float *centers, const uint32_t *order,
                  const uint32_t *query_codes, int64_t nq, const int64_t *offsets,
                  int64_t max_span, int32_t *out_idx, float *out_dist, int flags,

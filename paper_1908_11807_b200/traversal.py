@@ -335,6 +335,47 @@ _ROW_HITS = int(os.environ.get("LBVH_ROW_HITS", "24"))
 _ROW_BUDGET = 4 << 30
 
 
+def _spatial_2p_fused(tree: Bvh, b: _Batch, sort_queries: bool, status: dv.Status):
+    """query_spatial_2p on a staged batch: the count stage (checks, order,
+    count with row buffer, scan, overflow list) in one C call, one sync for
+    the total, then compaction and the overflow fill."""
+    l = _lib.lib()
+    ct = tree.ctree()
+    st = dv.stream()
+    nq = b.nq
+    rows = next((r for r in (_ROW_HITS, _ROW_HITS // 2) if r and nq * r * 4 <= _ROW_BUDGET), 0)
+    counts = dv.empty(nq, torch.int32)
+    buf = dv.empty((nq, rows), torch.int32) if rows else None
+    offsets = dv.empty(nq + 1, torch.int64)
+    order = dv.empty(nq, torch.int32)
+    over_list = dv.empty(nq, torch.int32) if rows else None
+    over_n = dv.empty(1, torch.int32)
+    ws = dv.workspace(l.lbvh_spatial_count_batch_workspace_bytes(nq))
+    evs = _kernel_events("spatial_count")
+    _lib.check(l.lbvh_spatial_count_batch(
+        ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, nq, _ORDER_BITS if sort_queries else 0,
+        rows, dv.ptr(order), dv.ptr(counts), dv.ptr(buf), dv.ptr(offsets), dv.ptr(over_list),
+        dv.ptr(over_n), dv.ptr(ws), ws.numel(), status.ptr, evs[0], evs[1], st))
+    flags, total, n_over = dv.d2h_many(status.dev, offsets[nq:], over_n)
+    _raise_flags(int(flags[0]) & 0xFFFFFFFF)
+    total, n_over = int(total[0]), int(n_over[0])
+    out = dv.empty(total, torch.int32)
+    if total:
+        if rows:
+            _lib.check(l.lbvh_compact(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), nq,
+                                      dv.ptr(out), st))
+            if n_over:
+                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
+                    ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(over_list), n_over,
+                    dv.ptr(offsets), dv.ptr(out), None, 0, status.ptr, st)))
+        else:
+            _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
+                ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
+                dv.ptr(order) if sort_queries and nq > 1 else None, nq, dv.ptr(offsets),
+                dv.ptr(out), None, 0, status.ptr, st)))
+    return offsets, out
+
+
 def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
     l = _lib.lib()
     ct = tree.ctree()
@@ -393,9 +434,7 @@ def query_spatial_2p(tree: Bvh, queries, sort_queries: bool = True,
     if b.host_centers is not None:
         return _spatial_2p_pipelined(tree, b, sort_queries)
     status = dv.Status()
-    _check_batch(b, status, radii=True)
-    order = _order(tree, b, sort_queries)
-    offsets, out = _spatial_2p_device(tree, b, order, status)
+    offsets, out = _spatial_2p_fused(tree, b, sort_queries, status)
     offsets, out = _finish(b.host, status, offsets, out)
     return ResultSet._trusted(offsets, out)
 
