@@ -56,13 +56,32 @@ enum SpatialMode {
     kCountBuf = 3,  // count all, keep the first `cap` hits in the row
 };
 
+#ifndef LBVH_LDG256
+#define LBVH_LDG256 1
+#endif
+
+// 32 bytes in one read-only 256-bit load (sm_100: LDG.E.ENL2.256).
+__device__ __forceinline__ void ldg256(const void *p, float4 &x, float4 &y) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+        : "l"(p));
+}
+
 __device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, int32_t id,
                                           float4 &a, float4 &b, float4 &c, int4 &d) {
     const PackedNode *p = nodes + id;
-    a = __ldg(&p->a);
-    b = __ldg(&p->b);
-    c = __ldg(&p->c);
-    d = __ldg(&p->d);
+    if (LBVH_LDG256) {  // the 64-byte record in two 256-bit loads
+        float4 dd;
+        ldg256(&p->a, a, b);
+        ldg256(&p->c, c, dd);
+        d = make_int4(__float_as_int(dd.x), __float_as_int(dd.y), __float_as_int(dd.z),
+                      __float_as_int(dd.w));
+    } else {
+        a = __ldg(&p->a);
+        b = __ldg(&p->b);
+        c = __ldg(&p->c);
+        d = __ldg(&p->d);
+    }
 }
 
 // One hit (leaf ordinal `obj`); returns false when the 1P row overflows.
