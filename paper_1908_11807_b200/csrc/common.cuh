@@ -110,6 +110,14 @@ __device__ __forceinline__ uint64_t morton63(double x, double y, double z, const
            spread21(grid21(z, lo[2], ext[2]));
 }
 
+// 32 bytes in one read-only 256-bit load (sm_100: LDG.E.ENL2.256); p must
+// be 32-byte aligned.
+__device__ __forceinline__ void ldg256(const void *p, float4 &x, float4 &y) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+        : "l"(p));
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // GPU-scope release+acquire read-modify-writes (no full membar).

@@ -60,13 +60,6 @@ enum SpatialMode {
 #define LBVH_LDG256 1
 #endif
 
-// 32 bytes in one read-only 256-bit load (sm_100: LDG.E.ENL2.256).
-__device__ __forceinline__ void ldg256(const void *p, float4 &x, float4 &y) {
-    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
-        : "l"(p));
-}
-
 __device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, int32_t id,
                                           float4 &a, float4 &b, float4 &c, int4 &d) {
     const PackedNode *p = nodes + id;
@@ -218,7 +211,19 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
         if (cnt > cap) continue;  // did not fit its row: written by the overflow fill pass
         const int64_t dst = __ldg(offsets + q);
         const int32_t *row = buf + q * cap;
-        if ((cap & 3) == 0) {
+        if ((cap & 7) == 0) {  // 32-byte aligned rows: 256-bit loads
+            for (int32_t j = 0; j < cnt; j += 8) {
+                float4 x, y;
+                ldg256(row + j, x, y);
+                const int32_t v[8] = {__float_as_int(x.x), __float_as_int(x.y),
+                                      __float_as_int(x.z), __float_as_int(x.w),
+                                      __float_as_int(y.x), __float_as_int(y.y),
+                                      __float_as_int(y.z), __float_as_int(y.w)};
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j + u < cnt) out[dst + j + u] = v[u];
+            }
+        } else if ((cap & 3) == 0) {
             for (int32_t j = 0; j < cnt; j += 4) {
                 const int4 v = __ldcs(reinterpret_cast<const int4 *>(row + j));
                 out[dst + j] = v.x;

@@ -148,9 +148,13 @@ knn_wide_kernel(const lbvh_tree t, const float *__restrict__ centers,
     int32_t node = 0;
     while (true) {
         const WideNode *w = wide + node;
-        const float4 lx = __ldg(&w->lox), ly = __ldg(&w->loy), lz = __ldg(&w->loz);
-        const float4 hx = __ldg(&w->hix), hy = __ldg(&w->hiy), hz = __ldg(&w->hiz);
-        const int4 lk = __ldg(&w->link);
+        float4 lx, ly, lz, hx, hy, hz, lkf, pad;
+        ldg256(&w->lox, lx, ly);
+        ldg256(&w->loz, lz, hx);
+        ldg256(&w->hiy, hy, hz);
+        ldg256(&w->link, lkf, pad);
+        const int4 lk = make_int4(__float_as_int(lkf.x), __float_as_int(lkf.y),
+                                  __float_as_int(lkf.z), __float_as_int(lkf.w));
         float d0 = box_dist_sq(px, py, pz, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x);
         float d1 = box_dist_sq(px, py, pz, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y);
         float d2 = box_dist_sq(px, py, pz, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z);
