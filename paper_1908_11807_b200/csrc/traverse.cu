@@ -326,6 +326,19 @@ __device__ __forceinline__ int32_t subtree_entry(const lbvh_tree &t, float px, f
 #ifndef LBVH_KNN_BLOCK
 #define LBVH_KNN_BLOCK 256
 #endif
+#ifndef LBVH_KNN16_MINBLOCKS
+#define LBVH_KNN16_MINBLOCKS 3  // k=16: 14.3 ms vs 14.6 (4) and 15.7 (5, spills)
+#endif
+#ifndef LBVH_KNN32_MINBLOCKS
+#define LBVH_KNN32_MINBLOCKS 2
+#endif
+// Resident CTAs per SM by list size: the k-best keys take 2K registers, so
+// larger lists get fewer CTAs instead of spilling.
+__host__ __device__ constexpr int knn_min_blocks(int K) {
+    return (K <= 10 ? LBVH_KNN_MINBLOCKS : K <= 16 ? LBVH_KNN16_MINBLOCKS : LBVH_KNN32_MINBLOCKS) *
+           256 / LBVH_KNN_BLOCK;
+}
+
 // One query slot s of a kNN batch (s < nq).
 template <int K, bool REGNEXT>
 __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__restrict__ centers,
@@ -524,7 +537,7 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
 
 template <int K, bool REGNEXT>
 __global__ void __launch_bounds__(LBVH_KNN_BLOCK,
-                                  (K <= 16 ? LBVH_KNN_MINBLOCKS * 256 / LBVH_KNN_BLOCK : 1))
+                                  knn_min_blocks(K))
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
            const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
@@ -541,7 +554,7 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
 // exactly knn_kernel's).
 template <int K>
 __global__ void __launch_bounds__(LBVH_KNN_BLOCK,
-                                  (K <= 16 ? LBVH_KNN_MINBLOCKS * 256 / LBVH_KNN_BLOCK : 1))
+                                  knn_min_blocks(K))
 knn_warpq_kernel(const lbvh_tree t, const float *__restrict__ centers,
                  const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
                  int64_t nq, const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
@@ -579,7 +592,7 @@ knn_warpq_kernel(const lbvh_tree t, const float *__restrict__ centers,
 // such trees (stack exhaustion elsewhere keeps the reference's behaviour).
 // ---------------------------------------------------------------------------
 template <int K>
-__global__ void __launch_bounds__(LBVH_KNN_BLOCK, (K <= 16 ? LBVH_KNN_MINBLOCKS * 256 / LBVH_KNN_BLOCK : 1))
+__global__ void __launch_bounds__(LBVH_KNN_BLOCK, knn_min_blocks(K))
 knn_packet_kernel(const lbvh_tree t, const float *__restrict__ centers,
                   const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
                   int64_t nq, const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
@@ -963,6 +976,137 @@ done:
         for (int64_t j = 0; j < size; ++j) hd[j] = __fsqrt_rn(hd[j]);
 }
 
+// k > 32: the reference's bounded max-heap (_kernels.py:299-325, 385-414),
+// kept in shared memory (64-bit keys (dist^2 bits << 32 | ordinal), the
+// lexicographic "worse" order in one compare; lane-interleaved slots) instead
+// of the output span in global memory.  Traversal and stack discipline are
+// knn_pass's (push farther then nearer, pop with the prune test), so results
+// and stack exhaustion are the reference's.
+constexpr int kHeapThreads = 64;
+
+__device__ __forceinline__ uint64_t &hslot(uint64_t *h, int i) {
+    return h[(int64_t)i * kHeapThreads];
+}
+
+__global__ void __launch_bounds__(kHeapThreads)
+knn_smem_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                     const uint32_t *__restrict__ order, int64_t nq,
+                     const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
+                     float *__restrict__ out_dist, bool squared, uint32_t *status) {
+    extern __shared__ uint64_t s_heap[];
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    const int64_t base = __ldg(offsets + q);
+    const int kk = (int)(__ldg(offsets + q + 1) - base);
+    if (kk <= 0) return;
+    const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
+                pz = __ldg(centers + 3 * q + 2);
+    if (t.n == 1) {
+        const float d2 = box_dist_sq(px, py, pz, bx_of(t, 0), bx_of(t, 1), bx_of(t, 2),
+                                     bx_of(t, 3), bx_of(t, 4), bx_of(t, 5));
+        out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
+        out_idx[base] = __ldg(t.leaf_obj);
+        return;
+    }
+    uint64_t *h = s_heap + threadIdx.x;
+    int size = 0;
+    auto worst = [&]() { return __uint_as_float((uint32_t)(hslot(h, 0) >> 32)); };
+    auto offer = [&](float d, int32_t obj) {
+        const uint64_t c = ((uint64_t)__float_as_uint(d) << 32) | (uint32_t)obj;
+        if (size < kk) {  // sift up
+            int pos = size++;
+            while (pos > 0) {
+                const int up = (pos - 1) >> 1;
+                const uint64_t u = hslot(h, up);
+                if (!(c > u)) break;
+                hslot(h, pos) = u;
+                pos = up;
+            }
+            hslot(h, pos) = c;
+        } else if (c < hslot(h, 0)) {  // replace the worst, sift down
+            int pos = 0;
+            while (true) {
+                int child = 2 * pos + 1;
+                if (child >= kk) break;
+                uint64_t cv = hslot(h, child);
+                if (child + 1 < kk) {
+                    const uint64_t sv = hslot(h, child + 1);
+                    if (sv > cv) {
+                        cv = sv;
+                        ++child;
+                    }
+                }
+                if (!(cv > c)) break;
+                hslot(h, pos) = cv;
+                pos = child;
+            }
+            hslot(h, pos) = c;
+        }
+    };
+    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+    uint64_t stack[kStack];
+    int sp = 1;
+    stack[0] = 0;  // (dist^2 = 0, root)
+    uint32_t fail = 0;
+    while (sp > 0) {
+        const uint64_t e = stack[--sp];
+        if (size == kk && __uint_as_float((uint32_t)(e >> 32)) > worst()) continue;
+        float4 a, b, c;
+        int4 dd;
+        load_node(nodes, (int32_t)(uint32_t)e, a, b, c, dd);
+        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
+        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        const bool left_near = dl <= dr;
+        const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
+        const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
+#pragma unroll
+        for (int pick = 0; pick < 2; ++pick) {
+            const int32_t link = pick == 0 ? fl : nl;
+            const float cd = pick == 0 ? fd : ndist;
+            if (size == kk && cd > worst()) continue;
+            if (link < 0) {
+                offer(cd, link & 0x7FFFFFFF);
+            } else {
+                if (sp >= kStack) {
+                    fail = LBVH_FLAG_STACK_EXHAUSTED;
+                    goto done;
+                }
+                stack[sp++] = ((uint64_t)__float_as_uint(cd) << 32) | (uint32_t)link;
+            }
+        }
+    }
+done:
+    if (fail) atomicOr(status, fail);
+    // heap sort: ascending (dist^2, ordinal) into the span
+    for (int hs = size; hs > 0; --hs) {
+        const uint64_t top = hslot(h, 0);
+        const int64_t o = base + hs - 1;
+        out_idx[o] = (int32_t)(uint32_t)top;
+        const float d2 = __uint_as_float((uint32_t)(top >> 32));
+        out_dist[o] = squared ? d2 : __fsqrt_rn(d2);
+        const uint64_t c = hslot(h, hs - 1);
+        int pos = 0;
+        const int n = hs - 1;
+        while (true) {
+            int child = 2 * pos + 1;
+            if (child >= n) break;
+            uint64_t cv = hslot(h, child);
+            if (child + 1 < n) {
+                const uint64_t sv = hslot(h, child + 1);
+                if (sv > cv) {
+                    cv = sv;
+                    ++child;
+                }
+            }
+            if (!(cv > c)) break;
+            hslot(h, pos) = cv;
+            pos = child;
+        }
+        if (n > 0) hslot(h, pos) = c;
+    }
+}
+
 __global__ void __launch_bounds__(256)
 check_queries_kernel(const float *__restrict__ centers, int64_t nq,
                      const float *__restrict__ radii, uint32_t *status) {
@@ -1199,6 +1343,21 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     LBVH_KNN_CASE(16)
     LBVH_KNN_CASE(32)
 #undef LBVH_KNN_CASE
+    // shared-memory heap up to 400 slots per query (64 threads x 8 B x k <= 200 KB)
+    const size_t smem = (size_t)kHeapThreads * 8 * (size_t)max_span;
+    static const int smem_heap = env_int("LBVH_KNN_SMEM_HEAP", 1);
+    if (smem_heap && max_span <= 400) {
+        static size_t opted = 0;
+        if (smem > opted) {
+            cudaFuncSetAttribute(knn_smem_heap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kHeapThreads * 8 * 400));
+            opted = (size_t)kHeapThreads * 8 * 400;
+        }
+        knn_smem_heap_kernel<<<div_up(nq, kHeapThreads), kHeapThreads, smem, stream>>>(
+            *t, centers, order, nq, offsets, out_idx, out_dist, squared, status);
+        count_launches(1);
+        return check_launch();
+    }
     knn_heap_kernel<<<div_up(nq, 128), 128, 0, stream>>>(*t, centers, order, nq, offsets,
                                                          out_idx, out_dist, squared, status);
     count_launches(1);

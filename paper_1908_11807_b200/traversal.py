@@ -331,8 +331,8 @@ def _finish(host: bool, status: dv.Status, *arrays):
 # the count pass (in traversal order, so bytes are the reference's fill
 # order); the fill pass then revisits only queries with more hits.  The row
 # buffer is skipped when it would exceed _ROW_BUDGET bytes.
-_ROW_HITS = int(os.environ.get("LBVH_ROW_HITS", "24"))
-_ROW_BUDGET = 4 << 30
+_ROW_HITS = int(os.environ.get("LBVH_ROW_HITS", "48"))
+_ROW_BUDGET = 8 << 30
 
 
 def _spatial_2p_fused(tree: Bvh, b: _Batch, sort_queries: bool, status: dv.Status):
