@@ -1340,8 +1340,13 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     LBVH_KNN_CASE(4)
     LBVH_KNN_CASE(8)
     LBVH_KNN_CASE(10)
-    LBVH_KNN_CASE(16)
-    LBVH_KNN_CASE(32)
+    // smallest k on the shared-memory heap path: k = 24 / 32 run at 23.9 / 31.7 ms there vs
+    // 33.9 / 42.2 ms with 32-slot register lists (C2); k = 16 stays in registers (14.3 vs 18.6)
+    static const int heap_min = env_int("LBVH_KNN_HEAP_MIN", 17);
+    if (max_span < heap_min || kth) {
+        LBVH_KNN_CASE(16)
+        LBVH_KNN_CASE(32)
+    }
 #undef LBVH_KNN_CASE
     // shared-memory heap up to 400 slots per query (64 threads x 8 B x k <= 200 KB)
     const size_t smem = (size_t)kHeapThreads * 8 * (size_t)max_span;

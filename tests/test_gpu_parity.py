@@ -228,6 +228,21 @@ def test_device_generators_match_host(shape, variant, count, seed):
     assert dev.is_cuda and dev.cpu().numpy().tobytes() == host.tobytes()
 
 
+@pytest.mark.parametrize("k", [11, 16, 17, 24, 32, 33, 64, 400, 401])
+def test_knn_list_sizes_against_oracle(k):
+    """Every kNN kernel size class (register lists, shared-memory heap up to
+    k = 400, global-memory heap beyond) returns the reference's spans."""
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 20_000, 0))
+    pts[100:110] = pts[5]  # exact distance ties across ordinals
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 3_000, 1))
+    q[0] = pts[5]
+    ko, ki, kd = oracle.query_knn(oracle.build(pts), q, k)
+    rk = lb.query_knn(lb.build(pts), (q, k))
+    assert np.array_equal(rk.offsets, ko)
+    assert np.array_equal(rk.indices, ki)
+    assert rk.distances.tobytes() == kd.tobytes()
+
+
 def test_large_scale_properties_1e7():
     """Full C2 size: size-independent properties (sortedness of leaf codes,
     containment, root box == scene box), plus oracle parity on a query sample."""
