@@ -251,6 +251,10 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
  * squared distances (no sqrt) -- used by the distributed merge, which must
  * order candidates by exact (d^2, ordinal). */
 #define LBVH_KNN_SQUARED 0x1
+/* offsets[q] == q * max_span for every query (uniform k): the kernel computes
+ * span starts instead of reading them (the offsets array is still read by
+ * the other paths and must hold the same values). */
+#define LBVH_KNN_UNIFORM_SPANS 0x2
 /* workspace (optional, lbvh_knn_workspace_bytes(nq)): enables the persistent
  * kernel with per-lane query refill and a separate seed pass; without it
  * the one-thread-per-query kernel runs.  Results are identical. */

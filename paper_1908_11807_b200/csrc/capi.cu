@@ -264,7 +264,8 @@ int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int6
     const int64_t span = k < tree->n ? k : tree->n;
     if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
     rc = knn(tree, centers, sorted ? order : nullptr, sorted ? codes : nullptr, nq, offsets,
-             span, out_idx, out_dist, flags, rest, rest_bytes, status, st, nullptr);
+             span, out_idx, out_dist, flags | LBVH_KNN_UNIFORM_SPANS, rest, rest_bytes, status,
+             st, nullptr);
     if (ev_after) cudaEventRecord((cudaEvent_t)ev_after, st);
     return rc;
 }

@@ -347,10 +347,12 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
                                           const int64_t *__restrict__ offsets,
                                           int32_t *__restrict__ out_idx,
                                           float *__restrict__ out_dist, bool squared,
-                                          uint32_t *status, float *__restrict__ kth = nullptr) {
+                                          uint32_t *status, float *__restrict__ kth = nullptr,
+                                          int uniform = 0) {
     const int64_t q = order ? (int64_t)__ldg(order + s) : s;
-    const int64_t base = __ldg(offsets + q);
-    const int kk = (int)(__ldg(offsets + q + 1) - base);
+    // uniform spans (LBVH_KNN_UNIFORM_SPANS): offsets[q] = q * span, computed
+    const int64_t base = uniform ? q * uniform : __ldg(offsets + q);
+    const int kk = uniform ? uniform : (int)(__ldg(offsets + q + 1) - base);
     if (kk <= 0) return;
     const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
                 pz = __ldg(centers + 3 * q + 2);
@@ -541,11 +543,12 @@ __global__ void __launch_bounds__(LBVH_KNN_BLOCK,
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes, int64_t nq,
            const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-           float *__restrict__ out_dist, bool squared, uint32_t *status, float *kth) {
+           float *__restrict__ out_dist, bool squared, uint32_t *status, float *kth,
+           int uniform) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
     knn_query<K, REGNEXT>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
-                          status, kth);
+                          status, kth, uniform);
 }
 
 // Persistent warps: each warp takes the next 32 Morton-consecutive query
@@ -1321,15 +1324,16 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         else if (variant == 1)                                                              \
             knn_kernel<KV, true><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,     \
                                                         offsets, out_idx, out_dist, squared, \
-                                                        status, kth);                       \
+                                                        status, kth, uniform);              \
         else                                                                                \
             knn_kernel<KV, false><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,    \
                                                          offsets, out_idx, out_dist,        \
-                                                         squared, status, kth);             \
+                                                         squared, status, kth, uniform);    \
         count_launches(1);                                                                  \
         return check_launch();                                                              \
     }
     const bool squared = (flags & LBVH_KNN_SQUARED) != 0;
+    const int uniform = (flags & LBVH_KNN_UNIFORM_SPANS) ? (int)max_span : 0;
     static const int wide = env_int("LBVH_KNN_WIDE", 1);
     if (wide && !kth && t->nodes4 && (t->flags & LBVH_TREE_CODES30) && !use_persistent &&
         !packet) {
