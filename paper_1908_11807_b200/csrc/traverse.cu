@@ -237,86 +237,11 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
     }
 }
 
-// lower_bound(target) over the sorted 30-bit leaf codes through the leaf
-// directory (target <= 2^30).
-__device__ __forceinline__ int64_t dir_lower_bound(const lbvh_tree &t, uint64_t target) {
-    if (target >= (1ull << 30)) return t.n;
-    const int sh = 30 - t.leaf_dir_bits;
-    const uint64_t p = target >> sh;
-    int64_t lo = __ldg(t.leaf_dir + p);
-    if ((target & ((1ull << sh) - 1)) == 0) return lo;
-    int64_t hi = __ldg(t.leaf_dir + p + 1);
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if ((uint64_t)__ldg(t.leaf_codes + mid) < target)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-// Common-prefix length of augmented keys x, x+1 (_kernels.py:23-58).
-__device__ __forceinline__ int aug_delta(const uint32_t *codes, int64_t x) {
-    const uint64_t a = ((uint64_t)__ldg(codes + x) << 32) | (uint64_t)x;
-    const uint64_t b = ((uint64_t)__ldg(codes + x + 1) << 32) | (uint64_t)(x + 1);
-    return __clzll(a ^ b);
-}
-
-// Subtree entry for a kNN query with search-radius bound rho2 (exact upper
-// bound of its k-th squared distance).  On a 30-bit tree of point leaves,
-// every leaf within the bound lies in the cube [p - rho, p + rho], whose
-// Morton codes lie between the codes of its corners; the leaves sharing the
-// corners' common code prefix form exactly one node's range of the Karras
-// radix tree, so the traversal can start at that node instead of the root
-// without changing the result.  The node's ordinal follows the reference's
-// id rule (left child -> r, right child -> l; tree.py:85-105).
-__device__ __forceinline__ int32_t subtree_entry(const lbvh_tree &t, float px, float py,
-                                                 float pz, float rho2) {
-    if (!(rho2 < INFINITY)) return 0;  // NaN (no bound) or inf
-    const float *bx = t.root_box;
-    double lo[3], ext[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        lo[a] = (double)__ldg(bx + a);
-        ext[a] = __dsub_rn((double)__ldg(bx + 3 + a), lo[a]);
-    }
-    // |dx| <= sqrt(rho2) * (1 + 2^-20) for any leaf with fp32 dist^2 <= rho2
-    const double rho = __dmul_ru(__dsqrt_ru((double)rho2), 1.0 + 0x1p-20);
-    const uint32_t cmin = morton3(__dsub_rd((double)px, rho), __dsub_rd((double)py, rho),
-                                  __dsub_rd((double)pz, rho), lo, ext);
-    const uint32_t cmax = morton3(__dadd_ru((double)px, rho), __dadd_ru((double)py, rho),
-                                  __dadd_ru((double)pz, rho), lo, ext);
-    const uint32_t x = cmin ^ cmax;
-    const int pbits = x ? __clz(x) - 2 : 30;
-    if (pbits <= 0) return 0;
-    const int sh = 30 - pbits;
-    const uint64_t base = (uint64_t)(cmin >> sh) << sh;
-    const int64_t l = dir_lower_bound(t, base);
-    const int64_t r = dir_lower_bound(t, base + (1ull << sh)) - 1;
-    const int64_t n = t.n;
-    if (r <= l) return 0;  // a single leaf (kk == 1): start from the root
-    if (l == 0 && r == n - 1) return 0;
-    const bool is_left =
-        (l == 0) || (r != n - 1 && aug_delta(t.leaf_codes, r) > aug_delta(t.leaf_codes, l - 1));
-    return (int32_t)(is_left ? r : l);
-}
-
-#ifndef LBVH_KNN_SUBTREE
-#define LBVH_KNN_SUBTREE 0  // measured slower (9.00 vs 8.61 ms, C2): the top levels are L1-hot
-#endif
-
 // 5 resident CTAs per SM (<= 48 registers, no spills) with the 12-entry
 // shared-memory stack measured fastest at K=10 (8.75 vs 8.89 ms for 6 CTAs
 // and a local-memory stack, C2); K=32 keeps the compiler's choice.
 #ifndef LBVH_KNN_MINBLOCKS
 #define LBVH_KNN_MINBLOCKS 5
-#endif
-#ifndef LBVH_KNN_STACKTOP
-#define LBVH_KNN_STACKTOP 0
-#endif
-#ifndef LBVH_KNN_DEFER
-#define LBVH_KNN_DEFER 0
 #endif
 #ifndef LBVH_KNN_SMEMSTACK
 #define LBVH_KNN_SMEMSTACK 12
@@ -376,49 +301,18 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     // and pop) and the capacity test still counts it, so node order and
     // stack exhaustion are the reference's either way.
     uint64_t stack[kStack];
-    // LBVH_KNN_STACKTOP: the top entry lives in a register (`stop`) and the
-    // local array holds the entries below it, so a pop never waits on a
-    // local-memory load (the next top is loaded while the popped node is
-    // processed).
-    constexpr bool STACKTOP = REGNEXT && LBVH_KNN_STACKTOP;
-    // LBVH_KNN_SMEMSTACK = D > 0: the first D entries live in shared memory
-    // as bare node ids (lane-interleaved, conflict-free), deeper ones in
-    // local memory.  Popped entries are not re-tested (a pruned entry costs
-    // one node visit whose children are then pruned), so pushes -- and the
-    // capacity test -- are exactly as above.
+    // LBVH_KNN_SMEMSTACK = D > 0 (REGNEXT): the first D entries live in
+    // shared memory as bare node ids (lane-interleaved, conflict-free),
+    // deeper ones in local memory.  Popped entries are not re-tested (a
+    // pruned entry costs one node visit whose children are then pruned), so
+    // pushes -- and the capacity test -- are exactly as above.
     constexpr int SMS = REGNEXT ? LBVH_KNN_SMEMSTACK : 0;
     __shared__ int32_t sst[(SMS > 0 ? SMS : 1) * LBVH_KNN_BLOCK];
     int32_t *const sbase = sst + (threadIdx.x % LBVH_KNN_BLOCK);
-    uint64_t stop = 0;
-    // LBVH_KNN_DEFER: leaf candidates wait in a 4-entry per-lane buffer and
-    // are offered when some lane's buffer reaches 3 -- by every lane of the
-    // warp at once, so the k-best insertions run on many lanes together.
-    // Pruning meanwhile uses the not-yet-updated k-th distance, which is
-    // only less tight; the final list is the same.
-    constexpr bool DEFER = REGNEXT && LBVH_KNN_DEFER;
-    uint64_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0;
-    int np = 0;
-    auto pend = [&](float d, int32_t obj) {
-        pk3 = pk2;
-        pk2 = pk1;
-        pk1 = pk0;
-        pk0 = TopK<K>::make(d, obj);
-        ++np;
-    };
-    auto flush = [&]() {
-        if (np > 0) top.offer_key(pk0);
-        if (np > 1) top.offer_key(pk1);
-        if (np > 2) top.offer_key(pk2);
-        if (np > 3) top.offer_key(pk3);
-        np = 0;
-    };
+    int32_t *const lstack = reinterpret_cast<int32_t *>(stack);
     uint32_t fail = 0;
     int sp;
     int32_t node = 0;  // the root; never pruned (the list is empty)
-    if (REGNEXT && LBVH_KNN_SUBTREE && t.leaf_dir &&
-        (t.flags & (LBVH_TREE_POINT_LEAVES | LBVH_TREE_CODES30)) ==
-            (LBVH_TREE_POINT_LEAVES | LBVH_TREE_CODES30))
-        node = subtree_entry(t, px, py, pz, bound);
     if (REGNEXT) {
         sp = 0;
     } else {
@@ -445,37 +339,26 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         int32_t next = -1;
         if (!(fd > top.worst())) {  // NaN worst = list not full yet
             if (fl < 0) {
-                if (DEFER)
-                    pend(fd, fl & 0x7FFFFFFF);
-                else
-                    top.offer(fd, fl & 0x7FFFFFFF);
+                top.offer(fd, fl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                const uint64_t e = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
                 if (SMS > 0) {
                     if (sp < SMS)
                         sbase[sp * LBVH_KNN_BLOCK] = fl;
                     else
-                        reinterpret_cast<int32_t *>(stack)[sp] = fl;
-                    ++sp;
-                } else if (STACKTOP) {
-                    if (sp > 0) stack[sp - 1] = stop;
-                    stop = e;
+                        lstack[sp] = fl;
                     ++sp;
                 } else {
-                    stack[sp++] = e;
+                    stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
                 }
             }
         }
         if (!(ndist > top.worst())) {
             if (nl < 0) {
-                if (DEFER)
-                    pend(ndist, nl & 0x7FFFFFFF);
-                else
-                    top.offer(ndist, nl & 0x7FFFFFFF);
+                top.offer(ndist, nl & 0x7FFFFFFF);
             } else {
                 if (sp >= kStack) {
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
@@ -488,36 +371,21 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
             }
         }
         if (REGNEXT) {
-            if (DEFER) {
-                const unsigned am = __activemask();
-                if (__any_sync(am, np >= 3)) flush();
-            }
             if (next < 0) {
-                // pop until an entry survives the prune test (_kernels.py:364-368)
                 if (SMS > 0) {
-                    if (sp > 0) {
-                        --sp;
-                        next = sp < SMS ? sbase[sp * LBVH_KNN_BLOCK]
-                                        : reinterpret_cast<int32_t *>(stack)[sp];
+                    if (sp == 0) break;
+                    --sp;
+                    next = sp < SMS ? sbase[sp * LBVH_KNN_BLOCK] : lstack[sp];
+                } else {
+                    // pop until an entry survives the prune test (_kernels.py:364-368)
+                    while (sp > 0) {
+                        const uint64_t e = stack[--sp];
+                        if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
+                            next = (int32_t)(uint32_t)e;
+                            break;
+                        }
                     }
-                }
-                while (SMS == 0 && sp > 0) {
-                    uint64_t e;
-                    if (STACKTOP) {
-                        e = stop;
-                        --sp;
-                        if (sp > 0) stop = stack[sp - 1];
-                    } else {
-                        e = stack[--sp];
-                    }
-                    if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
-                        next = (int32_t)(uint32_t)e;
-                        break;
-                    }
-                }
-                if (next < 0) {
-                    if (DEFER) flush();
-                    break;
+                    if (next < 0) break;
                 }
             }
             node = next;
@@ -549,324 +417,6 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
     if (s >= nq) return;
     knn_query<K, REGNEXT>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
                           status, kth, uniform);
-}
-
-// Persistent warps: each warp takes the next 32 Morton-consecutive query
-// slots from a global counter when all its lanes are done, so SM slots are
-// never held by a CTA waiting for its slowest warp (per-lane work is
-// exactly knn_kernel's).
-template <int K>
-__global__ void __launch_bounds__(LBVH_KNN_BLOCK,
-                                  knn_min_blocks(K))
-knn_warpq_kernel(const lbvh_tree t, const float *__restrict__ centers,
-                 const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
-                 int64_t nq, const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-                 float *__restrict__ out_dist, bool squared, uint32_t *status,
-                 unsigned long long *counter) {
-    const int lane = threadIdx.x & 31;
-    while (true) {
-        unsigned long long s0 = 0;
-        if (lane == 0) s0 = atomicAdd(counter, 32ull);
-        s0 = __shfl_sync(0xFFFFFFFFu, s0, 0);
-        if ((int64_t)s0 >= nq) break;
-        const int64_t s = (int64_t)s0 + lane;
-        if (s < nq)
-            knn_query<K, true>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
-                               status);
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-packet kNN.
-//
-// A warp holds 32 Morton-consecutive queries and walks ONE depth-first path
-// through the tree for all of them: every step loads one node record (the
-// same address in every lane, so one L1 transaction serves the warp), each
-// lane tests the two child boxes against its own query and k-th distance,
-// and the warp descends into a child if any lane still needs it (nearer
-// child of the lane majority first, the other pushed on a warp-uniform
-// stack that keeps each lane's own distance for the pop-time prune test).
-// Lanes offer leaves only within their own current k-th distance, so each
-// query's result is exactly the k smallest (dist^2, ordinal) pairs -- the
-// visiting order changes nothing.  The stack holds at most one entry per
-// level, so on trees of depth <= 63 neither this nor the reference's
-// per-query stack can overflow; the launcher only picks this kernel for
-// such trees (stack exhaustion elsewhere keeps the reference's behaviour).
-// ---------------------------------------------------------------------------
-template <int K>
-__global__ void __launch_bounds__(LBVH_KNN_BLOCK, knn_min_blocks(K))
-knn_packet_kernel(const lbvh_tree t, const float *__restrict__ centers,
-                  const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
-                  int64_t nq, const int64_t *__restrict__ offsets, int32_t *__restrict__ out_idx,
-                  float *__restrict__ out_dist, bool squared, uint32_t *status) {
-    const unsigned kFull = 0xFFFFFFFFu;
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= nq) return;  // whole warp idle
-    bool active = s < nq;
-    int64_t q = 0, base = 0;
-    int kk = 0;
-    float px = 0.f, py = 0.f, pz = 0.f;
-    if (active) {
-        q = order ? (int64_t)__ldg(order + s) : s;
-        base = __ldg(offsets + q);
-        kk = (int)(__ldg(offsets + q + 1) - base);
-        px = __ldg(centers + 3 * q);
-        py = __ldg(centers + 3 * q + 1);
-        pz = __ldg(centers + 3 * q + 2);
-        active = kk > 0;
-    }
-    if (t.n == 1) {
-        if (active) {
-            const float *bx = t.root_box;
-            const float d2 = box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]);
-            out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
-            out_idx[base] = __ldg(t.leaf_obj);
-        }
-        return;
-    }
-    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
-    TopK<K> top;
-    float bound = __int_as_float(0x7FFFFFFF);
-    if (active && qcodes && t.leaf_codes) bound = seed_bound<K>(t, __ldg(qcodes + s), kk, px, py, pz);
-    top.init(active ? kk : K, bound);
-    // An idle lane needs nothing: worst = -inf makes every distance "farther".
-    const float kIdle = -INFINITY;
-    uint64_t stack[kStack];
-    int sp = 0;  // warp-uniform
-    int32_t node = 0;
-    uint32_t fail = 0;
-    while (true) {
-        float4 a, b, c;
-        int4 dd;
-        load_node(nodes, node, a, b, c, dd);
-        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
-        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
-        float w = active ? top.worst() : kIdle;
-        bool nl = !(dl > w), nr = !(dr > w);
-        // leaves: offered by the lanes that still need them, nearer one first
-        if ((dd.x < 0) | (dd.y < 0)) {
-            const bool left_near = dl <= dr;
-            if (left_near) {
-                if (dd.x < 0 && nl) top.offer(dl, dd.x & 0x7FFFFFFF);
-                if (dd.y < 0 && !(dr > (active ? top.worst() : kIdle))) top.offer(dr, dd.y & 0x7FFFFFFF);
-            } else {
-                if (dd.y < 0 && nr) top.offer(dr, dd.y & 0x7FFFFFFF);
-                if (dd.x < 0 && !(dl > (active ? top.worst() : kIdle))) top.offer(dl, dd.x & 0x7FFFFFFF);
-            }
-            if (dd.x < 0) nl = false;
-            if (dd.y < 0) nr = false;
-            w = active ? top.worst() : kIdle;
-            nl = nl && !(dl > w);
-            nr = nr && !(dr > w);
-        }
-        const unsigned bl = __ballot_sync(kFull, nl), br = __ballot_sync(kFull, nr);
-        int32_t next = -1;
-        if (bl && br) {
-            // lanes for which the left child is the nearer one
-            const unsigned pl = __ballot_sync(kFull, nl && (!nr || dl <= dr));
-            const bool left_first = 2 * __popc(pl) >= __popc(bl | br);
-            if (sp >= kStack) {
-                fail = LBVH_FLAG_STACK_EXHAUSTED;
-                break;
-            }
-            const float pd = left_first ? dr : dl;
-            const int32_t pn = left_first ? dd.y : dd.x;
-            stack[sp++] = ((uint64_t)__float_as_uint(active ? pd : INFINITY) << 32) | (uint32_t)pn;
-            next = left_first ? dd.x : dd.y;
-        } else if (bl) {
-            next = dd.x;
-        } else if (br) {
-            next = dd.y;
-        } else {
-            while (sp > 0) {
-                const uint64_t e = stack[--sp];
-                const bool need = !(__uint_as_float((uint32_t)(e >> 32)) >
-                                    (active ? top.worst() : kIdle));
-                if (__any_sync(kFull, need)) {
-                    next = (int32_t)(uint32_t)e;
-                    break;
-                }
-            }
-            if (next < 0) break;
-        }
-        node = next;
-    }
-    if (fail && (threadIdx.x & 31) == 0) atomicOr(status, fail);
-    if (!active) return;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        if (j >= K - kk) {
-            const int64_t o = base + (j - (K - kk));
-            out_idx[o] = top.ordinal(j);
-            out_dist[o] = squared ? top.dist(j) : __fsqrt_rn(top.dist(j));
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent kNN with per-lane query refill.
-//
-// One thread per query leaves lanes idle while the slowest query of a warp
-// finishes (traversal lengths vary ~2x).  Here each warp owns a run of
-// kChunk consecutive Morton-ordered query slots (grabbed with one atomic),
-// and a lane that finishes its query immediately starts the next slot of the
-// run, so lanes stay busy and the warp's queries stay spatially coherent.
-// The search-radius seeds are computed by a separate convergent pass.  Per
-// query the traversal is exactly knn_kernel<K, true>'s, so results (and
-// stack-exhaustion behaviour) are identical.
-// ---------------------------------------------------------------------------
-
-constexpr int kChunk = 128;
-
-__device__ __forceinline__ uint32_t lanemask_lt_() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-template <int K>
-__global__ void __launch_bounds__(256)
-knn_seed_kernel(const lbvh_tree t, const float *__restrict__ centers,
-                const uint32_t *__restrict__ order, const uint32_t *__restrict__ qcodes,
-                int64_t nq, const int64_t *__restrict__ offsets, float *__restrict__ bounds) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nq) return;
-    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
-    const int kk = (int)(__ldg(offsets + q + 1) - __ldg(offsets + q));
-    float b = __int_as_float(0x7FFFFFFF);
-    if (kk > 0 && t.n > 1)
-        b = seed_bound<K>(t, __ldg(qcodes + s), kk, __ldg(centers + 3 * q),
-                          __ldg(centers + 3 * q + 1), __ldg(centers + 3 * q + 2));
-    bounds[s] = b;
-}
-
-template <int K>
-__global__ void __launch_bounds__(256)
-knn_persistent_kernel(const lbvh_tree t, const float *__restrict__ centers,
-                      const uint32_t *__restrict__ order, const float *__restrict__ bounds,
-                      int64_t nq, const int64_t *__restrict__ offsets,
-                      int32_t *__restrict__ out_idx, float *__restrict__ out_dist, bool squared,
-                      uint32_t *status, unsigned long long *counter) {
-    const unsigned kFull = 0xFFFFFFFFu;
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt = lanemask_lt_();
-    const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
-    int64_t chunk_next = 0, chunk_end = 0;
-    bool exhausted = false, active = false;
-    int64_t base = 0;
-    int kk = 0;
-    float px = 0.f, py = 0.f, pz = 0.f;
-    TopK<K> top;
-    top.init(K, __int_as_float(0x7FFFFFFF));
-    uint64_t stack[kStack];
-    int sp = 0;
-    int32_t node = 0;
-    uint32_t fail = 0;
-    while (true) {
-        // ---- refill idle lanes from this warp's run of query slots
-        const unsigned need = __ballot_sync(kFull, !active);
-        if (need) {
-            if (chunk_next >= chunk_end && !exhausted) {
-                unsigned long long s0 = 0;
-                if (lane == 0) s0 = atomicAdd(counter, (unsigned long long)kChunk);
-                s0 = __shfl_sync(kFull, s0, 0);
-                if ((int64_t)s0 >= nq) {
-                    exhausted = true;
-                } else {
-                    chunk_next = (int64_t)s0;
-                    chunk_end = chunk_next + kChunk < nq ? chunk_next + kChunk : nq;
-                }
-            }
-            const int64_t slot = chunk_next + __popc(need & lt);
-            if (!active && slot < chunk_end) {
-                const int64_t q = order ? (int64_t)__ldg(order + slot) : slot;
-                base = __ldg(offsets + q);
-                kk = (int)(__ldg(offsets + q + 1) - base);
-                px = __ldg(centers + 3 * q);
-                py = __ldg(centers + 3 * q + 1);
-                pz = __ldg(centers + 3 * q + 2);
-                if (kk > 0) {
-                    if (t.n == 1) {
-                        const float d2 = box_dist_sq(px, py, pz, bx_of(t, 0), bx_of(t, 1),
-                                                     bx_of(t, 2), bx_of(t, 3), bx_of(t, 4),
-                                                     bx_of(t, 5));
-                        out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
-                        out_idx[base] = __ldg(t.leaf_obj);
-                    } else {
-                        top.init(kk, bounds ? __ldg(bounds + slot) : __int_as_float(0x7FFFFFFF));
-                        sp = 0;
-                        node = 0;
-                        active = true;
-                    }
-                }
-            }
-            const int64_t avail = chunk_end - chunk_next;
-            const int64_t took = __popc(need) < avail ? (int64_t)__popc(need) : avail;
-            chunk_next += took;
-        }
-        if (!__any_sync(kFull, active)) {
-            if (exhausted) break;
-            continue;
-        }
-        if (!active) continue;
-        // ---- one node of this lane's traversal (knn_kernel<K, true> step)
-        float4 a, b, c;
-        int4 dd;
-        load_node(nodes, node, a, b, c, dd);
-        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
-        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
-        const bool left_near = dl <= dr;
-        const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
-        const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
-        int32_t next = -1;
-        bool done = false;
-        if (!(fd > top.worst())) {
-            if (fl < 0) {
-                top.offer(fd, fl & 0x7FFFFFFF);
-            } else if (sp >= kStack) {
-                fail = LBVH_FLAG_STACK_EXHAUSTED;
-                done = true;
-            } else {
-                stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
-            }
-        }
-        if (!done && !(ndist > top.worst())) {
-            if (nl < 0) {
-                top.offer(ndist, nl & 0x7FFFFFFF);
-            } else if (sp >= kStack) {
-                fail = LBVH_FLAG_STACK_EXHAUSTED;
-                done = true;
-            } else {
-                next = nl;
-            }
-        }
-        if (!done && next < 0) {
-            while (sp > 0) {
-                const uint64_t e = stack[--sp];
-                if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
-                    next = (int32_t)(uint32_t)e;
-                    break;
-                }
-            }
-            if (next < 0) done = true;
-        }
-        if (!done) {
-            node = next;
-            continue;
-        }
-        // ---- query finished: write its span, go idle
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            if (j >= K - kk) {
-                const int64_t o = base + (j - (K - kk));
-                out_idx[o] = top.ordinal(j);
-                out_dist[o] = squared ? top.dist(j) : __fsqrt_rn(top.dist(j));
-            }
-        }
-        active = false;
-    }
-    if (fail) atomicOr(status, fail);
 }
 
 // General k: the output span doubles as a bounded max-heap, exactly the
@@ -1194,66 +744,6 @@ size_t knn_workspace_bytes(int64_t nq) {
     return align_up(sizeof(float) * (size_t)(nq > 0 ? nq : 1)) + 256;
 }
 
-template <int K>
-int launch_knn_persistent(const lbvh_tree *t, const float *centers, const uint32_t *order,
-                          const uint32_t *qcodes, int64_t nq, const int64_t *offsets,
-                          int32_t *out_idx, float *out_dist, bool squared, uint32_t *status,
-                          void *ws, cudaStream_t stream) {
-    Carve c(ws, knn_workspace_bytes(nq));
-    float *bounds = c.take<float>(nq);
-    unsigned long long *counter = (unsigned long long *)((char *)ws + knn_workspace_bytes(nq) - 64);
-    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
-    const bool seed = qcodes && t->leaf_codes;
-    if (seed) {
-        knn_seed_kernel<K><<<div_up(nq, 256), 256, 0, stream>>>(*t, centers, order, qcodes, nq,
-                                                                offsets, bounds);
-        count_launches(1);
-    }
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_persistent_kernel<K>, 256, 0);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int dev = 0, sms = kNumSMs;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    unsigned g = div_up(nq, 256);
-    const unsigned cap = (unsigned)(sms * per_sm);
-    g = g < cap ? g : cap;
-    knn_persistent_kernel<K><<<g, 256, 0, stream>>>(*t, centers, order, seed ? bounds : nullptr,
-                                                    nq, offsets, out_idx, out_dist, squared,
-                                                    status, counter);
-    count_launches(1);
-    return check_launch();
-}
-
-template <int K>
-int launch_knn_warpq(const lbvh_tree *t, const float *centers, const uint32_t *order,
-                     const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int32_t *out_idx,
-                     float *out_dist, bool squared, uint32_t *status, void *ws,
-                     cudaStream_t stream) {
-    unsigned long long *counter =
-        (unsigned long long *)((char *)ws + knn_workspace_bytes(nq) - 64);
-    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_warpq_kernel<K>,
-                                                      LBVH_KNN_BLOCK, 0);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int dev = 0, sms = kNumSMs;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    unsigned g = div_up(nq, LBVH_KNN_BLOCK);
-    const unsigned cap = (unsigned)(sms * per_sm);
-    g = g < cap ? g : cap;
-    knn_warpq_kernel<K><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq, offsets,
-                                                          out_idx, out_dist, squared, status,
-                                                          counter);
-    count_launches(1);
-    return check_launch();
-}
-
 namespace {
 __global__ void __launch_bounds__(256)
 leaf_directory_kernel(const uint32_t *__restrict__ codes, int64_t n, int bits,
@@ -1299,44 +789,24 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     // 1 = nearer child kept in a register (measured faster with the seed),
     // 0 = reference push/pop per node.  Same results either way.
     static const int variant = env_int("LBVH_KNN_VARIANT", 1);
-    // 1 = persistent kernel with per-lane query refill (needs the workspace).
-    // Measured 1.7x slower on C2 (lanes drift apart in Morton order and lose
-    // L1 locality), so off by default; kept as an A/B variant.
-    static const int persistent = env_int("LBVH_KNN_PERSISTENT", 0);
     if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
-    const bool use_persistent = persistent && !kth && ws && ws_bytes >= knn_workspace_bytes(nq);
-    static const int packet = env_int("LBVH_KNN_PACKET", 0);
-    static const int warpq = env_int("LBVH_KNN_WARPQ", 0);
-    const bool use_warpq = warpq && !kth && ws && ws_bytes >= knn_workspace_bytes(nq);
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
-        if (use_persistent)                                                                 \
-            return launch_knn_persistent<KV>(t, centers, order, qcodes, nq, offsets,        \
-                                             out_idx, out_dist, squared, status, ws,        \
-                                             stream);                                       \
-        if (use_warpq)                                                                      \
-            return launch_knn_warpq<KV>(t, centers, order, qcodes, nq, offsets, out_idx,     \
-                                        out_dist, squared, status, ws, stream);             \
-        if (packet && !kth)                                                                 \
-            knn_packet_kernel<KV><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, \
-                                                                 nq, offsets, out_idx,       \
-                                                                 out_dist, squared, status); \
-        else if (variant == 1)                                                              \
-            knn_kernel<KV, true><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,     \
-                                                        offsets, out_idx, out_dist, squared, \
-                                                        status, kth, uniform);              \
+        if (variant == 1)                                                                   \
+            knn_kernel<KV, true><<<g, LBVH_KNN_BLOCK, 0, stream>>>(                        \
+                *t, centers, order, qcodes, nq, offsets, out_idx, out_dist, squared, status, \
+                kth, uniform);                                                              \
         else                                                                                \
-            knn_kernel<KV, false><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,    \
-                                                         offsets, out_idx, out_dist,        \
-                                                         squared, status, kth, uniform);    \
+            knn_kernel<KV, false><<<g, LBVH_KNN_BLOCK, 0, stream>>>(                       \
+                *t, centers, order, qcodes, nq, offsets, out_idx, out_dist, squared, status, \
+                kth, uniform);                                                              \
         count_launches(1);                                                                  \
         return check_launch();                                                              \
     }
     const bool squared = (flags & LBVH_KNN_SQUARED) != 0;
     const int uniform = (flags & LBVH_KNN_UNIFORM_SPANS) ? (int)max_span : 0;
     static const int wide = env_int("LBVH_KNN_WIDE", 1);
-    if (wide && !kth && t->nodes4 && (t->flags & LBVH_TREE_CODES30) && !use_persistent &&
-        !packet) {
+    if (wide && !kth && t->nodes4 && (t->flags & LBVH_TREE_CODES30)) {
         const int rc = knn_wide(t, centers, order, qcodes, nq, offsets, max_span, out_idx,
                                 out_dist, squared, status, stream);
         if (rc >= 0) return rc;
