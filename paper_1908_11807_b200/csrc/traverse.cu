@@ -246,6 +246,9 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
 #ifndef LBVH_KNN_SMEMSTACK
 #define LBVH_KNN_SMEMSTACK 12
 #endif
+#ifndef LBVH_KNN_PAIR_STORES
+#define LBVH_KNN_PAIR_STORES 1
+#endif
 // Threads per CTA of knn_kernel (resident threads per SM stay
 // LBVH_KNN_MINBLOCKS * 256 for K <= 16).
 #ifndef LBVH_KNN_BLOCK
@@ -395,6 +398,18 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     // the k-th squared distance (exact; the sharded search's forwarding bound)
     if (kth) kth[q] = top.dist(K - 1);
     // Spans are written even after a failure; the driver raises anyway.
+    if (LBVH_KNN_PAIR_STORES && (K & 1) == 0 && kk == K && (base & 1) == 0) {
+        // full span at an even offset: 64-bit stores (half the store requests)
+#pragma unroll
+        for (int j = 0; j < K; j += 2) {
+            const float d0 = squared ? top.dist(j) : __fsqrt_rn(top.dist(j));
+            const float d1 = squared ? top.dist(j + 1) : __fsqrt_rn(top.dist(j + 1));
+            *reinterpret_cast<int2 *>(out_idx + base + j) =
+                make_int2(top.ordinal(j), top.ordinal(j + 1));
+            *reinterpret_cast<float2 *>(out_dist + base + j) = make_float2(d0, d1);
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         if (j >= K - kk) {
