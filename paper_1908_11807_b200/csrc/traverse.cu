@@ -42,9 +42,6 @@ __device__ __forceinline__ void prefetch_children(const PackedNode *nodes, int4 
     }
 }
 
-#ifndef LBVH_SPATIAL_SMEMSTACK
-#define LBVH_SPATIAL_SMEMSTACK 0
-#endif
 #ifndef LBVH_SPATIAL_STACKTOP
 #define LBVH_SPATIAL_STACKTOP 1  // 6.95 vs 7.05 ms per 1e7-query 2P batch (C2), 32 registers
 #endif
@@ -124,11 +121,6 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
     // overflow test still counts it as a stack entry, so the node sequence,
     // hit order and stack-exhaustion behaviour are the reference's.
     int32_t stack[kStack];
-    // The first LBVH_SPATIAL_SMEMSTACK entries live in shared memory
-    // (lane-interleaved, conflict-free), deeper ones in local memory.
-    constexpr int SMS = LBVH_SPATIAL_SMEMSTACK;
-    __shared__ int32_t sst[(SMS > 0 ? SMS : 1) * 256];
-    int32_t *const sbase = sst + threadIdx.x;
     // LBVH_SPATIAL_STACKTOP: the top entry lives in a register; a pop never
     // waits on memory (the next top is reloaded while the node is fetched)
     constexpr bool STOP = LBVH_SPATIAL_STACKTOP;
@@ -159,8 +151,6 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
                 if (STOP) {  // register top; the previous top goes to memory
                     if (sp > 0) stack[sp - 1] = stop;
                     stop = d.x;
-                } else if (sp < SMS) {
-                    sbase[sp * 256] = d.x;
                 } else {
                     stack[sp] = d.x;
                 }
@@ -189,7 +179,7 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
                 node = stop;  // no memory round trip on the critical path
                 if (sp > 0) stop = stack[sp - 1];
             } else {
-                node = sp < SMS ? sbase[sp * 256] : stack[sp];
+                node = stack[sp];
             }
         } else {
             break;
