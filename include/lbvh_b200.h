@@ -281,14 +281,16 @@ int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const 
 /* query_knn for device-resident centers and a uniform k in one call: value
  * checks (LBVH_FLAG_NONFINITE), uniform CRS offsets (nq+1), Morton query
  * order on the tree's grid (order_bits of the 30-bit code; 0 = unsorted) and
- * the search.  Workspace: lbvh_knn_batch_workspace_bytes(nq).  ev_before /
- * ev_after (optional cudaEvent_t) are recorded around the search kernel on
- * `stream` (kernel timing inside a caller's timed region). */
+ * the search.  Workspace: lbvh_knn_batch_workspace_bytes(nq).  kth_d2
+ * (optional, k <= 32) receives each query's exact k-th squared distance as
+ * lbvh_knn_kth.  ev_before / ev_after (optional cudaEvent_t) are recorded
+ * around the search kernel on `stream` (kernel timing inside a caller's
+ * timed region). */
 size_t lbvh_knn_batch_workspace_bytes(int64_t nq);
 int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int64_t k,
                    int order_bits, int64_t *offsets, int32_t *out_idx, float *out_dist,
                    int flags, void *workspace, size_t workspace_bytes, uint32_t *status,
-                   void *ev_before, void *ev_after, void *stream);
+                   float *kth_d2, void *ev_before, void *ev_after, void *stream);
 
 /* lbvh_knn that also writes kth_d2[q] = the exact squared distance of query
  * q's last (k-th) neighbour -- the sharded search's forwarding bound -- so

@@ -239,8 +239,8 @@ size_t lbvh_knn_batch_workspace_bytes(int64_t nq) {
 
 int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int64_t k,
                    int order_bits, int64_t *offsets, int32_t *out_idx, float *out_dist,
-                   int flags, void *ws, size_t ws_bytes, uint32_t *status, void *ev_before,
-                   void *ev_after, void *stream) {
+                   int flags, void *ws, size_t ws_bytes, uint32_t *status, float *kth_d2,
+                   void *ev_before, void *ev_after, void *stream) {
     if (!tree || nq < 0 || k < 1 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (!centers || !offsets || !out_idx || !out_dist || !ws) return LBVH_ERR_INVALID_ARG;
@@ -265,7 +265,7 @@ int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int6
     if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
     rc = knn(tree, centers, sorted ? order : nullptr, sorted ? codes : nullptr, nq, offsets,
              span, out_idx, out_dist, flags | LBVH_KNN_UNIFORM_SPANS, rest, rest_bytes, status,
-             st, nullptr);
+             st, kth_d2);
     if (ev_after) cudaEventRecord((cudaEvent_t)ev_after, st);
     return rc;
 }

@@ -625,7 +625,7 @@ def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultS
         _lib.check(l.lbvh_knn_batch(
             tree.ctree(), dv.ptr(b.centers), nq, b.k, _ORDER_BITS if sort_queries else 0,
             dv.ptr(offsets), dv.ptr(out_idx), dv.ptr(out_dist), flags, dv.ptr(ws), ws.numel(),
-            status.ptr, evs[0], evs[1], st))
+            status.ptr, None, evs[0], evs[1], st))
         offsets, out_idx, out_dist = _finish(b.host, status, offsets, out_idx, out_dist)
         return ResultSet._trusted(offsets, out_idx, out_dist)
     _check_batch(b, status, radii=False)
@@ -682,7 +682,7 @@ def knn_with_kth(tree: Bvh, centers: torch.Tensor, k: int):
     """Device kNN (k <= 32) returning ``(ordinals i32 (m, kk), distances f32
     (m, kk), kth_d2 f32 (m,))``: the final sqrt'ed lists plus each query's
     exact squared k-th distance (the sharded search's forwarding bound), in
-    one kernel."""
+    one C call."""
     b = _knn_batch((centers, k))
     l = _lib.lib()
     st = dv.stream()
@@ -694,17 +694,13 @@ def knn_with_kth(tree: Bvh, centers: torch.Tensor, k: int):
     if nq == 0:
         return out_idx.reshape(0, span), out_dist.reshape(0, span), kth
     status = dv.Status()
-    _check_batch(b, status, radii=False)
     offsets = dv.empty(nq + 1, torch.int64)
-    ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
-    _lib.check(l.lbvh_knn_offsets(None, b.k, n, nq, dv.ptr(offsets), None, status.ptr,
-                                  dv.ptr(ws), ws.numel(), st))
-    order, qcodes = _order(tree, b, True, with_codes=True)
-    kws = dv.workspace(l.lbvh_knn_workspace_bytes(nq))
-    _lib.check(_launch("knn", lambda: l.lbvh_knn_kth(
-        tree.ctree(), dv.ptr(b.centers), dv.ptr(order), dv.ptr(qcodes), nq, dv.ptr(offsets),
-        span, dv.ptr(out_idx), dv.ptr(out_dist), 0, dv.ptr(kws), kws.numel(), status.ptr,
-        dv.ptr(kth), st)))
+    ws = dv.workspace(l.lbvh_knn_batch_workspace_bytes(nq))
+    evs = _kernel_events("knn")
+    _lib.check(l.lbvh_knn_batch(
+        tree.ctree(), dv.ptr(b.centers), nq, b.k, _ORDER_BITS, dv.ptr(offsets), dv.ptr(out_idx),
+        dv.ptr(out_dist), 0, dv.ptr(ws), ws.numel(), status.ptr, dv.ptr(kth), evs[0], evs[1],
+        st))
     _raise_flags(status.read())
     return out_idx.reshape(nq, span), out_dist.reshape(nq, span), kth
 
