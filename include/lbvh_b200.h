@@ -355,6 +355,9 @@ int lbvh_remap_leaves(const lbvh_tree *tree, int32_t *leaf_obj, void *nodes, con
 int lbvh_knn_finalize(int64_t m, int kk, const int32_t *local_idx, const float *d2,
                       const int64_t *gids, const int64_t *merged_pos, const uint64_t *merged,
                       float *out_dist, int32_t *out_gid, void *stream);
+/* dst row i = src row idx[i] (3 f32 per row): queries into send order. */
+int lbvh_gather_rows3(const float *src, const int64_t *idx, int64_t n, float *dst,
+                      void *stream);
 /* m received rows (rd f32, rg i32; m x kk) -> out_d / out_g rows dst[i]. */
 int lbvh_scatter_result_rows(int64_t m, int kk, const int64_t *dst, const float *rd,
                              const int32_t *rg, float *out_d, int32_t *out_g, void *stream);

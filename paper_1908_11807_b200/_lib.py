@@ -133,6 +133,8 @@ _SIGS = {
                                 ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p,
                                 ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn_finalize": ([ctypes.c_int64, ctypes.c_int] + [ctypes.c_void_p] * 8, ctypes.c_int),
+    "lbvh_gather_rows3": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                           ctypes.c_void_p], ctypes.c_int),
     "lbvh_scatter_result_rows": ([ctypes.c_int64, ctypes.c_int] + [ctypes.c_void_p] * 6,
                                  ctypes.c_int),
     "lbvh_morton_codes_f32": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,

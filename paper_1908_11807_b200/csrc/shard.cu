@@ -89,6 +89,20 @@ scatter_rows_kernel(int64_t m, int kk, const int64_t *__restrict__ dst,
     }
 }
 
+// dst[i] = src[idx[i]] for 3-float rows (queries gathered into send order).
+__global__ void __launch_bounds__(256)
+gather_rows3_kernel(const float *__restrict__ src, const int64_t *__restrict__ idx, int64_t n,
+                    float *__restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = __ldg(idx + i);
+        const float x = __ldg(src + 3 * j), y = __ldg(src + 3 * j + 1), z = __ldg(src + 3 * j + 2);
+        dst[3 * i] = x;
+        dst[3 * i + 1] = y;
+        dst[3 * i + 2] = z;
+    }
+}
+
 // Leaf ordinals of a local tree -> global ordinals (map[local] = global), in
 // leaf_obj and in the packed nodes' leaf links.
 __global__ void __launch_bounds__(256)
@@ -154,6 +168,15 @@ int lbvh_scatter_result_rows(int64_t m, int kk, const int64_t *dst, const float 
     unsigned g = div_up(m * kk, 256);
     g = g < kNumSMs * 16 ? g : kNumSMs * 16;
     scatter_rows_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(m, kk, dst, rd, rg, out_d, out_g);
+    count_launches(1);
+    return check_launch();
+}
+
+int lbvh_gather_rows3(const float *src, const int64_t *idx, int64_t n, float *dst,
+                      void *stream) {
+    if (n < 0 || (n > 0 && (!src || !idx || !dst))) return LBVH_ERR_INVALID_ARG;
+    if (n == 0) return LBVH_OK;
+    gather_rows3_kernel<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(src, idx, n, dst);
     count_launches(1);
     return check_launch();
 }

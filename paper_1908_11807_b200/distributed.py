@@ -576,7 +576,11 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
     rank boundary).  With several ranks the home work runs in chunks and
     chunk j's results travel (asynchronous all-to-all) while chunk j+1 is
     searched."""
+    from . import _device as dv
+    from . import _lib
+
     dev, world, g = t.engine.device, t.world, t.group
+    c = c.contiguous()
     nq = int(c.shape[0])
     kk = min(k, t.total)
     if world == 1 and not _FORCE_ROUTE:
@@ -589,7 +593,10 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
     home = torch.searchsorted(t.split_codes.to(torch.int32), codes, right=True)
     order, counts = _partition(home, world)
     sent = counts.tolist()
-    hc, hcounts = _alltoallv(c[order], None, world, g, grouped_counts=sent)
+    send = torch.empty_like(c)
+    _lib.check(_lib.lib().lbvh_gather_rows3(dv.ptr(c), dv.ptr(order), nq, dv.ptr(send),
+                                             dv.stream()))
+    hc, hcounts = _alltoallv(send, None, world, g, grouped_counts=sent)
     hc = hc.contiguous()
     mh = int(hc.shape[0])
     # rows of origin o occupy [hstart[o], hstart[o + 1]) of hc
