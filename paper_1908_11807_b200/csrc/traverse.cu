@@ -88,8 +88,11 @@ __device__ __forceinline__ bool emit(int32_t *__restrict__ out, int64_t base, in
 // `skip` (kFill only, optional): counts of a kCountBuf pass; queries whose
 // hits all fit in its rows (count <= cap) are skipped -- the compaction
 // kernel copies those.
+#ifndef LBVH_SPATIAL_BLOCK
+#define LBVH_SPATIAL_BLOCK 256
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(LBVH_SPATIAL_BLOCK, 2048 / LBVH_SPATIAL_BLOCK)
 spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
                const float *__restrict__ radii, float radius, const uint32_t *__restrict__ order,
                int64_t nq, int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
@@ -697,7 +700,7 @@ int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii,
     if (MODE != kFill && !counts) return LBVH_ERR_INVALID_ARG;
     if (MODE == kFill && !offsets) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
-    spatial_kernel<MODE><<<div_up(nq, 256), 256, 0, stream>>>(
+    spatial_kernel<MODE><<<div_up(nq, LBVH_SPATIAL_BLOCK), LBVH_SPATIAL_BLOCK, 0, stream>>>(
         *t, centers, radii, radius, order, nq, counts, offsets, out, cap, skip, status);
     count_launches(1);
     return check_launch();
