@@ -177,12 +177,14 @@ int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
 
 /* ---------------------------------------------------------------- query */
 
-/* query_sort_order(centers, scene)   replaces traversal.py:146-165.
- * order: nq u32 permutation.  scene_box: 6 floats DEVICE (tree root box).
- * sorted_codes (optional): the queries' Morton codes in `order` order.
- * order_bits: sort by the top order_bits of the 30-bit code (stable; 30 =
- * the reference's exact order).  Any order gives identical results; the
- * traversal drivers use 24 bits (3 radix passes, same warp coherence). */
+/* Traversal order of a query batch (the role of traversal.py:146-165's
+ * pre-sort).  order: nq u32 permutation.  scene_box: 6 floats DEVICE (tree
+ * root box).  sorted_codes (optional): the queries' Morton codes in `order`
+ * order (kNN seed).  order_bits: sort by the top order_bits of the 30-bit
+ * code.  Codes use fp32 cell arithmetic and may differ from the reference's
+ * f64 codes on cell boundaries: any order gives identical query results; the
+ * exact reference permutation (query_sort_order) is lbvh_morton_codes +
+ * lbvh_sort_pairs.  The drivers use 24 bits (3 radix passes). */
 size_t lbvh_query_workspace_bytes(int64_t nq);
 int lbvh_query_order(const float *centers, int64_t nq, const float *scene_box,
                      int order_bits, uint32_t *order, uint32_t *sorted_codes, void *workspace,

@@ -873,6 +873,36 @@ int morton_codes_f32(const float *pts, int64_t n, const float *scene, uint32_t *
     return check_launch();
 }
 
+namespace {
+// Query codes for traversal ordering and the kNN seed only: fp32 cell
+// arithmetic (may differ from the f64 reference codes on cell boundaries,
+// which changes neither results -- query order never does, and any window of
+// leaves gives a valid seed -- nor, measurably, coherence).
+__global__ void __launch_bounds__(256)
+query_morton_kernel(const float *__restrict__ centers, int64_t n, const float *__restrict__ scene,
+                    uint32_t *__restrict__ codes, uint32_t *__restrict__ iota) {
+    float lo[3], scale[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __ldg(scene + a);
+        const float ext = __ldg(scene + 3 + a) - lo[a];
+        scale[a] = ext > 0.0f ? 1024.0f / ext : 0.0f;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t g[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float t = (__ldg(centers + 3 * i + a) - lo[a]) * scale[a];
+            t = fminf(fmaxf(t, 0.0f), 1023.0f);  // NaN -> 0 (flagged by the value check)
+            g[a] = (uint32_t)t;
+        }
+        codes[i] = (spread_bits(g[0]) << 2) | (spread_bits(g[1]) << 1) | spread_bits(g[2]);
+        iota[i] = (uint32_t)i;
+    }
+}
+}  // namespace
+
 int query_order(const float *centers, int64_t nq, const float *scene, int order_bits,
                 uint32_t *order, uint32_t *sorted_codes, void *ws, size_t ws_bytes,
                 cudaStream_t stream) {
@@ -884,8 +914,13 @@ int query_order(const float *centers, int64_t nq, const float *scene, int order_
     Carve c(ws, ws_bytes);
     uint32_t *codes = sorted_codes ? sorted_codes : c.take<uint32_t>(nq);
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
-    morton_kernel<uint32_t><<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq,
-                                                                       scene, codes, order);
+    static const int fast = env_int("LBVH_QUERY_MORTON_F32", 1);
+    if (fast)
+        query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, codes,
+                                                                      order);
+    else
+        morton_kernel<uint32_t><<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq,
+                                                                           scene, codes, order);
     count_launches(1);
     int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
                         30 - order_bits);
