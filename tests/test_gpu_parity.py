@@ -243,6 +243,27 @@ def test_knn_list_sizes_against_oracle(k):
     assert rk.distances.tobytes() == kd.tobytes()
 
 
+@pytest.mark.parametrize("budget_rows", [0, 12])
+def test_radius_2p_without_or_with_narrow_rows(monkeypatch, budget_rows):
+    """2P without a row buffer (budget exhausted: count -> scan -> full fill,
+    the reference's scheme) and with rows narrower than most spans must give
+    the same CRS as the default path."""
+    from paper_1908_11807_b200 import traversal
+
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 50_000, 0))
+    q = torch.from_numpy(datasets.generate(datasets.CloudSpec("cube", "filled", 20_000, 1))).cuda()
+    t = lb.build(pts)
+    r = lb.default_radius(20)
+    ref = lb.query_spatial_2p(t, (q, r)).to_host()
+    if budget_rows == 0:
+        monkeypatch.setattr(traversal, "_ROW_BUDGET", 1)
+    else:
+        monkeypatch.setattr(traversal, "_ROW_HITS", budget_rows)
+    got = lb.query_spatial_2p(t, (q, r)).to_host()
+    assert np.array_equal(got.offsets, ref.offsets)
+    assert np.array_equal(got.indices, ref.indices)
+
+
 def test_large_scale_properties_1e7():
     """Full C2 size: size-independent properties (sortedness of leaf codes,
     containment, root box == scene box), plus oracle parity on a query sample."""
