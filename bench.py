@@ -545,7 +545,7 @@ def cpu_baseline(args, pts, qs, k):
     bounded sample: the full m-point tree, the first cpu_sample queries."""
     from oracle import oracle
 
-    threads = oracle.max_threads()
+    threads = host_threads(oracle)
     ref = oracle.build(pts, threads=threads)
     sample = qs[: args.cpu_sample]
     oracle.query_knn(ref, sample[:1000], k, threads=threads)  # warm
@@ -567,6 +567,16 @@ def cpu_baseline(args, pts, qs, k):
 # ---------------------------------------------------------------------------
 
 
+def host_threads(oracle) -> int:
+    """All host cores this process may use (torchrun exports OMP_NUM_THREADS=1,
+    which the oracle's num_threads clause overrides)."""
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count() or 1
+    return max(avail, oracle.max_threads())
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -579,7 +589,7 @@ def run_reference(args):
     k = args.k
     pts = ds.generate(ds.CloudSpec("cube", "filled", m, 0))
     qs = ds.generate(ds.CloudSpec("cube", "filled", nq, 1))
-    threads = oracle.max_threads()
+    threads = host_threads(oracle)
     ref = oracle.build(pts, threads=threads)
     sample = max(1000, min(args.cpu_sample // 4, nq))
     for w in range(args.warmup):
