@@ -204,26 +204,31 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
         if (cnt > cap) continue;  // did not fit its row: written by the overflow fill pass
         const int64_t dst = __ldg(offsets + q);
         const int32_t *row = buf + q * cap;
-        if ((cap & 7) == 0) {  // 32-byte aligned rows: 256-bit loads
-            for (int32_t j = 0; j < cnt; j += 8) {
+        if ((cap & 7) == 0) {  // 32-byte aligned rows: 256-bit loads of full chunks
+            int32_t j = 0;
+            for (; j + 8 <= cnt; j += 8) {
                 float4 x, y;
                 ldg256(row + j, x, y);
-                const int32_t v[8] = {__float_as_int(x.x), __float_as_int(x.y),
-                                      __float_as_int(x.z), __float_as_int(x.w),
-                                      __float_as_int(y.x), __float_as_int(y.y),
-                                      __float_as_int(y.z), __float_as_int(y.w)};
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (j + u < cnt) out[dst + j + u] = v[u];
+                out[dst + j] = __float_as_int(x.x);
+                out[dst + j + 1] = __float_as_int(x.y);
+                out[dst + j + 2] = __float_as_int(x.z);
+                out[dst + j + 3] = __float_as_int(x.w);
+                out[dst + j + 4] = __float_as_int(y.x);
+                out[dst + j + 5] = __float_as_int(y.y);
+                out[dst + j + 6] = __float_as_int(y.z);
+                out[dst + j + 7] = __float_as_int(y.w);
             }
+            for (; j < cnt; ++j) out[dst + j] = __ldcs(row + j);  // never reads unwritten slots
         } else if ((cap & 3) == 0) {
-            for (int32_t j = 0; j < cnt; j += 4) {
+            int32_t j = 0;
+            for (; j + 4 <= cnt; j += 4) {
                 const int4 v = __ldcs(reinterpret_cast<const int4 *>(row + j));
                 out[dst + j] = v.x;
-                if (j + 1 < cnt) out[dst + j + 1] = v.y;
-                if (j + 2 < cnt) out[dst + j + 2] = v.z;
-                if (j + 3 < cnt) out[dst + j + 3] = v.w;
+                out[dst + j + 1] = v.y;
+                out[dst + j + 2] = v.z;
+                out[dst + j + 3] = v.w;
             }
+            for (; j < cnt; ++j) out[dst + j] = __ldcs(row + j);
         } else {
             for (int32_t j = 0; j < cnt; ++j) out[dst + j] = __ldcs(row + j);
         }
