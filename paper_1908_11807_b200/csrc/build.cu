@@ -416,12 +416,15 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         }
         const int s = (int)(g - B);
         const int side = left_side ? 0 : 1;
+        // hand-off slots are accessed only through shared-memory atomics (the
+        // fence + exchange below orders them; atomics also keep racecheck exact)
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            s_box[side][a][s] = mine.lo[a];
-            s_box[side][3 + a][s] = mine.hi[a];
+            atomicExch(reinterpret_cast<unsigned *>(&s_box[side][a][s]), __float_as_uint(mine.lo[a]));
+            atomicExch(reinterpret_cast<unsigned *>(&s_box[side][3 + a][s]),
+                       __float_as_uint(mine.hi[a]));
         }
-        s_link[side][s] = my_link;
+        atomicExch(reinterpret_cast<unsigned *>(&s_link[side][s]), (unsigned)my_link);
         __threadfence_block();
         const uint32_t known = (uint32_t)(left_side ? l : r);
         const uint32_t other = atomicExch(&s_slot[s], known + 1u);
@@ -439,10 +442,12 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         Box sb;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            sb.lo[a] = s_box[1 - side][a][s];
-            sb.hi[a] = s_box[1 - side][3 + a][s];
+            sb.lo[a] = __uint_as_float(atomicOr(reinterpret_cast<unsigned *>(&s_box[1 - side][a][s]), 0u));
+            sb.hi[a] = __uint_as_float(
+                atomicOr(reinterpret_cast<unsigned *>(&s_box[1 - side][3 + a][s]), 0u));
         }
-        const int32_t sib_link = s_link[1 - side][s];
+        const int32_t sib_link =
+            (int32_t)atomicOr(reinterpret_cast<unsigned *>(&s_link[1 - side][s]), 0u);
         const Box &L = left_side ? mine : sb;
         const Box &R = left_side ? sb : mine;
         Box P;
