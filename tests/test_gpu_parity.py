@@ -343,3 +343,50 @@ def test_pipelined_host_knn_equals_device_path():
     assert np.array_equal(host.indices[-50000:], ki)
     unsorted = lb.query_knn(t, (pin.numpy(), 10), sort_queries=False)
     assert np.array_equal(unsorted.indices, host.indices)
+
+
+@pytest.mark.parametrize("kmax", [8, 16, 40])
+def test_per_query_k_device_tensors_against_oracle(kmax):
+    """Per-query k as a CUDA tensor: spans of min(k_q, n), register lists or the
+    shared-memory heap chosen by max(k), identical to the reference."""
+    rng = np.random.default_rng(kmax)
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 30_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 4_000, 1))
+    ks = rng.integers(1, kmax + 1, size=q.shape[0])
+    ko, ki, kd = oracle.query_knn(oracle.build(pts), q, ks)
+    rk = lb.query_knn(lb.build(pts), (torch.from_numpy(q).cuda(), torch.from_numpy(ks).cuda()))
+    h = rk.to_host()
+    assert np.array_equal(h.offsets, ko)
+    assert np.array_equal(h.indices, ki)
+    assert h.distances.tobytes() == kd.tobytes()
+
+
+def test_per_query_radii_device_tensors_2p_and_1p():
+    pts = datasets.generate(datasets.CloudSpec("sphere", "hollow", 30_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", 4_000, 1)) * 0.3
+    radii = np.random.default_rng(3).uniform(0.0, 4.0, size=q.shape[0]).astype(np.float32)
+    ref = oracle.build(pts)
+    so, si = oracle.query_spatial_2p(ref, q, radii)
+    t = lb.build(pts)
+    qd, rd = torch.from_numpy(q).cuda(), torch.from_numpy(radii).cuda()
+    rs = lb.query_spatial_2p(t, (qd, rd)).to_host()
+    assert np.array_equal(rs.offsets, so) and np.array_equal(rs.indices, si)
+    r1, fb = lb.query_spatial_1p(t, (qd, rd), 8)
+    o1, i1, fb1 = oracle.query_spatial_1p(ref, q, radii, 8)
+    r1 = r1.to_host()
+    assert fb == fb1 and np.array_equal(r1.offsets, o1)
+    assert np.array_equal(sorted_concat(r1.offsets, r1.indices), sorted_concat(o1, i1))
+
+
+@pytest.mark.parametrize("k", [10, 20, 100])
+def test_all_duplicate_points_tie_order(k):
+    """10,000 copies of one point (test_acceptance.py:171): every distance ties,
+    so spans are decided by ordinal alone -- in every kernel size class."""
+    pts = np.tile(np.array([[0.5, -2.0, 3.25]], dtype=np.float32), (10_000, 1))
+    q = np.array([[0.5, -2.0, 3.25], [10.0, 10.0, 10.0], [-3.0, 0.0, 1.0]], dtype=np.float32)
+    ko, ki, kd = oracle.query_knn(oracle.build(pts), q, k)
+    rk = lb.query_knn(lb.build(pts), (q, k))
+    assert np.array_equal(rk.offsets, ko)
+    assert np.array_equal(rk.indices, ki)
+    assert rk.distances.tobytes() == kd.tobytes()
+    assert np.array_equal(rk.indices[:k], np.arange(k, dtype=np.int32))
