@@ -390,3 +390,24 @@ def test_all_duplicate_points_tie_order(k):
     assert np.array_equal(rk.indices, ki)
     assert rk.distances.tobytes() == kd.tobytes()
     assert np.array_equal(rk.indices[:k], np.arange(k, dtype=np.int32))
+
+
+@pytest.mark.parametrize("k", [3, 10, 20])
+def test_extreme_magnitudes_infinite_distances(k):
+    """Coordinates near +-3e38 (test_build.py:220-233): squared distances
+    overflow to +inf, so many candidates tie at inf and the ordinal decides --
+    register lists and the shared-memory heap must agree with the reference."""
+    rng = np.random.default_rng(11)
+    pts = (rng.uniform(-1, 1, size=(200, 3)) * 3e38).astype(np.float32)
+    pts[:4] = [[-3e38] * 3, [3e38] * 3, [0, 0, 0], [3e38, -3e38, 0]]
+    q = (rng.uniform(-1, 1, size=(64, 3)) * 3e38).astype(np.float32)
+    ref = oracle.build(pts)
+    t = lb.build(pts)
+    ko, ki, kd = oracle.query_knn(ref, q, k)
+    rk = lb.query_knn(t, (q, k))
+    assert np.array_equal(rk.offsets, ko)
+    assert np.array_equal(rk.indices, ki)
+    assert rk.distances.tobytes() == kd.tobytes()
+    so, si = oracle.query_spatial_2p(ref, q, 1e38)
+    rs = lb.query_spatial_2p(t, (q, 1e38))
+    assert np.array_equal(rs.offsets, so) and np.array_equal(rs.indices, si)
