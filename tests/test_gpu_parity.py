@@ -411,3 +411,23 @@ def test_extreme_magnitudes_infinite_distances(k):
     so, si = oracle.query_spatial_2p(ref, q, 1e38)
     rs = lb.query_spatial_2p(t, (q, 1e38))
     assert np.array_equal(rs.offsets, so) and np.array_equal(rs.indices, si)
+
+
+@pytest.mark.parametrize("k", [5, 24])
+def test_volumetric_boxes_knn_and_radius_device(k):
+    """(n, 6) box leaves given as a CUDA tensor: point-to-box distances (0 inside
+    a box, so heavy ties at 0) through the fused device calls."""
+    rng = np.random.default_rng(21)
+    lo = rng.uniform(-20, 20, size=(5_000, 3)).astype(np.float32)
+    hi = lo + rng.uniform(0, 3, size=(5_000, 3)).astype(np.float32)
+    rows = np.concatenate([lo, hi], axis=1)
+    q = rng.uniform(-22, 22, size=(2_000, 3)).astype(np.float32)
+    ref = oracle.build(rows)
+    t = lb.build(torch.from_numpy(rows).cuda())
+    ko, ki, kd = oracle.query_knn(ref, q, k)
+    h = lb.query_knn(t, (torch.from_numpy(q).cuda(), k)).to_host()
+    assert np.array_equal(h.offsets, ko) and np.array_equal(h.indices, ki)
+    assert h.distances.tobytes() == kd.tobytes()
+    so, si = oracle.query_spatial_2p(ref, q, 1.5)
+    rs = lb.query_spatial_2p(t, (torch.from_numpy(q).cuda(), 1.5)).to_host()
+    assert np.array_equal(rs.offsets, so) and np.array_equal(rs.indices, si)
