@@ -25,6 +25,8 @@ LIB = os.path.join(OUT_DIR, "liblbvh_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}"]
+# extra flags for A/B builds of compiler options (e.g. LBVH_NVCC_EXTRA="-Xptxas -O3")
+NVCC_FLAGS += os.environ.get("LBVH_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:
