@@ -44,6 +44,12 @@ constexpr int kSortWarps = kSortThreads / 32;
 #define LBVH_SORT_EARLY_AGG 1
 #endif
 
+// > 0: the digit histogram kernel runs at most this many CTAs per SM over a
+// grid-stride loop (0: one CTA per 8192 keys).
+#ifndef LBVH_SORT_HIST_STRIDE
+#define LBVH_SORT_HIST_STRIDE 2  // 1e7 keys: 21.7 vs 33 us (2 vs 4: same)
+#endif
+
 template <typename KeyT>
 struct SortCfg {
     static constexpr int kItems = sizeof(KeyT) == 4 ? LBVH_SORT_ITEMS : 8;
@@ -67,6 +73,29 @@ histogram_kernel(const KeyT *__restrict__ keys, int64_t n, int passes, int first
     __shared__ uint32_t s_hist[P][kRadix];
     for (int i = threadIdx.x; i < P * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
+#if LBVH_SORT_HIST_STRIDE
+    // grid-stride over 8192-key chunks, the chunk's loads issued together;
+    // a grid of a few CTAs per SM keeps the final global atomics few
+    for (int64_t base = (int64_t)blockIdx.x * kHistThreads * kHistItems; base < n;
+         base += (int64_t)gridDim.x * kHistThreads * kHistItems) {
+        KeyT k[kHistItems];
+#pragma unroll
+        for (int j = 0; j < kHistItems; ++j) {
+            const int64_t i = base + (int64_t)j * kHistThreads + threadIdx.x;
+            k[j] = i < n ? __ldcs(keys + i) : (KeyT)0;
+        }
+#pragma unroll
+        for (int j = 0; j < kHistItems; ++j) {
+            if (base + (int64_t)j * kHistThreads + threadIdx.x >= n) break;
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                if (p < passes)
+                    atomicAdd(&s_hist[p][(uint32_t)(k[j] >> (first_bit + p * kRadixBits)) &
+                                         (kRadix - 1)],
+                              1u);
+        }
+    }
+#else
     int64_t base = (int64_t)blockIdx.x * kHistThreads * kHistItems;
     for (int j = 0; j < kHistItems; ++j) {
         int64_t i = base + (int64_t)j * kHistThreads + threadIdx.x;
@@ -78,6 +107,7 @@ histogram_kernel(const KeyT *__restrict__ keys, int64_t n, int passes, int first
                           1u);
         }
     }
+#endif
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
         uint32_t c = (&s_hist[0][0])[i];
@@ -331,6 +361,8 @@ int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, siz
     cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
+    if (LBVH_SORT_HIST_STRIDE && hist_blocks > (unsigned)(kNumSMs * LBVH_SORT_HIST_STRIDE))
+        hist_blocks = kNumSMs * LBVH_SORT_HIST_STRIDE;
     histogram_kernel<KeyT><<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, first_bit,
                                                                       hist);
     exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes);
