@@ -47,7 +47,5 @@ if op == "build":
 else:
     chk = (f"check={float(rs.distances.double().sum()):.6f}" if op == "knn"
            else f"check={int(rs.offsets[-1])}:{int((rs.indices.long() % 1000003).sum())}")
-_unused = ("" if op == "build" else f"check={float(rs.distances.double().sum()):.6f}" if op == "knn"
-       else f"check={int(rs.offsets[-1])}:{int((rs.indices.long() % 1000003).sum())}")
 print(f"{op} n={n} k={k} src={src} median_ms={times[len(times) // 2]:.4f} min_ms={times[0]:.4f} "
       f"{chk}")
