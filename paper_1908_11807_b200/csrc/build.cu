@@ -49,6 +49,9 @@ __device__ __forceinline__ void warp_minmax(float v[6]) {
     }
 }
 
+#ifndef LBVH_REDUCE_VEC
+#define LBVH_REDUCE_VEC 1  // point clouds: 3 float4 loads per 4 points (build 1.44 vs 1.46 ms)
+#endif
 // K1: scene box (exact min/max) and the check_boxes value checks.  The last
 // CTA to finish folds the per-CTA partials (threadfence reduction).
 __global__ void __launch_bounds__(kReduceThreads)
@@ -58,7 +61,28 @@ scene_reduce_kernel(const float *__restrict__ mins, const float *__restrict__ ma
     float v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
     uint32_t bad = 0;
     const bool same = (mins == maxs);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+    int64_t first = 0;
+#if LBVH_REDUCE_VEC
+    if (same && (reinterpret_cast<uintptr_t>(mins) & 15) == 0) {
+        // points: 4 points = 3 float4 per step, axes in a fixed pattern
+        const float4 *m4 = reinterpret_cast<const float4 *>(mins);
+        const int64_t chunks = n / 4;
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks;
+             c += (int64_t)gridDim.x * blockDim.x) {
+            const float4 x = __ldcs(m4 + 3 * c), y = __ldcs(m4 + 3 * c + 1),
+                         z = __ldcs(m4 + 3 * c + 2);
+            const float f[12] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w, z.x, z.y, z.z, z.w};
+#pragma unroll
+            for (int j = 0; j < 12; ++j) {
+                if (!isfinite(f[j])) bad |= LBVH_FLAG_NONFINITE;
+                v[j % 3] = fminf(v[j % 3], f[j]);
+                v[3 + j % 3] = fmaxf(v[3 + j % 3], f[j]);
+            }
+        }
+        first = chunks * 4;
+    }
+#endif
+    for (int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
