@@ -4,6 +4,7 @@ GPU package through its public API."""
 
 import numpy as np
 import pytest
+import torch
 from hypothesis import given, settings, strategies as st
 
 import paper_1908_11807_b200 as lb
@@ -85,6 +86,16 @@ def test_empty_and_invalid_inputs():
         lb.build(np.float32([[0, 0, 0], [np.inf, 0, 0]]))
     with pytest.raises(ValueError, match="min corner above"):
         lb.build(np.float32([[1, 0, 0, 0, 1, 1]]))
+
+
+@pytest.mark.parametrize("pos", [0, 517, 998, 999])
+def test_device_build_flags_nonfinite_points(pos):
+    # device input skips the host validation: the scene-reduce kernel's checks
+    # (vectorised 4-point steps and the scalar tail) must flag every position
+    pts = np.random.default_rng(3).uniform(-1, 1, size=(1000, 3)).astype(np.float32)
+    pts[pos, pos % 3] = np.nan if pos % 2 else np.inf
+    with pytest.raises(ValueError, match="finite"):
+        lb.build(torch.from_numpy(pts).cuda())
 
 
 def test_leaves_in_morton_sorted_order():
