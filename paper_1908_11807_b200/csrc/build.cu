@@ -962,15 +962,22 @@ int query_order(const float *centers, int64_t nq, const float *scene, int order_
     uint32_t *codes = sorted_codes ? sorted_codes : c.take<uint32_t>(nq);
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
     static const int fast = env_int("LBVH_QUERY_MORTON_F32", 1);
+    // odd pass counts: encode straight into the sort's ping-pong buffers so
+    // the last pass writes (codes, order) -- no copy-back
+    const bool odd = (sort_pass_count(30, 30 - order_bits) & 1) != 0;
+    uint32_t *kin = codes, *vin = order;
+    if (odd) sort_alt_buffers(sort_ws, sort_workspace_bytes(nq), nq, &kin, &vin);
     if (fast)
-        query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, codes,
-                                                                      order);
+        query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, kin,
+                                                                      vin);
     else
         morton_kernel<uint32_t><<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq,
-                                                                           scene, codes, order);
+                                                                           scene, kin, vin);
     count_launches(1);
-    int rc = sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
-                        30 - order_bits);
+    int rc = odd ? sort_pairs_from_alt(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq),
+                                       stream, 30 - order_bits)
+                 : sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
+                              30 - order_bits);
     if (rc != LBVH_OK) return rc;
     return check_launch();
 }

@@ -18,6 +18,12 @@ size_t sort_workspace_bytes(int64_t n);
 // Stable LSD sort on key bits [first_bit, key_bits).
 int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                size_t ws_bytes, cudaStream_t stream, int first_bit = 0);
+// The workspace's ping-pong buffers, where sort_pairs_from_alt expects its
+// input; pass count of a sort of bits [first_bit, key_bits).
+void sort_alt_buffers(void *ws, size_t ws_bytes, int64_t n, uint32_t **k_alt, uint32_t **v_alt);
+int sort_pass_count(int key_bits, int first_bit);
+int sort_pairs_from_alt(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+                        size_t ws_bytes, cudaStream_t stream, int first_bit);
 size_t sort64_workspace_bytes(int64_t n);
 int sort_pairs64(uint64_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                  size_t ws_bytes, cudaStream_t stream);

@@ -337,9 +337,12 @@ size_t sort_ws_bytes(int64_t n) {
     return b + 256;
 }
 
+// from_alt: the input pairs were written to the workspace's ping-pong buffers
+// (sort_alt_buffers) -- with an odd pass count the result then lands in
+// (keys, vals) without the final device copies.
 template <typename KeyT>
 int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, size_t ws_bytes,
-              cudaStream_t stream, int first_bit) {
+              cudaStream_t stream, int first_bit, bool from_alt = false) {
     using C = SortCfg<KeyT>;
     if (n <= 1) return LBVH_OK;
     if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
@@ -363,13 +366,17 @@ int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, siz
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
     if (LBVH_SORT_HIST_STRIDE && hist_blocks > (unsigned)(kNumSMs * LBVH_SORT_HIST_STRIDE))
         hist_blocks = kNumSMs * LBVH_SORT_HIST_STRIDE;
-    histogram_kernel<KeyT><<<hist_blocks, kHistThreads, 0, stream>>>(keys, n, passes, first_bit,
+    KeyT *ks = keys, *kd = k_alt;
+    uint32_t *vs = vals, *vd = v_alt;
+    if (from_alt) {
+        ks = k_alt; kd = keys;
+        vs = v_alt; vd = vals;
+    }
+    histogram_kernel<KeyT><<<hist_blocks, kHistThreads, 0, stream>>>(ks, n, passes, first_bit,
                                                                       hist);
     exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes);
     count_launches(2);
 
-    KeyT *ks = keys, *kd = k_alt;
-    uint32_t *vs = vals, *vd = v_alt;
     for (int p = 0; p < passes; ++p) {
         onesweep_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, stream>>>(
             ks, vs, kd, vd, n, first_bit + p * kRadixBits, hist + p * kRadix,
@@ -393,6 +400,21 @@ size_t sort64_workspace_bytes(int64_t n) { return sort_ws_bytes<uint64_t>(n); }
 int sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                size_t ws_bytes, cudaStream_t stream, int first_bit) {
     return sort_impl<uint32_t>(keys, vals, n, key_bits, ws, ws_bytes, stream, first_bit);
+}
+
+void sort_alt_buffers(void *ws, size_t ws_bytes, int64_t n, uint32_t **k_alt, uint32_t **v_alt) {
+    Carve c(ws, ws_bytes);
+    *k_alt = c.take<uint32_t>(n);
+    *v_alt = c.take<uint32_t>(n);
+}
+
+int sort_pass_count(int key_bits, int first_bit) {
+    return (key_bits - first_bit + kRadixBits - 1) / kRadixBits;
+}
+
+int sort_pairs_from_alt(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+                        size_t ws_bytes, cudaStream_t stream, int first_bit) {
+    return sort_impl<uint32_t>(keys, vals, n, key_bits, ws, ws_bytes, stream, first_bit, true);
 }
 
 int sort_pairs64(uint64_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,

@@ -57,7 +57,7 @@ class Bvh:
     in which case the arrays are uploaded and packed on first query.
     """
 
-    __slots__ = ("_host", "_dev", "_n")
+    __slots__ = ("_host", "_dev", "_n", "_ct")
 
     _FIELDS = ("node_mins", "node_maxs", "left", "right", "leaf_obj", "scene_min", "scene_max")
 
@@ -135,7 +135,13 @@ class Bvh:
         object.__setattr__(self, "_dev", d)
 
     def ctree(self) -> _lib.CTree:
-        return _ctree(self.device_arrays(), self._n)
+        """The C-ABI tree struct (cached: device buffers never move once built)."""
+        d = self.device_arrays()
+        ct = getattr(self, "_ct", None)
+        if ct is None or ct[0] is not d:
+            ct = (d, _ctree(d, self._n))
+            object.__setattr__(self, "_ct", ct)
+        return ct[1]
 
     # -- reference API -----------------------------------------------------
     @property
