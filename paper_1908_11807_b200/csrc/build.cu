@@ -927,7 +927,12 @@ namespace {
 // leaves gives a valid seed -- nor, measurably, coherence).
 __global__ void __launch_bounds__(256)
 query_morton_kernel(const float *__restrict__ centers, int64_t n, const float *__restrict__ scene,
-                    uint32_t *__restrict__ codes, uint32_t *__restrict__ iota) {
+                    uint32_t *__restrict__ codes, uint32_t *__restrict__ iota,
+                    uint32_t *status = nullptr, int64_t *__restrict__ offsets = nullptr,
+                    int64_t span = 0) {
+    // optional fused batch prologue: the value check of the centers
+    // (check_queries_kernel) and uniform CRS offsets (uniform_offsets_kernel)
+    uint32_t bad = 0;
     float lo[3], scale[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -940,19 +945,27 @@ query_morton_kernel(const float *__restrict__ centers, int64_t n, const float *_
         uint32_t g[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            float t = (__ldg(centers + 3 * i + a) - lo[a]) * scale[a];
+            const float c = __ldg(centers + 3 * i + a);
+            if (!isfinite(c)) bad |= LBVH_FLAG_NONFINITE;
+            float t = (c - lo[a]) * scale[a];
             t = fminf(fmaxf(t, 0.0f), 1023.0f);  // NaN -> 0 (flagged by the value check)
             g[a] = (uint32_t)t;
         }
         codes[i] = (spread_bits(g[0]) << 2) | (spread_bits(g[1]) << 1) | spread_bits(g[2]);
         iota[i] = (uint32_t)i;
+        if (offsets) offsets[i] = i * span;
+    }
+    if (offsets && blockIdx.x == 0 && threadIdx.x == 0) offsets[n] = n * span;
+    if (status) {
+        bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+        if (bad && (threadIdx.x & 31) == 0) atomicOr(status, bad);
     }
 }
 }  // namespace
 
 int query_order(const float *centers, int64_t nq, const float *scene, int order_bits,
                 uint32_t *order, uint32_t *sorted_codes, void *ws, size_t ws_bytes,
-                cudaStream_t stream) {
+                cudaStream_t stream, uint32_t *status, int64_t *offsets, int64_t span) {
     if (nq < 0 || (nq > 0 && (!centers || !order)) || !scene) return LBVH_ERR_INVALID_ARG;
     if (order_bits < 1 || order_bits > 30) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
@@ -967,9 +980,9 @@ int query_order(const float *centers, int64_t nq, const float *scene, int order_
     const bool odd = (sort_pass_count(30, 30 - order_bits) & 1) != 0;
     uint32_t *kin = codes, *vin = order;
     if (odd) sort_alt_buffers(sort_ws, sort_workspace_bytes(nq), nq, &kin, &vin);
-    if (fast)
+    if (fast || status || offsets)
         query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, kin,
-                                                                      vin);
+                                                                      vin, status, offsets, span);
     else
         morton_kernel<uint32_t><<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq,
                                                                            scene, kin, vin);

@@ -45,8 +45,10 @@ int unpack_boxes(const lbvh_tree *, float *, float *, cudaStream_t);
 int morton_codes_f64(const double *, int64_t, const double *, const double *, uint32_t *,
                      cudaStream_t);
 size_t query_workspace_bytes(int64_t nq);
+// status / offsets (optional): fused value check and uniform CRS offsets
 int query_order(const float *, int64_t, const float *, int, uint32_t *, uint32_t *, void *,
-                size_t, cudaStream_t);
+                size_t, cudaStream_t, uint32_t *status = nullptr, int64_t *offsets = nullptr,
+                int64_t span = 0);
 int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
                   int64_t, int32_t *, int32_t *, int64_t, uint32_t *, cudaStream_t);
 int spatial_fill(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
@@ -251,17 +253,20 @@ int lbvh_knn_batch(const lbvh_tree *tree, const float *centers, int64_t nq, int6
     uint32_t *codes = c.take<uint32_t>(nq);
     void *rest = c.take<char>(1);
     const size_t rest_bytes = ws_bytes - ((char *)rest - (char *)ws);
-    int rc = check_queries(centers, nq, nullptr, status, st);
-    if (rc) return rc;
-    rc = knn_offsets(nullptr, k, tree->n, nq, offsets, nullptr, status, rest, rest_bytes, st);
-    if (rc) return rc;
+    const int64_t span = k < tree->n ? k : tree->n;
     const bool sorted = order_bits > 0 && nq > 1;
+    int rc;
     if (sorted) {
+        // one pass over the centers: value check, uniform offsets, Morton codes
         rc = query_order(centers, nq, tree->root_box, order_bits, order, codes, rest,
-                         rest_bytes, st);
+                         rest_bytes, st, status, offsets, span);
+        if (rc) return rc;
+    } else {
+        rc = check_queries(centers, nq, nullptr, status, st);
+        if (rc) return rc;
+        rc = knn_offsets(nullptr, k, tree->n, nq, offsets, nullptr, status, rest, rest_bytes, st);
         if (rc) return rc;
     }
-    const int64_t span = k < tree->n ? k : tree->n;
     if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
     rc = knn(tree, centers, sorted ? order : nullptr, sorted ? codes : nullptr, nq, offsets,
              span, out_idx, out_dist, flags | LBVH_KNN_UNIFORM_SPANS, rest, rest_bytes, status,

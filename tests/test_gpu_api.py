@@ -98,6 +98,21 @@ def test_device_build_flags_nonfinite_points(pos):
         lb.build(torch.from_numpy(pts).cuda())
 
 
+@pytest.mark.parametrize("pos", [0, 1234, 4999])
+def test_device_knn_flags_nonfinite_centers(pos):
+    # device centers: the fused prologue (value check + offsets + Morton codes)
+    # of the one-call kNN batch must flag a bad center anywhere in the batch
+    pts = np.random.default_rng(4).uniform(-1, 1, size=(2000, 3)).astype(np.float32)
+    t = lb.build(pts)
+    qs = np.random.default_rng(5).uniform(-1, 1, size=(5000, 3)).astype(np.float32)
+    qs[pos, 2 - pos % 3] = np.inf if pos % 2 else np.nan
+    with pytest.raises(ValueError, match="finite"):
+        lb.query_knn(t, (torch.from_numpy(qs).cuda(), 7))
+    good = torch.from_numpy(np.nan_to_num(qs, posinf=0.5, nan=0.25)).cuda()
+    rs = lb.query_knn(t, (good, 7))
+    assert torch.equal(rs.offsets.cpu(), torch.arange(5001, dtype=torch.int64) * 7)
+
+
 def test_leaves_in_morton_sorted_order():
     pts = np.random.default_rng(11).uniform(-3, 3, size=(200, 3)).astype(np.float32)
     t = lb.build(pts)
