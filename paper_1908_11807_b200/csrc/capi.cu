@@ -292,12 +292,17 @@ int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const 
         return LBVH_ERR_INVALID_ARG;
     if (ws_bytes < lbvh_spatial_count_batch_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
     cudaStream_t st = S(stream);
-    int rc = check_queries(centers, nq, radii, status, st);
-    if (rc) return rc;
     const bool sorted = order_bits > 0 && nq > 1;
+    // scalar radius: the centers' value check rides on the query Morton pass
+    const bool fused_check = sorted && !radii;
+    int rc = LBVH_OK;
+    if (!fused_check) {
+        rc = check_queries(centers, nq, radii, status, st);
+        if (rc) return rc;
+    }
     if (sorted) {
         rc = query_order(centers, nq, tree->root_box, order_bits, order, nullptr, ws, ws_bytes,
-                         st);
+                         st, fused_check ? status : nullptr);
         if (rc) return rc;
     }
     const uint32_t *ord = sorted ? order : nullptr;

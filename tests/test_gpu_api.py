@@ -113,6 +113,20 @@ def test_device_knn_flags_nonfinite_centers(pos):
     assert torch.equal(rs.offsets.cpu(), torch.arange(5001, dtype=torch.int64) * 7)
 
 
+@pytest.mark.parametrize("pos", [0, 2500, 4999])
+def test_device_radius_flags_nonfinite_centers(pos):
+    # scalar radius on device centers: the value check is fused into the
+    # query Morton pass of the one-call count stage
+    pts = np.random.default_rng(6).uniform(-1, 1, size=(2000, 3)).astype(np.float32)
+    t = lb.build(pts)
+    qs = np.random.default_rng(7).uniform(-1, 1, size=(5000, 3)).astype(np.float32)
+    qs[pos, pos % 3] = -np.inf if pos % 2 else np.nan
+    for run in (lambda q: lb.query_spatial_2p(t, (q, 0.1)),
+                lambda q: lb.query_spatial_1p(t, (q, 0.1), 16)):
+        with pytest.raises(ValueError, match="finite"):
+            run(torch.from_numpy(qs).cuda())
+
+
 def test_leaves_in_morton_sorted_order():
     pts = np.random.default_rng(11).uniform(-3, 3, size=(200, 3)).astype(np.float32)
     t = lb.build(pts)
