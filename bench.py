@@ -37,6 +37,12 @@ import time
 
 import numpy as np
 
+# This image sets NCCL_DEBUG=VERSION, which makes NCCL print "NCCL version ..."
+# to stdout at communicator init; stdout must carry only the one JSON line, so
+# that setting (and only that one) is dropped before torch loads NCCL.
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    del os.environ["NCCL_DEBUG"]
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
