@@ -25,7 +25,14 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream() -> int:
+    """cudaStream_t of torch's current stream (the raw getter skips building a
+    Stream object: this is on every call's host path)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 

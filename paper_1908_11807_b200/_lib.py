@@ -169,12 +169,21 @@ def load_library(path: str = LIB_PATH):
         return lib
 
 
+_CUDA_OK = False
+
+
 def lib():
-    """The library, after asserting a CUDA device is present."""
+    """The library, after asserting a CUDA device is present (checked once:
+    this sits on every query call's host path)."""
+    global _CUDA_OK
+    if _CUDA_OK and _lib is not None:
+        return _lib
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1908_11807_b200 needs a CUDA device (sm_100a); "
                            "there is no CPU fallback")
-    return load_library()
+    l = load_library()
+    _CUDA_OK = True
+    return l
 
 
 def check(rc: int) -> None:
