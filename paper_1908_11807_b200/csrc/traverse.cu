@@ -741,6 +741,57 @@ int spatial_1p(const lbvh_tree *t, const float *centers, const float *radii, flo
                                    cap, nullptr, status, stream);
 }
 
+// Warp-cooperative compaction (LBVH_COMPACT_WARP): a warp takes 32 rows,
+// scans their hit counts and writes the concatenation with consecutive lanes
+// on consecutive output words (element e of the warp's run belongs to the row
+// found by a 5-step shuffle search of the scan).  Rows that overflowed their
+// buffer count 0 here (the fill pass writes them).
+#ifndef LBVH_COMPACT_WARP
+#define LBVH_COMPACT_WARP 1  // radius 2P at C2: 5.51 vs 5.88 ms; ~30 hits/query: 10.8 vs 12.1
+#endif
+__global__ void __launch_bounds__(256)
+compact_warp_kernel(const int32_t *__restrict__ buf, int64_t cap,
+                    const int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
+                    int64_t nq, int32_t *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * 32 < nq;
+         w += warps) {
+        const int64_t q = w * 32 + lane;
+        int32_t cnt = 0;
+        int64_t dst = 0;
+        if (q < nq) {
+            cnt = __ldg(counts + q);
+            cnt = cnt <= cap ? cnt : 0;
+            dst = __ldg(offsets + q);
+        }
+        int32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const int32_t excl = incl - cnt;
+        for (int32_t base = 0; base < total; base += 32) {
+            const int32_t e = base + lane;
+            // row r: the last lane whose exclusive prefix is <= e
+            int r = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int32_t pre = __shfl_sync(0xFFFFFFFFu, excl, r + step);
+                if (pre <= e) r += step;
+            }
+            const int32_t pre_r = __shfl_sync(0xFFFFFFFFu, excl, r);
+            const int64_t dst_r = __shfl_sync(0xFFFFFFFFu, dst, r);
+            if (e < total) {
+                const int32_t j = e - pre_r;
+                out[dst_r + j] = __ldcs(buf + (w * 32 + r) * cap + j);
+            }
+        }
+    }
+}
+
 int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_t *offsets,
             int64_t nq, int32_t *out, cudaStream_t stream) {
     if (nq < 0 || cap < 1) return LBVH_ERR_INVALID_ARG;
@@ -748,7 +799,10 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
     if (!buf || !counts || !offsets) return LBVH_ERR_INVALID_ARG;
     unsigned g = div_up(nq, 256);
     g = g < kNumSMs * 8 ? g : kNumSMs * 8;
-    compact_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
+    if (LBVH_COMPACT_WARP)
+        compact_warp_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
+    else
+        compact_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
     count_launches(1);
     return check_launch();
 }
