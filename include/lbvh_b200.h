@@ -76,9 +76,6 @@ typedef struct lbvh_tree {
     int32_t leaf_dir_bits;
     /* LBVH_TREE_* bits describing how the tree was built (0 = unknown). */
     int32_t flags;
-    /* Optional (n-1) x 128 B 4-wide records (lbvh_wide_records); used by
-     * lbvh_knn on LBVH_TREE_CODES30 trees. */
-    const void *nodes4;
 } lbvh_tree;
 
 /* Every leaf box is a point (built from (n, 3) input: maxs == mins). */
@@ -113,6 +110,15 @@ size_t lbvh_sort_workspace_bytes(int64_t n);
  * Outputs: node_mins/node_maxs (2n-1)x3, left/right (n-1), leaf_obj n,
  * root_box 6 floats (== scene box), nodes (n-1) x 64 B, status word.
  * sorted_codes (optional, may be NULL): n u32 30-bit Morton codes in leaf order.
+ * leaf_dir (optional, may be NULL): the kNN seed's leaf directory over
+ * sorted_codes with leaf_dir_bits <= 24 ((1 << bits) + 1 u32, exactly what
+ * lbvh_leaf_directory writes), produced inside the hierarchy pass.
+ * flags: LBVH_BUILD_DEFER_ROWS leaves the reference-layout rows no query reads
+ * unwritten -- the internal rows of node_mins/node_maxs and, for point input
+ * (mins == maxs), the node_maxs leaf rows; lbvh_finish_rows writes them
+ * (bit-identical) when the caller first needs the reference layout.  The
+ * packed records, node_mins leaf rows, left/right and leaf_obj are always
+ * written.
  * morton_bits: 30 = the reference's codes (bit-exact tree); 63 = 21 bits per
  * axis, the same recipe (north_star "30/63-bit"; not in the reference, so
  * its parity is pinned only by the oracle restatement).  Leaves are then
@@ -121,7 +127,14 @@ size_t lbvh_sort_workspace_bytes(int64_t n);
 int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
                void *workspace, size_t workspace_bytes, float *node_mins, float *node_maxs,
                int32_t *left, int32_t *right, int32_t *leaf_obj, float *root_box,
-               void *nodes, uint32_t *sorted_codes, uint32_t *status, void *stream);
+               void *nodes, uint32_t *sorted_codes, uint32_t *leaf_dir, int leaf_dir_bits,
+               int flags, uint32_t *status, void *stream);
+#define LBVH_BUILD_DEFER_ROWS 0x1
+
+/* The rows an LBVH_BUILD_DEFER_ROWS build left out (internal rows from the
+ * packed records with the refit's left-first fold; node_maxs leaf rows copied
+ * from node_mins when tree->flags has LBVH_TREE_POINT_LEAVES). */
+int lbvh_finish_rows(const lbvh_tree *tree, float *node_mins, float *node_maxs, void *stream);
 
 /* Leaf directory over the build's sorted 30-bit leaf codes (kNN seed index;
  * no reference counterpart).  lbvh_leaf_directory_bits(n) is the bucket
@@ -129,12 +142,6 @@ int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
 int lbvh_leaf_directory_bits(int64_t n);
 int lbvh_leaf_directory(const uint32_t *leaf_codes, int64_t n, int bits, uint32_t *dir,
                         void *stream);
-
-/* 4-wide kNN records of a built tree (n >= 2): record X holds, for each
- * child C of internal node X, C itself if it is a leaf, else C's two
- * children (boxes SoA + links), 128 B per internal node.  Layout only: kNN
- * results are unchanged (no reference counterpart). */
-int lbvh_wide_records(const lbvh_tree *tree, void *nodes4, void *stream);
 
 /* morton_codes(points, scene_min, scene_max)   replaces morton.py:68-91
  * points n x 3 f64 (device); scene bounds host doubles (smin[3], smax[3]). */
@@ -257,9 +264,8 @@ int lbvh_knn_offsets(const int64_t *ks, int64_t k, int64_t n, int64_t nq, int64_
  * span starts instead of reading them (the offsets array is still read by
  * the other paths and must hold the same values). */
 #define LBVH_KNN_UNIFORM_SPANS 0x2
-/* workspace (optional, lbvh_knn_workspace_bytes(nq)): enables the persistent
- * kernel with per-lane query refill and a separate seed pass; without it
- * the one-thread-per-query kernel runs.  Results are identical. */
+/* workspace: reserved for future variants; accepted and unused today
+ * (lbvh_knn_workspace_bytes returns 0; NULL / 0 is valid). */
 size_t lbvh_knn_workspace_bytes(int64_t nq);
 int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
              const uint32_t *query_codes, int64_t nq, const int64_t *offsets,

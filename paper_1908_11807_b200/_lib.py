@@ -26,6 +26,7 @@ FLAG_BAD_RADIUS = 0x10
 FLAG_BAD_K = 0x20
 FLAG_BAD_TREE = 0x40
 NODE_BYTES = 64
+BUILD_DEFER_ROWS = 0x1
 KNN_SQUARED = 0x1
 MAX_ITEMS = (1 << 30) - 1
 
@@ -46,7 +47,7 @@ class CTree(ctypes.Structure):
                 ("leaf_obj", ctypes.c_void_p), ("nodes", ctypes.c_void_p),
                 ("root_box", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p),
                 ("leaf_dir", ctypes.c_void_p), ("leaf_dir_bits", ctypes.c_int32),
-                ("flags", ctypes.c_int32), ("nodes4", ctypes.c_void_p)]
+                ("flags", ctypes.c_int32)]
 
 TREE_POINT_LEAVES = 0x1
 TREE_CODES30 = 0x2
@@ -57,8 +58,6 @@ _SIGS = {
     "lbvh_last_cuda_error": ([], ctypes.c_char_p),
     "lbvh_abi_version": ([], ctypes.c_int),
     "lbvh_leaf_directory_bits": ([ctypes.c_int64], ctypes.c_int),
-    "lbvh_wide_records": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p],
-                          ctypes.c_int),
     "lbvh_leaf_directory": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                              ctypes.c_void_p], ctypes.c_int),
     "lbvh_launch_count": ([], ctypes.c_uint64),
@@ -68,7 +67,10 @@ _SIGS = {
     "lbvh_query_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_scan_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_build": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
-                    ctypes.c_void_p, ctypes.c_size_t] + [ctypes.c_void_p] * 10, ctypes.c_int),
+                    ctypes.c_void_p, ctypes.c_size_t] + [ctypes.c_void_p] * 9
+                   + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_finish_rows": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
+                          ctypes.c_void_p], ctypes.c_int),
     "lbvh_morton_codes": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_sort_pairs": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,

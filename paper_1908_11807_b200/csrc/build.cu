@@ -25,17 +25,6 @@ namespace {
 
 constexpr int kReduceThreads = 256;
 
-#ifndef LBVH_HIER_PAIRS
-#define LBVH_HIER_PAIRS 0
-#endif
-// Release-only exchange + strong relaxed sibling loads measured 6% faster
-// builds than acq_rel (no CCTL.IVALL of the SM's L1 on every handshake).
-// The sibling loads' addresses depend on the exchange result, so they issue
-// only after it returns and read the released rows at L2.
-#ifndef LBVH_HIER_ACQREL
-#define LBVH_HIER_ACQREL 0
-#endif
-
 __device__ __forceinline__ void warp_minmax(float v[6]) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -216,80 +205,43 @@ __device__ __forceinline__ void store_packed(PackedNode *nodes, int64_t id, cons
     __stcg(&p->d, make_int4(lc, rc, 0, 0));
 }
 
-// K4 + K5.  WITH_BOXES=false is the topology-only variant behind
-// lbvh_generate_topology (sorted codes in, left/right/parent out).
 // leaf_codes (optional): the 30-bit code of every leaf in leaf order (for
 // 63-bit codes the top 30 bits, which are exactly the 30-bit code).
 __device__ __forceinline__ uint32_t code30(uint32_t c) { return c; }
 __device__ __forceinline__ uint32_t code30(uint64_t c) { return (uint32_t)(c >> 33); }
 
-template <bool WITH_BOXES, bool ROWS_LATE = false, typename CodeT = uint32_t>
+// Split prefix of adjacent keys (a, i), (b, i+1): delta() on staged codes.
+__device__ __forceinline__ int delta_of(uint32_t a, uint32_t b, int64_t i) {
+    if (a != b) return __clz(a ^ b);
+    return 32 + __clz((uint32_t)i ^ (uint32_t)(i + 1));
+}
+__device__ __forceinline__ int delta_of(uint64_t a, uint64_t b, int64_t i) {
+    if (a != b) return __clzll(a ^ b);
+    return 64 + __clz((uint32_t)i ^ (uint32_t)(i + 1));
+}
+
+// Topology only (lbvh_generate_topology, generate_topology tree.py:85-105):
+// the bottom-up construction of the build without boxes -- sorted codes in,
+// Karras left/right/parent out.  The handshake carries no data besides the
+// exchanged range end, so a release-only exchange suffices.
 __global__ void __launch_bounds__(256)
-hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
-                 const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
-                 uint32_t *slots, float *node_mins, float *node_maxs, int32_t *__restrict__ left,
-                 int32_t *__restrict__ right, int32_t *__restrict__ parent,
-                 int32_t *__restrict__ leaf_obj, PackedNode *__restrict__ nodes,
-                 float *__restrict__ root_box, uint32_t *__restrict__ leaf_codes) {
+topology_kernel(const uint32_t *__restrict__ codes, int64_t n, uint32_t *slots,
+                int32_t *__restrict__ left, int32_t *__restrict__ right,
+                int32_t *__restrict__ parent) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const int64_t internal = n - 1;
-    Box mine;
-    int32_t my_link = 0;  // packed-layout link of the current node
-    if (leaf_codes) leaf_codes[p] = code30(__ldg(codes + p));
-    if (WITH_BOXES) {
-        const uint32_t obj = __ldg(perm + p);
-        leaf_obj[p] = (int32_t)obj;
-        const bool same = (mins == maxs);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            mine.lo[a] = __ldg(mins + 3 * (int64_t)obj + a);
-            mine.hi[a] = same ? mine.lo[a] : __ldg(maxs + 3 * (int64_t)obj + a);
-        }
-        store_box(node_mins, node_maxs, internal + p, mine);
-        my_link = (int32_t)(obj | kLeafTag);
-        if (n == 1) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                root_box[a] = mine.lo[a];
-                root_box[3 + a] = mine.hi[a];
-            }
-            return;
-        }
-    } else if (n == 1) {
-        if (parent) parent[0] = -1;
+    if (n == 1) {
+        parent[0] = -1;
         return;
     }
+    const int64_t internal = n - 1;
     int64_t l = p, r = p;
     bool left_side = is_left_child(codes, n, l, r);
-    // Leaf pairs: when leaf p is a left child and leaf p+1 a right child,
-    // their parent [p, p+1] has two leaf children; thread p builds it
-    // without the slot handshake (the sibling box comes straight from the
-    // input rows) and thread p+1 stops here.  About a third of the internal
-    // nodes are such pairs, so a third of the exchanges and fences go away.
-    bool pair = false;
-    if (WITH_BOXES && LBVH_HIER_PAIRS) {
-        if (!left_side && is_left_child(codes, n, p - 1, p - 1)) return;  // p-1 builds it
-        pair = left_side && !is_left_child(codes, n, p + 1, p + 1);
-    }
     while (true) {
         const int64_t g = left_side ? r : l - 1;
         const uint32_t known = (uint32_t)(left_side ? l : r);
-        uint32_t other;
-        if (WITH_BOXES && LBVH_HIER_PAIRS && pair) {
-            other = (uint32_t)(p + 2);  // sibling range [p+1, p+1]
-        } else {
-            // The exchange releases this subtree's boxes to the sibling and
-            // (acq_rel) acquires the sibling's when we arrive second.
-#if LBVH_HIER_ACQREL
-            other = atomic_exch_acq_rel(slots + g, known + 1u);
-#else
-            // release only: the second arrival reads the sibling's rows with
-            // L2 (.cg) loads whose addresses depend on the exchange result
-            other = atomic_exch_release(slots + g, known + 1u);
-#endif
-            if (other == 0) return;  // first arrival: sibling subtree not done
-        }
+        const uint32_t other = atomic_exch_release(slots + g, known + 1u);
+        if (other == 0) return;  // first arrival: sibling subtree not done
         const int64_t pl = left_side ? l : (int64_t)(other - 1u);
         const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
         const int64_t lc = (pl == g) ? internal + g : g;
@@ -299,69 +251,12 @@ hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ p
         const int64_t pid = root ? 0 : (parent_left ? pr : pl);
         left[pid] = (int32_t)lc;
         right[pid] = (int32_t)rc;
-        if (parent) {
-            parent[lc] = (int32_t)pid;
-            parent[rc] = (int32_t)pid;
-            if (root) parent[0] = -1;
+        parent[lc] = (int32_t)pid;
+        parent[rc] = (int32_t)pid;
+        if (root) {
+            parent[0] = -1;
+            return;
         }
-        if (WITH_BOXES) {
-            const int64_t sib = left_side ? rc : lc;
-            Box sb;
-            if (ROWS_LATE && sib < internal) {
-                // sibling box = union of its children, from its packed record
-                // (written before its release); same left-first fold as below
-                const PackedNode *sp = nodes + sib;
-                const float4 a = ld_relaxed(&sp->a), b = ld_relaxed(&sp->b),
-                             c = ld_relaxed(&sp->c);
-                sb.lo[0] = min_left(a.x, b.z); sb.lo[1] = min_left(a.y, b.w);
-                sb.lo[2] = min_left(a.z, c.x);
-                sb.hi[0] = max_left(a.w, c.y); sb.hi[1] = max_left(b.x, c.z);
-                sb.hi[2] = max_left(b.y, c.w);
-            } else if (WITH_BOXES && LBVH_HIER_PAIRS && pair) {
-                // leaf p+1's box from the input rows (its own row is being
-                // written concurrently by thread p+1)
-                const uint32_t so = __ldg(perm + p + 1);
-                const bool same = (mins == maxs);
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    sb.lo[a] = __ldg(mins + 3 * (int64_t)so + a);
-                    sb.hi[a] = same ? sb.lo[a] : __ldg(maxs + 3 * (int64_t)so + a);
-                }
-            } else {
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    sb.lo[a] = ld_relaxed(node_mins + 3 * sib + a);
-                    sb.hi[a] = ld_relaxed(node_maxs + 3 * sib + a);
-                }
-            }
-            pair = false;
-            int32_t sib_link;
-            if (sib >= internal)
-                sib_link = (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
-            else
-                sib_link = (int32_t)sib;
-            const Box &L = left_side ? mine : sb;
-            const Box &R = left_side ? sb : mine;
-            Box P;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                P.lo[a] = min_left(L.lo[a], R.lo[a]);
-                P.hi[a] = max_left(L.hi[a], R.hi[a]);
-            }
-            store_packed(nodes, pid, L, R, left_side ? my_link : sib_link,
-                         left_side ? sib_link : my_link);
-            if (!ROWS_LATE) store_box(node_mins, node_maxs, pid, P);
-            mine = P;
-            my_link = (int32_t)pid;
-            if (root) {
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    root_box[a] = P.lo[a];
-                    root_box[3 + a] = P.hi[a];
-                }
-            }
-        }
-        if (root) return;
         l = pl;
         r = pr;
         left_side = parent_left;
@@ -369,9 +264,8 @@ hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ p
 }
 
 // ---------------------------------------------------------------------------
-// Two-level hierarchy (K4+K5, default): the same bottom-up construction and
-// Karras ordinals as hierarchy_kernel, split by where the two children of a
-// node meet.
+// Hierarchy (K4+K5): Apetrei's bottom-up construction emitting Karras
+// ordinals, in two levels split by where the two children of a node meet.
 //
 // hierarchy_local_kernel: CTA c owns leaves [B, E].  A thread climbs while the
 // split slot g of its node satisfies B <= g < E, i.e. both children of the
@@ -380,53 +274,70 @@ hierarchy_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ p
 // global atomics, no fences.  A node whose slot leaves the CTA is appended to
 // the frontier list; a first arrival whose partner never came (the sibling
 // subtree crosses the CTA edge) is copied to the global slot array at the end.
+// The CTA's codes are staged once in shared memory (coalesced) and the split
+// prefixes delta(i), i in [B-1, E], computed from them, so the climb and the
+// leaf directory read no global codes.
 //
-// hierarchy_frontier_kernel: the frontier nodes continue with the global
-// release handshake of hierarchy_kernel.  A kernel-A first arrival is then
+// hierarchy_frontier_kernel: the frontier nodes continue with a global
+// handshake (release exchange; the second arrival fences acq_rel before it
+// reads the sibling's record).  A local-kernel first arrival is then
 // indistinguishable from a global one, so the meeting rule is unchanged.
+// It also writes the leaf-directory runs the local kernel deferred.
 // ---------------------------------------------------------------------------
-#ifndef LBVH_HIER_T
-#define LBVH_HIER_T 256
-#endif
-#ifndef LBVH_HIER_MINBLOCKS
-#define LBVH_HIER_MINBLOCKS 1
-#endif
-constexpr int kHierT = LBVH_HIER_T;
-// 1: the local kernel computes the split prefixes delta(i), i in [B-1, E], once
-// (coalesced code loads) into shared memory and climbs on those.
-#ifndef LBVH_HIER_SDELTA
-#define LBVH_HIER_SDELTA 1  // build at 1e7: 1.46 vs 1.54 ms
-#endif
+constexpr int kHierT = 256;
+// Leaf-directory runs longer than this (empty buckets between two adjacent
+// leaves: clustered clouds) are deferred to the frontier kernel, where the
+// whole grid writes them.
+constexpr int64_t kDirInline = 32;
+
+struct DirRun {
+    uint32_t lo, hi, value, pad;  // dir[lo, hi) = value
+};
+
+__device__ __forceinline__ void dir_run(uint32_t *__restrict__ dir, int64_t lo, int64_t hi,
+                                        uint32_t value, DirRun *runs, uint32_t *run_count) {
+    if (hi - lo <= kDirInline) {
+        for (int64_t b = lo; b < hi; ++b) dir[b] = value;
+    } else {
+        const uint32_t at = atomicAdd(run_count, 1u);
+        runs[at] = DirRun{(uint32_t)lo, (uint32_t)hi, value, 0u};
+    }
+}
 
 template <typename CodeT>
-__global__ void __launch_bounds__(kHierT, LBVH_HIER_MINBLOCKS)
+__global__ void __launch_bounds__(kHierT)
 hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
                        const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
                        uint32_t *__restrict__ slots, float *__restrict__ node_mins,
-                       float *__restrict__ node_maxs, int32_t *__restrict__ left,
-                       int32_t *__restrict__ right, int32_t *__restrict__ leaf_obj,
-                       PackedNode *__restrict__ nodes, float *__restrict__ root_box,
-                       uint32_t *__restrict__ leaf_codes, uint2 *__restrict__ frontier,
+                       float *__restrict__ node_maxs, bool leaf_maxs_rows,
+                       int32_t *__restrict__ left, int32_t *__restrict__ right,
+                       int32_t *__restrict__ leaf_obj, PackedNode *__restrict__ nodes,
+                       float *__restrict__ root_box, uint32_t *__restrict__ leaf_codes,
+                       uint32_t *__restrict__ leaf_dir, int dir_bits, DirRun *runs,
+                       uint32_t *run_count, uint2 *__restrict__ frontier,
                        uint32_t *frontier_count) {
     __shared__ uint32_t s_slot[kHierT];
     __shared__ float s_box[2][6][kHierT];
     __shared__ int32_t s_link[2][kHierT];
-    __shared__ uint8_t s_delta[LBVH_HIER_SDELTA ? kHierT + 1 : 1];  // delta(B - 1 + i)
+    __shared__ CodeT s_code[kHierT + 2];     // codes[B - 1 + i]
+    __shared__ uint8_t s_delta[kHierT + 1];  // delta(B - 1 + i)
     const int tid = threadIdx.x;
     const int64_t B = (int64_t)blockIdx.x * kHierT;
     const int64_t E = (B + kHierT < n ? B + kHierT : n) - 1;
     const int64_t p = B + tid;
     const int64_t internal = n - 1;
     s_slot[tid] = 0;
-    if (LBVH_HIER_SDELTA) {
-        if (p < n - 1) s_delta[tid + 1] = (uint8_t)delta(codes, p);
-        if (tid == 0 && B > 0) s_delta[0] = (uint8_t)delta(codes, B - 1);
+    for (int i = tid; i < kHierT + 2; i += kHierT) {
+        const int64_t j = B - 1 + i;
+        if (j >= 0 && j < n) s_code[i] = __ldg(codes + j);
     }
+    __syncthreads();
+    if (p < n - 1) s_delta[tid + 1] = (uint8_t)delta_of(s_code[tid + 1], s_code[tid + 2], p);
+    if (tid == 0 && B > 0) s_delta[0] = (uint8_t)delta_of(s_code[0], s_code[1], B - 1);
     __syncthreads();
     // is_left_child over the CTA's range: l >= B and r <= E, so both prefixes
     // delta(r) and delta(l - 1) are in s_delta
     auto left_child = [&](int64_t l, int64_t r) -> bool {
-        if (!LBVH_HIER_SDELTA) return is_left_child(codes, n, l, r);
         if (l == 0) return true;
         if (r == n - 1) return false;
         return s_delta[r - B + 1] > s_delta[l - B];
@@ -436,7 +347,19 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     int32_t my_link = 0;
     int64_t l = p, r = p;
     if (active) {
-        if (leaf_codes) leaf_codes[p] = code30(__ldg(codes + p));
+        const uint32_t c30 = code30(s_code[tid + 1]);
+        if (leaf_codes) leaf_codes[p] = c30;
+        if (leaf_dir) {
+            // dir[b] = first leaf whose code >> (30 - bits) >= b: leaf p owns
+            // the buckets after its predecessor's, the last leaf the tail = n
+            const int sh = 30 - dir_bits;
+            const int64_t cb = (int64_t)(c30 >> sh);
+            const int64_t pb = p == 0 ? -1 : (int64_t)(code30(s_code[tid]) >> sh);
+            dir_run(leaf_dir, pb + 1, cb + 1, (uint32_t)p, runs, run_count);
+            if (p == n - 1)
+                dir_run(leaf_dir, cb + 1, ((int64_t)1 << dir_bits) + 1, (uint32_t)n, runs,
+                        run_count);
+        }
         const uint32_t obj = __ldg(perm + p);
         leaf_obj[p] = (int32_t)obj;
         const bool same = (mins == maxs);
@@ -445,8 +368,20 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
             mine.lo[a] = __ldg(mins + 3 * (int64_t)obj + a);
             mine.hi[a] = same ? mine.lo[a] : __ldg(maxs + 3 * (int64_t)obj + a);
         }
-        store_box(node_mins, node_maxs, internal + p, mine);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            node_mins[3 * (internal + p) + a] = mine.lo[a];
+            if (leaf_maxs_rows) node_maxs[3 * (internal + p) + a] = mine.hi[a];
+        }
         my_link = (int32_t)(obj | kLeafTag);
+        if (n == 1) {  // leaf-only tree (tree.py:177-209 with n == 1)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                root_box[a] = mine.lo[a];
+                root_box[3 + a] = mine.hi[a];
+            }
+            active = false;
+        }
     }
     while (active) {
         const bool left_side = left_child(l, r);
@@ -519,44 +454,74 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     if (v) slots[B + tid] = v;
 }
 
+// Box of a node the local kernel (or an earlier frontier step) finished:
+// a leaf's row, or the union of an internal node's packed child boxes
+// (same left-first fold as the refit).  Strong loads: written by other CTAs.
+__device__ __forceinline__ void frontier_box(const PackedNode *nodes, const float *node_mins,
+                                             const float *node_maxs, bool leaf_maxs_rows,
+                                             int64_t internal, int64_t id, Box &b) {
+    if (id < internal) {
+        const PackedNode *pn = nodes + id;
+        const float4 a = ld_relaxed(&pn->a), c = ld_relaxed(&pn->b), e = ld_relaxed(&pn->c);
+        b.lo[0] = min_left(a.x, c.z); b.lo[1] = min_left(a.y, c.w);
+        b.lo[2] = min_left(a.z, e.x);
+        b.hi[0] = max_left(a.w, e.y); b.hi[1] = max_left(c.x, e.z);
+        b.hi[2] = max_left(c.y, e.w);
+    } else {
+        const float *hi = leaf_maxs_rows ? node_maxs : node_mins;  // point leaves: hi == lo
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            b.lo[a] = ld_relaxed(node_mins + 3 * id + a);
+            b.hi[a] = ld_relaxed(hi + 3 * id + a);
+        }
+    }
+}
+
 template <typename CodeT>
 __global__ void __launch_bounds__(256)
 hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
-                          int64_t n, uint32_t *slots, float *node_mins, float *node_maxs,
+                          int64_t n, uint32_t *slots, const float *node_mins,
+                          const float *node_maxs, bool leaf_maxs_rows,
                           int32_t *__restrict__ left, int32_t *__restrict__ right,
-                          PackedNode *__restrict__ nodes, float *__restrict__ root_box,
-                          const uint2 *__restrict__ frontier, const uint32_t *frontier_count) {
+                          PackedNode *nodes, float *__restrict__ root_box,
+                          const uint2 *__restrict__ frontier, const uint32_t *frontier_count,
+                          uint32_t *__restrict__ leaf_dir, const DirRun *__restrict__ runs,
+                          const uint32_t *run_count) {
     const int64_t internal = n - 1;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (leaf_dir) {  // long leaf-directory runs, written by the whole grid
+        const uint32_t nr = *run_count;
+        for (uint32_t k = 0; k < nr; ++k) {
+            const DirRun e = runs[k];
+            for (int64_t b = e.lo + tid; b < (int64_t)e.hi; b += stride) leaf_dir[b] = e.value;
+        }
+    }
     const int64_t count = (int64_t)*frontier_count;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = tid; i < count; i += stride) {
         const uint2 e = frontier[i];
         int64_t l = e.x, r = e.y;
         Box mine;
         int32_t my_link;
         if (l == r) {  // a leaf (row written by the local kernel)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                mine.lo[a] = ld_relaxed(node_mins + 3 * (internal + l) + a);
-                mine.hi[a] = ld_relaxed(node_maxs + 3 * (internal + l) + a);
-            }
+            frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, internal + l,
+                         mine);
             my_link = (int32_t)(__ldg(perm + l) | kLeafTag);
         } else {       // an internal node built by the local kernel
             const int64_t id = is_left_child(codes, n, l, r) ? r : l;
-            const PackedNode *pn = nodes + id;
-            const float4 a = ld_relaxed(&pn->a), b = ld_relaxed(&pn->b), c = ld_relaxed(&pn->c);
-            mine.lo[0] = min_left(a.x, b.z); mine.lo[1] = min_left(a.y, b.w);
-            mine.lo[2] = min_left(a.z, c.x);
-            mine.hi[0] = max_left(a.w, c.y); mine.hi[1] = max_left(b.x, c.z);
-            mine.hi[2] = max_left(b.y, c.w);
+            frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, id, mine);
             my_link = (int32_t)id;
         }
         bool left_side = is_left_child(codes, n, l, r);
         while (true) {
             const int64_t g = left_side ? r : l - 1;
             const uint32_t known = (uint32_t)(left_side ? l : r);
+            // release: this subtree's record is visible to whoever arrives second
             const uint32_t other = atomic_exch_release(slots + g, known + 1u);
             if (other == 0) break;  // first arrival: sibling subtree not done
+            // second arrival: the exchange read the partner's release; the
+            // fence completes the acquire pattern before its record is read
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             const int64_t pl = left_side ? l : (int64_t)(other - 1u);
             const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
             const int64_t lc = (pl == g) ? internal + g : g;
@@ -568,24 +533,10 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__res
             right[pid] = (int32_t)rc;
             const int64_t sib = left_side ? rc : lc;
             Box sb;
-            int32_t sib_link;
-            if (sib < internal) {
-                const PackedNode *sp = nodes + sib;
-                const float4 a = ld_relaxed(&sp->a), b = ld_relaxed(&sp->b),
-                             c = ld_relaxed(&sp->c);
-                sb.lo[0] = min_left(a.x, b.z); sb.lo[1] = min_left(a.y, b.w);
-                sb.lo[2] = min_left(a.z, c.x);
-                sb.hi[0] = max_left(a.w, c.y); sb.hi[1] = max_left(b.x, c.z);
-                sb.hi[2] = max_left(b.y, c.w);
-                sib_link = (int32_t)sib;
-            } else {
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    sb.lo[a] = ld_relaxed(node_mins + 3 * sib + a);
-                    sb.hi[a] = ld_relaxed(node_maxs + 3 * sib + a);
-                }
-                sib_link = (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
-            }
+            frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, sib, sb);
+            const int32_t sib_link = sib < internal
+                                         ? (int32_t)sib
+                                         : (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
             const Box &L = left_side ? mine : sb;
             const Box &R = left_side ? sb : mine;
             Box P;
@@ -613,15 +564,16 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__res
     }
 }
 
-// Reference-layout rows of the internal nodes, written after the hierarchy
-// pass: row i = union of the two child boxes in packed record i, folded with
-// the refit's left-first rule (identical bits to an in-pass write).  Thread i
-// reads record i and writes row i: fully coalesced.
+// Reference-layout rows the build defers (LBVH_BUILD_DEFER_ROWS): internal
+// row i = union of the two child boxes in packed record i, folded with the
+// refit's left-first rule (identical bits to an in-pass write), and for
+// point leaves the node_maxs leaf rows (== node_mins rows).  Coalesced.
 __global__ void __launch_bounds__(256)
-internal_rows_kernel(const PackedNode *__restrict__ nodes, int64_t n_internal,
-                     float *__restrict__ node_mins, float *__restrict__ node_maxs) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_internal;
-         i += (int64_t)gridDim.x * blockDim.x) {
+finish_rows_kernel(const PackedNode *__restrict__ nodes, int64_t n, bool copy_leaf_maxs,
+                   float *__restrict__ node_mins, float *__restrict__ node_maxs) {
+    const int64_t n_internal = n - 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_internal; i += stride) {
         const PackedNode *p = nodes + i;
         const float4 a = __ldcs(&p->a), b = __ldcs(&p->b), c = __ldcs(&p->c);
         node_mins[3 * i] = min_left(a.x, b.z);
@@ -631,6 +583,9 @@ internal_rows_kernel(const PackedNode *__restrict__ nodes, int64_t n_internal,
         node_maxs[3 * i + 1] = max_left(b.x, c.z);
         node_maxs[3 * i + 2] = max_left(b.y, c.w);
     }
+    if (copy_leaf_maxs)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n; i += stride)
+            node_maxs[3 * n_internal + i] = __ldcs(node_mins + 3 * n_internal + i);
 }
 
 // Atomic-flag refit over an arbitrary (left, right, parent) topology --
@@ -745,13 +700,17 @@ unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
 
 // ----------------------------------------------------------------- host API
 
+constexpr int kDirBitsMax = 24;
+constexpr size_t kDirRunsMax = (((size_t)1 << kDirBitsMax) + 1) / (kDirInline + 1) + 2;
+
 size_t build_workspace_bytes(int64_t n) {
     // sized for the wider (63-bit) pipeline so one size serves both
     size_t b = 0;
     b += align_up(sizeof(uint64_t) * (size_t)n) + align_up(sizeof(uint32_t) * (size_t)n);
     b += align_up(sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1));  // handshake slots
+    b += align_up(sizeof(uint32_t) * 4);                         // counters
     b += align_up(sizeof(float) * 6 * kNumSMs * 8);              // reduce partials
-    b += align_up(sizeof(uint32_t) * 4);                         // reduce counter
+    b += align_up(sizeof(DirRun) * kDirRunsMax);                 // long directory runs
     size_t s32 = sort_workspace_bytes(n), s64 = sort64_workspace_bytes(n);
     b += s32 > s64 ? s32 : s64;
     return b + 1024;
@@ -769,15 +728,17 @@ template <typename CodeT>
 int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
                float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
                int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
-               uint32_t *status, cudaStream_t stream) {
+               uint32_t *leaf_dir, int dir_bits, int flags, uint32_t *status,
+               cudaStream_t stream) {
     Carve c(ws, ws_bytes);
     CodeT *codes = c.take<CodeT>(n);
     uint32_t *perm = c.take<uint32_t>(n);
     size_t zero_begin = align_up(c.off);
     uint32_t *slots = c.take<uint32_t>(n > 1 ? n - 1 : 1);
-    uint32_t *counter = c.take<uint32_t>(4);
+    uint32_t *counter = c.take<uint32_t>(4);  // reduce CTAs, -, frontier, directory runs
     size_t zero_end = c.off;
     float *partials = c.take<float>(6 * kNumSMs * 8);
+    DirRun *runs = c.take<DirRun>(kDirRunsMax);
     void *sort_ws = c.take<char>(sizeof(CodeT) == 4 ? sort_workspace_bytes(n)
                                                     : sort64_workspace_bytes(n));
     if (!c.ok()) return LBVH_ERR_WORKSPACE;
@@ -791,34 +752,23 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
     count_launches(2);
     int rc = sort_codes(codes, perm, n, sort_ws, stream);
     if (rc != LBVH_OK) return rc;
-    // 1 (measured 15% faster at 1e7): sibling boxes from packed records,
-    // internal reference rows in a separate coalesced pass.
-    static const int rows_late = env_int("LBVH_BUILD_ROWS_LATE", 1);
-    static const int two_level = env_int("LBVH_BUILD_TWO_LEVEL", 1);
-    if (two_level && n > 1) {
-        // the sort's ping-pong buffers are dead now: frontier list lives there
-        uint2 *frontier = reinterpret_cast<uint2 *>(sort_ws);
-        uint32_t *fcount = counter + 2;
-        hierarchy_local_kernel<CodeT><<<div_up(n, kHierT), kHierT, 0, stream>>>(
-            codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, leaf_obj,
-            (PackedNode *)nodes, root_box, sorted_codes, frontier, fcount);
-        hierarchy_frontier_kernel<CodeT><<<grid_for(n / 64 + 1, 256, 8), 256, 0, stream>>>(
-            codes, perm, n, slots, node_mins, node_maxs, left, right, (PackedNode *)nodes,
-            root_box, frontier, fcount);
-        internal_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
-            (const PackedNode *)nodes, n - 1, node_mins, node_maxs);
-        count_launches(3);
-    } else if (rows_late && n > 1) {
-        hierarchy_kernel<true, true, CodeT><<<div_up(n, 256), 256, 0, stream>>>(
-            codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-            leaf_obj, (PackedNode *)nodes, root_box, sorted_codes);
-        internal_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
-            (const PackedNode *)nodes, n - 1, node_mins, node_maxs);
-        count_launches(2);
-    } else {
-        hierarchy_kernel<true, false, CodeT><<<div_up(n, 256), 256, 0, stream>>>(
-            codes, perm, mins, maxs, n, slots, node_mins, node_maxs, left, right, nullptr,
-            leaf_obj, (PackedNode *)nodes, root_box, sorted_codes);
+    // point input with deferred rows: node_maxs leaf rows (== node_mins rows)
+    // are written by lbvh_finish_rows, the frontier reads node_mins for both
+    const bool defer = (flags & LBVH_BUILD_DEFER_ROWS) != 0;
+    const bool leaf_maxs_rows = !(defer && mins == maxs);
+    // the sort's ping-pong buffers are dead now: the frontier list lives there
+    uint2 *frontier = reinterpret_cast<uint2 *>(sort_ws);
+    hierarchy_local_kernel<CodeT><<<div_up(n, kHierT), kHierT, 0, stream>>>(
+        codes, perm, mins, maxs, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
+        leaf_obj, (PackedNode *)nodes, root_box, sorted_codes, leaf_dir, dir_bits, runs,
+        counter + 3, frontier, counter + 2);
+    hierarchy_frontier_kernel<CodeT><<<grid_for(n / 64 + 1, 256, 8), 256, 0, stream>>>(
+        codes, perm, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
+        (PackedNode *)nodes, root_box, frontier, counter + 2, leaf_dir, runs, counter + 3);
+    count_launches(2);
+    if (!defer && n > 1) {
+        finish_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(
+            (const PackedNode *)nodes, n, false, node_mins, node_maxs);
         count_launches(1);
     }
     return check_launch();
@@ -828,20 +778,35 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
 int build(const float *mins, const float *maxs, int64_t n, int morton_bits, void *ws,
           size_t ws_bytes, float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
           int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
-          uint32_t *status, cudaStream_t stream) {
+          uint32_t *leaf_dir, int leaf_dir_bits, int flags, uint32_t *status,
+          cudaStream_t stream) {
     if (n == 0) return LBVH_ERR_EMPTY_SCENE;
     if (n < 0 || !mins || !maxs || !node_mins || !node_maxs || !leaf_obj || !root_box ||
         !status || (morton_bits != 30 && morton_bits != 63))
         return LBVH_ERR_INVALID_ARG;
     if (n > 1 && (!left || !right || !nodes)) return LBVH_ERR_INVALID_ARG;
+    if (leaf_dir && (leaf_dir_bits < 0 || leaf_dir_bits > kDirBitsMax))
+        return LBVH_ERR_INVALID_ARG;
     if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     if (ws_bytes < build_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
     if (morton_bits == 63)
         return build_impl<uint64_t>(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left,
-                                    right, leaf_obj, root_box, nodes, sorted_codes, status,
-                                    stream);
+                                    right, leaf_obj, root_box, nodes, sorted_codes, leaf_dir,
+                                    leaf_dir_bits, flags, status, stream);
     return build_impl<uint32_t>(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left, right,
-                                leaf_obj, root_box, nodes, sorted_codes, status, stream);
+                                leaf_obj, root_box, nodes, sorted_codes, leaf_dir,
+                                leaf_dir_bits, flags, status, stream);
+}
+
+int finish_rows(const lbvh_tree *t, float *node_mins, float *node_maxs, cudaStream_t stream) {
+    if (!t || t->n < 1 || !node_mins || !node_maxs) return LBVH_ERR_INVALID_ARG;
+    if (t->n > 1 && !t->nodes) return LBVH_ERR_INVALID_ARG;
+    const bool leaves = (t->flags & LBVH_TREE_POINT_LEAVES) != 0;
+    if (t->n == 1 && !leaves) return LBVH_OK;
+    finish_rows_kernel<<<grid_for(3 * t->n, 256, 16), 256, 0, stream>>>(
+        (const PackedNode *)t->nodes, t->n, leaves, node_mins, node_maxs);
+    count_launches(1);
+    return check_launch();
 }
 
 size_t topology_workspace_bytes(int64_t n) {
@@ -856,9 +821,8 @@ int generate_topology(const uint32_t *codes, int64_t n, int32_t *left, int32_t *
     if (ws_bytes < topology_workspace_bytes(n)) return LBVH_ERR_WORKSPACE;
     uint32_t *slots = (uint32_t *)ws;
     cudaMemsetAsync(slots, 0, sizeof(uint32_t) * (size_t)(n > 1 ? n - 1 : 1), stream);
-    hierarchy_kernel<false><<<div_up(n, 256), 256, 0, stream>>>(
-        codes, nullptr, nullptr, nullptr, n, slots, nullptr, nullptr, left, right, parent,
-        nullptr, nullptr, nullptr, nullptr); count_launches(1);
+    topology_kernel<<<div_up(n, 256), 256, 0, stream>>>(codes, n, slots, left, right, parent);
+    count_launches(1);
     return check_launch();
 }
 
@@ -974,18 +938,15 @@ int query_order(const float *centers, int64_t nq, const float *scene, int order_
     Carve c(ws, ws_bytes);
     uint32_t *codes = sorted_codes ? sorted_codes : c.take<uint32_t>(nq);
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
-    static const int fast = env_int("LBVH_QUERY_MORTON_F32", 1);
     // odd pass counts: encode straight into the sort's ping-pong buffers so
     // the last pass writes (codes, order) -- no copy-back
     const bool odd = (sort_pass_count(30, 30 - order_bits) & 1) != 0;
     uint32_t *kin = codes, *vin = order;
     if (odd) sort_alt_buffers(sort_ws, sort_workspace_bytes(nq), nq, &kin, &vin);
-    if (fast || status || offsets)
-        query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, kin,
-                                                                      vin, status, offsets, span);
-    else
-        morton_kernel<uint32_t><<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, centers, nq,
-                                                                           scene, kin, vin);
+    // fp32 codes on the tree's grid: an ordering choice only (results never
+    // depend on it); query_sort_order keeps the exact f64 recipe
+    query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, kin, vin,
+                                                                  status, offsets, span);
     count_launches(1);
     int rc = odd ? sort_pairs_from_alt(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq),
                                        stream, 30 - order_bits)

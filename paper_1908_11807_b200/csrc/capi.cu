@@ -33,8 +33,9 @@ int check_launch() {
 // defined in build.cu / traverse.cu / scan.cu
 size_t build_workspace_bytes(int64_t n);
 int build(const float *, const float *, int64_t, int, void *, size_t, float *, float *,
-          int32_t *, int32_t *, int32_t *, float *, void *, uint32_t *, uint32_t *,
-          cudaStream_t);
+          int32_t *, int32_t *, int32_t *, float *, void *, uint32_t *, uint32_t *, int, int,
+          uint32_t *, cudaStream_t);
+int finish_rows(const lbvh_tree *, float *, float *, cudaStream_t);
 size_t topology_workspace_bytes(int64_t n);
 int generate_topology(const uint32_t *, int64_t, int32_t *, int32_t *, int32_t *, void *, size_t,
                       cudaStream_t);
@@ -62,7 +63,6 @@ int knn_offsets(const int64_t *, int64_t, int64_t, int64_t, int64_t *, int32_t *
                 void *, size_t, cudaStream_t);
 int leaf_directory(const uint32_t *, int64_t, int, uint32_t *, cudaStream_t);
 int morton_codes_f32(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
-int wide_records(const lbvh_tree *, void *, cudaStream_t);
 int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
         const int64_t *, int64_t, int32_t *, float *, int, void *, size_t, uint32_t *,
         cudaStream_t, float *);
@@ -111,9 +111,15 @@ size_t lbvh_scan_workspace_bytes(int64_t nq) { return scan_workspace_bytes(nq); 
 int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits, void *ws,
                size_t ws_bytes, float *node_mins, float *node_maxs, int32_t *left,
                int32_t *right, int32_t *leaf_obj, float *root_box, void *nodes,
-               uint32_t *sorted_codes, uint32_t *status, void *stream) {
+               uint32_t *sorted_codes, uint32_t *leaf_dir, int leaf_dir_bits, int flags,
+               uint32_t *status, void *stream) {
     return build(mins, maxs, n, morton_bits, ws, ws_bytes, node_mins, node_maxs, left, right,
-                 leaf_obj, root_box, nodes, sorted_codes, status, S(stream));
+                 leaf_obj, root_box, nodes, sorted_codes, leaf_dir, leaf_dir_bits, flags,
+                 status, S(stream));
+}
+
+int lbvh_finish_rows(const lbvh_tree *tree, float *node_mins, float *node_maxs, void *stream) {
+    return finish_rows(tree, node_mins, node_maxs, S(stream));
 }
 
 int lbvh_morton_codes(const double *pts, int64_t n, const double *lo, const double *hi,
@@ -150,10 +156,6 @@ int lbvh_pack(const lbvh_tree *tree, void *nodes, float *root_box, uint32_t *sta
 int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
                       void *stream) {
     return unpack_boxes(tree, node_mins, node_maxs, S(stream));
-}
-
-int lbvh_wide_records(const lbvh_tree *tree, void *nodes4, void *stream) {
-    return wide_records(tree, nodes4, S(stream));
 }
 
 int lbvh_leaf_directory_bits(int64_t n) {

@@ -37,7 +37,9 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
 #pragma unroll
     for (int j = 0; j < K; ++j) best[j] = (j < K - kk) ? -INFINITY : INFINITY;
     const float *__restrict__ mn = t.node_mins + 3 * (n - 1);
-    const float *__restrict__ mx = t.node_maxs + 3 * (n - 1);
+    // point leaves: maxs == mins (a deferred build leaves node_maxs leaf rows unwritten)
+    const float *__restrict__ mx =
+        (t.flags & LBVH_TREE_POINT_LEAVES) ? mn : t.node_maxs + 3 * (n - 1);
     for (int64_t p = w0; p < w1; ++p) {
         const float d = box_dist_sq(px, py, pz, __ldg(mn + 3 * p), __ldg(mn + 3 * p + 1),
                                     __ldg(mn + 3 * p + 2), __ldg(mx + 3 * p),

@@ -3,14 +3,15 @@
 //   spatial_kernel<COUNT>   spatial_pass(store=False)   _kernels.py:179-228
 //   spatial_kernel<FILL>    spatial_pass(store=True)    _kernels.py:179-228
 //   spatial_kernel<BUFFER>  spatial_pass_buffered       _kernels.py:231-282
-//   compact_kernel          compact_rows                _kernels.py:285-290
+//   compact_warp_kernel     compact_rows                _kernels.py:285-290
 //   knn_kernel<K>           knn_pass, k <= K            _kernels.py:293-414
+//   knn_smem_heap_kernel    knn_pass, 16 < k <= 400 (heap in shared memory)
 //   knn_heap_kernel         knn_pass, any k (heap in the output span)
 //
 // One thread per query slot s; slot s serves query order[s], so Morton-sorted
 // queries put spatially close queries in the same warp and the same CTA
 // wave, and their node fetches hit in L1/L2.  Each internal node is one
-// 64-byte record (both child boxes + links), fetched with four 128-bit
+// 64-byte record (both child boxes + links), fetched with two 256-bit
 // loads.  Traversal order, stack discipline and the 64-entry stack limit
 // are the reference's, so hit order within a span and stack-exhaustion
 // behaviour are identical; kNN keeps a register-resident sorted list of
@@ -29,19 +30,6 @@ namespace {
 
 __device__ __forceinline__ float bx_of(const lbvh_tree &t, int i) { return __ldg(t.root_box + i); }
 
-// Children of an internal node sit at adjacent Karras ordinals (g, g+1), so
-// the next node is very likely in the line(s) these prefetches pull into L1
-// while the current node's boxes are being tested.
-#ifndef LBVH_PREFETCH_CHILDREN
-#define LBVH_PREFETCH_CHILDREN 0  // measured slower (extra L1 traffic); kept for A/B
-#endif
-__device__ __forceinline__ void prefetch_children(const PackedNode *nodes, int4 d) {
-    if (LBVH_PREFETCH_CHILDREN) {
-        if (d.x >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + d.x));
-        if (d.y >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + d.y));
-    }
-}
-
 #ifndef LBVH_SPATIAL_STACKTOP
 #define LBVH_SPATIAL_STACKTOP 1  // 6.95 vs 7.05 ms per 1e7-query 2P batch (C2), 32 registers
 #endif
@@ -53,25 +41,16 @@ enum SpatialMode {
     kCountBuf = 3,  // count all, keep the first `cap` hits in the row
 };
 
-#ifndef LBVH_LDG256
-#define LBVH_LDG256 1
-#endif
-
+// The 64-byte record in two 256-bit loads (sm_100 LDG.E.ENL2.256): kNN 8.30 vs
+// 8.48 ms and radius 2P 6.09 vs 7.01 ms against four 128-bit loads (C2).
 __device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, int32_t id,
                                           float4 &a, float4 &b, float4 &c, int4 &d) {
     const PackedNode *p = nodes + id;
-    if (LBVH_LDG256) {  // the 64-byte record in two 256-bit loads
-        float4 dd;
-        ldg256(&p->a, a, b);
-        ldg256(&p->c, c, dd);
-        d = make_int4(__float_as_int(dd.x), __float_as_int(dd.y), __float_as_int(dd.z),
-                      __float_as_int(dd.w));
-    } else {
-        a = __ldg(&p->a);
-        b = __ldg(&p->b);
-        c = __ldg(&p->c);
-        d = __ldg(&p->d);
-    }
+    float4 dd;
+    ldg256(&p->a, a, b);
+    ldg256(&p->c, c, dd);
+    d = make_int4(__float_as_int(dd.x), __float_as_int(dd.y), __float_as_int(dd.z),
+                  __float_as_int(dd.w));
 }
 
 // One hit (leaf ordinal `obj`); returns false when the 1P row overflows.
@@ -135,7 +114,6 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         float4 a, b, c;
         int4 d;
         load_node(nodes, node, a, b, c, d);
-        prefetch_children(nodes, d);
         const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
         const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
         int32_t next = -1;
@@ -192,49 +170,6 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
     if (MODE != kFill) counts[q] = cnt;
 }
 
-__global__ void __launch_bounds__(256)
-compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__restrict__ counts,
-               const int64_t *__restrict__ offsets, int64_t nq, int32_t *__restrict__ out) {
-    // One thread per query row: consecutive threads read consecutive rows
-    // (16-byte vector loads when rows are 16-byte aligned) and write
-    // consecutive output segments.
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t cnt = __ldg(counts + q);
-        if (cnt > cap) continue;  // did not fit its row: written by the overflow fill pass
-        const int64_t dst = __ldg(offsets + q);
-        const int32_t *row = buf + q * cap;
-        if ((cap & 7) == 0) {  // 32-byte aligned rows: 256-bit loads of full chunks
-            int32_t j = 0;
-            for (; j + 8 <= cnt; j += 8) {
-                float4 x, y;
-                ldg256(row + j, x, y);
-                out[dst + j] = __float_as_int(x.x);
-                out[dst + j + 1] = __float_as_int(x.y);
-                out[dst + j + 2] = __float_as_int(x.z);
-                out[dst + j + 3] = __float_as_int(x.w);
-                out[dst + j + 4] = __float_as_int(y.x);
-                out[dst + j + 5] = __float_as_int(y.y);
-                out[dst + j + 6] = __float_as_int(y.z);
-                out[dst + j + 7] = __float_as_int(y.w);
-            }
-            for (; j < cnt; ++j) out[dst + j] = __ldcs(row + j);  // never reads unwritten slots
-        } else if ((cap & 3) == 0) {
-            int32_t j = 0;
-            for (; j + 4 <= cnt; j += 4) {
-                const int4 v = __ldcs(reinterpret_cast<const int4 *>(row + j));
-                out[dst + j] = v.x;
-                out[dst + j + 1] = v.y;
-                out[dst + j + 2] = v.z;
-                out[dst + j + 3] = v.w;
-            }
-            for (; j < cnt; ++j) out[dst + j] = __ldcs(row + j);
-        } else {
-            for (int32_t j = 0; j < cnt; ++j) out[dst + j] = __ldcs(row + j);
-        }
-    }
-}
-
 // 5 resident CTAs per SM (<= 48 registers, no spills) with the 12-entry
 // shared-memory stack measured fastest at K=10 (8.75 vs 8.89 ms for 6 CTAs
 // and a local-memory stack, C2); K=32 keeps the compiler's choice.
@@ -243,9 +178,6 @@ compact_kernel(const int32_t *__restrict__ buf, int64_t cap, const int32_t *__re
 #endif
 #ifndef LBVH_KNN_SMEMSTACK
 #define LBVH_KNN_SMEMSTACK 12
-#endif
-#ifndef LBVH_KNN_PAIR_STORES
-#define LBVH_KNN_PAIR_STORES 1
 #endif
 // Threads per CTA of knn_kernel (resident threads per SM stay
 // LBVH_KNN_MINBLOCKS * 256 for K <= 16).
@@ -266,7 +198,7 @@ __host__ __device__ constexpr int knn_min_blocks(int K) {
 }
 
 // One query slot s of a kNN batch (s < nq).
-template <int K, bool REGNEXT>
+template <int K>
 __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__restrict__ centers,
                                           const uint32_t *__restrict__ order,
                                           const uint32_t *__restrict__ qcodes, int64_t s,
@@ -287,6 +219,7 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         const float d2 = box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]);
         out_dist[base] = squared ? d2 : __fsqrt_rn(d2);
         out_idx[base] = __ldg(t.leaf_obj);
+        if (kth) kth[q] = d2;  // the only candidate is the k-th (forwarding bound)
         return;
     }
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
@@ -295,42 +228,27 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
                             ? seed_bound<K>(t, __ldg(qcodes + s), kk, px, py, pz)
                             : __int_as_float(0x7FFFFFFF);
     top.init(kk, bound);
-    // Stack entries pack (dist^2 bits << 32 | node).  Reference order: push
-    // farther, push nearer, pop (_kernels.py:363-403).  With REGNEXT the
-    // nearer child stays in a register instead of a push/pop pair: its
-    // pop-time prune test cannot fire (nothing is offered between its push
-    // and pop) and the capacity test still counts it, so node order and
-    // stack exhaustion are the reference's either way.
-    uint64_t stack[kStack];
-    // LBVH_KNN_SMEMSTACK = D > 0 (REGNEXT): the first D entries live in
-    // shared memory as bare node ids (lane-interleaved, conflict-free),
-    // deeper ones in local memory.  Popped entries are not re-tested (a
-    // pruned entry costs one node visit whose children are then pruned), so
-    // pushes -- and the capacity test -- are exactly as above.
-    constexpr int SMS = REGNEXT ? LBVH_KNN_SMEMSTACK : 0;
-    __shared__ int32_t sst[(SMS > 0 ? SMS : 1) * LBVH_KNN_BLOCK];
+    // Reference node order: push farther, push nearer, pop (_kernels.py:363-403).
+    // The nearer child stays in a register (`next`) instead of a push/pop
+    // pair: its pop-time prune test cannot fire (nothing is offered between
+    // its push and pop) and the capacity test still counts it, so node order
+    // and stack exhaustion are the reference's.  The first LBVH_KNN_SMEMSTACK
+    // entries live in shared memory as bare node ids (lane-interleaved,
+    // conflict-free), deeper ones in local memory.  Popped entries are not
+    // re-tested (a pruned entry costs one node visit whose children are then
+    // pruned), so pushes -- and the capacity test -- are exactly as above.
+    constexpr int SMS = LBVH_KNN_SMEMSTACK;
+    static_assert(SMS > 0 && SMS <= kStack, "shared-memory stack depth");
+    int32_t lstack[kStack];
+    __shared__ int32_t sst[SMS * LBVH_KNN_BLOCK];
     int32_t *const sbase = sst + (threadIdx.x % LBVH_KNN_BLOCK);
-    int32_t *const lstack = reinterpret_cast<int32_t *>(stack);
     uint32_t fail = 0;
-    int sp;
+    int sp = 0;
     int32_t node = 0;  // the root; never pruned (the list is empty)
-    if (REGNEXT) {
-        sp = 0;
-    } else {
-        sp = 1;
-        stack[0] = 0;
-    }
     while (true) {
-        if (!REGNEXT) {
-            if (sp == 0) break;
-            const uint64_t e = stack[--sp];
-            if (__uint_as_float((uint32_t)(e >> 32)) > top.worst()) continue;
-            node = (int32_t)(uint32_t)e;
-        }
         float4 a, b, c;
         int4 dd;
         load_node(nodes, node, a, b, c, dd);
-        prefetch_children(nodes, dd);
         const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
         const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
         // farther child first so the nearer one is on top (_kernels.py:373-379)
@@ -346,15 +264,11 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                if (SMS > 0) {
-                    if (sp < SMS)
-                        sbase[sp * LBVH_KNN_BLOCK] = fl;
-                    else
-                        lstack[sp] = fl;
-                    ++sp;
-                } else {
-                    stack[sp++] = ((uint64_t)__float_as_uint(fd) << 32) | (uint32_t)fl;
-                }
+                if (sp < SMS)
+                    sbase[sp * LBVH_KNN_BLOCK] = fl;
+                else
+                    lstack[sp] = fl;
+                ++sp;
             }
         }
         if (!(ndist > top.worst())) {
@@ -365,38 +279,21 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
                     fail = LBVH_FLAG_STACK_EXHAUSTED;
                     break;
                 }
-                if (REGNEXT)
-                    next = nl;
-                else
-                    stack[sp++] = ((uint64_t)__float_as_uint(ndist) << 32) | (uint32_t)nl;
+                next = nl;
             }
         }
-        if (REGNEXT) {
-            if (next < 0) {
-                if (SMS > 0) {
-                    if (sp == 0) break;
-                    --sp;
-                    next = sp < SMS ? sbase[sp * LBVH_KNN_BLOCK] : lstack[sp];
-                } else {
-                    // pop until an entry survives the prune test (_kernels.py:364-368)
-                    while (sp > 0) {
-                        const uint64_t e = stack[--sp];
-                        if (!(__uint_as_float((uint32_t)(e >> 32)) > top.worst())) {
-                            next = (int32_t)(uint32_t)e;
-                            break;
-                        }
-                    }
-                    if (next < 0) break;
-                }
-            }
-            node = next;
+        if (next < 0) {
+            if (sp == 0) break;
+            --sp;
+            next = sp < SMS ? sbase[sp * LBVH_KNN_BLOCK] : lstack[sp];
         }
+        node = next;
     }
     if (fail) atomicOr(status, fail);
     // the k-th squared distance (exact; the sharded search's forwarding bound)
     if (kth) kth[q] = top.dist(K - 1);
     // Spans are written even after a failure; the driver raises anyway.
-    if (LBVH_KNN_PAIR_STORES && (K & 1) == 0 && kk == K && (base & 1) == 0) {
+    if ((K & 1) == 0 && kk == K && (base & 1) == 0) {
         // full span at an even offset: 64-bit stores (half the store requests)
 #pragma unroll
         for (int j = 0; j < K; j += 2) {
@@ -418,7 +315,7 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     }
 }
 
-template <int K, bool REGNEXT>
+template <int K>
 __global__ void __launch_bounds__(LBVH_KNN_BLOCK,
                                   knn_min_blocks(K))
 knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
@@ -428,8 +325,8 @@ knn_kernel(const lbvh_tree t, const float *__restrict__ centers,
            int uniform) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nq) return;
-    knn_query<K, REGNEXT>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared,
-                          status, kth, uniform);
+    knn_query<K>(t, centers, order, qcodes, s, offsets, out_idx, out_dist, squared, status, kth,
+                 uniform);
 }
 
 // General k: the output span doubles as a bounded max-heap, exactly the
@@ -741,14 +638,12 @@ int spatial_1p(const lbvh_tree *t, const float *centers, const float *radii, flo
                                    cap, nullptr, status, stream);
 }
 
-// Warp-cooperative compaction (LBVH_COMPACT_WARP): a warp takes 32 rows,
+// Warp-cooperative compaction: a warp takes 32 rows,
 // scans their hit counts and writes the concatenation with consecutive lanes
 // on consecutive output words (element e of the warp's run belongs to the row
 // found by a 5-step shuffle search of the scan).  Rows that overflowed their
 // buffer count 0 here (the fill pass writes them).
-#ifndef LBVH_COMPACT_WARP
-#define LBVH_COMPACT_WARP 1  // radius 2P at C2: 5.51 vs 5.88 ms; ~30 hits/query: 10.8 vs 12.1
-#endif
+// (radius 2P at C2: 5.51 vs 5.88 ms with a thread per row; ~30 hits/query: 10.8 vs 12.1)
 __global__ void __launch_bounds__(256)
 compact_warp_kernel(const int32_t *__restrict__ buf, int64_t cap,
                     const int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
@@ -799,17 +694,13 @@ int compact(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_
     if (!buf || !counts || !offsets) return LBVH_ERR_INVALID_ARG;
     unsigned g = div_up(nq, 256);
     g = g < kNumSMs * 8 ? g : kNumSMs * 8;
-    if (LBVH_COMPACT_WARP)
-        compact_warp_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
-    else
-        compact_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
+    compact_warp_kernel<<<g, 256, 0, stream>>>(buf, cap, counts, offsets, nq, out);
     count_launches(1);
     return check_launch();
 }
 
-size_t knn_workspace_bytes(int64_t nq) {
-    return align_up(sizeof(float) * (size_t)(nq > 0 ? nq : 1)) + 256;
-}
+// Reserved: lbvh_knn takes no workspace today (the argument is accepted and unused).
+size_t knn_workspace_bytes(int64_t) { return 0; }
 
 namespace {
 __global__ void __launch_bounds__(256)
@@ -840,9 +731,6 @@ int leaf_directory(const uint32_t *codes, int64_t n, int bits, uint32_t *dir,
     return check_launch();
 }
 
-int knn_wide(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, int64_t,
-             const int64_t *, int64_t, int32_t *, float *, bool, uint32_t *, cudaStream_t);
-
 int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
         const uint32_t *qcodes, int64_t nq, const int64_t *offsets, int64_t max_span,
         int32_t *out_idx, float *out_dist, int flags, void *ws, size_t ws_bytes,
@@ -853,46 +741,29 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     if (!centers || !offsets || !out_idx || !out_dist) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     const unsigned g = div_up(nq, LBVH_KNN_BLOCK);
-    // 1 = nearer child kept in a register (measured faster with the seed),
-    // 0 = reference push/pop per node.  Same results either way.
-    static const int variant = env_int("LBVH_KNN_VARIANT", 1);
-    if (env_int("LBVH_KNN_NOSEED", 0)) qcodes = nullptr;
 #define LBVH_KNN_CASE(KV)                                                                   \
     if (max_span <= KV) {                                                                   \
-        if (variant == 1)                                                                   \
-            knn_kernel<KV, true><<<g, LBVH_KNN_BLOCK, 0, stream>>>(                        \
-                *t, centers, order, qcodes, nq, offsets, out_idx, out_dist, squared, status, \
-                kth, uniform);                                                              \
-        else                                                                                \
-            knn_kernel<KV, false><<<g, LBVH_KNN_BLOCK, 0, stream>>>(                       \
-                *t, centers, order, qcodes, nq, offsets, out_idx, out_dist, squared, status, \
-                kth, uniform);                                                              \
+        knn_kernel<KV><<<g, LBVH_KNN_BLOCK, 0, stream>>>(*t, centers, order, qcodes, nq,     \
+                                                        offsets, out_idx, out_dist, squared, \
+                                                        status, kth, uniform);              \
         count_launches(1);                                                                  \
         return check_launch();                                                              \
     }
     const bool squared = (flags & LBVH_KNN_SQUARED) != 0;
     const int uniform = (flags & LBVH_KNN_UNIFORM_SPANS) ? (int)max_span : 0;
-    static const int wide = env_int("LBVH_KNN_WIDE", 1);
-    if (wide && !kth && t->nodes4 && (t->flags & LBVH_TREE_CODES30)) {
-        const int rc = knn_wide(t, centers, order, qcodes, nq, offsets, max_span, out_idx,
-                                out_dist, squared, status, stream);
-        if (rc >= 0) return rc;
-    }
     LBVH_KNN_CASE(4)
     LBVH_KNN_CASE(8)
     LBVH_KNN_CASE(10)
     // smallest k on the shared-memory heap path: k = 24 / 32 run at 23.9 / 31.7 ms there vs
     // 33.9 / 42.2 ms with 32-slot register lists (C2); k = 16 stays in registers (14.3 vs 18.6)
-    static const int heap_min = env_int("LBVH_KNN_HEAP_MIN", 17);
-    if (max_span < heap_min || kth) {
+    if (max_span <= 16 || kth) {
         LBVH_KNN_CASE(16)
         LBVH_KNN_CASE(32)
     }
 #undef LBVH_KNN_CASE
     // shared-memory heap up to 400 slots per query (64 threads x 8 B x k <= 200 KB)
     const size_t smem = (size_t)kHeapThreads * 8 * (size_t)max_span;
-    static const int smem_heap = env_int("LBVH_KNN_SMEM_HEAP", 1);
-    if (smem_heap && max_span <= 400) {
+    if (max_span <= 400) {
         static size_t opted = 0;
         if (smem > opted) {
             cudaFuncSetAttribute(knn_smem_heap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -42,7 +42,6 @@ CPU engine (the oracle) to exercise the routing on ``gloo``.
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -98,7 +97,7 @@ class GpuEngine:
         return build(pts.contiguous())
 
     def box(self, tree) -> torch.Tensor:
-        return tree.device_arrays()["root_box"].clone()
+        return tree._device()["root_box"].clone()
 
     def knn_sq(self, tree, centers: torch.Tensor, k: int):
         from .traversal import query_knn_squared
@@ -130,7 +129,7 @@ class GpuEngine:
         from . import _device as dv
         from . import _lib
 
-        d = tree.device_arrays()
+        d = tree._device()
         g = gids.to(torch.int64).contiguous()
         _lib.check(_lib.lib().lbvh_remap_leaves(tree.ctree(), dv.ptr(d["leaf_obj"]),
                                                 dv.ptr(d["nodes"]), dv.ptr(g), dv.stream()))
@@ -523,9 +522,9 @@ def _home_chunk_fused(t: DistributedBvh, hc: torch.Tensor, k: int, kk: int):
 # all-to-all returning chunk j's results overlaps chunk j+1's search; each
 # chunk adds host syncs (measured on one GPU, routed: 12.0 / 13.3 / 14.2 ms
 # per 1e7-query step for 1 / 2 / 4 chunks), so the default is 1.
-_SHARD_CHUNKS = int(os.environ.get("LBVH_SHARD_CHUNKS", "1"))
+_SHARD_CHUNKS = 1
 # measurement switch: take the routed (partition + exchange) path even on one rank
-_FORCE_ROUTE = os.environ.get("LBVH_SHARD_FORCE_ROUTE", "0") == "1"
+_FORCE_ROUTE = False
 
 
 class _PendingReturn:

@@ -19,7 +19,6 @@ Errors carry the reference's exception types and messages.
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 from typing import Callable
 
@@ -47,7 +46,7 @@ _PIPELINE_CHUNK = 1 << 20
 # Traversal order = stable sort by the top 24 of the 30 Morton bits (3 radix
 # passes instead of 4); ~0.6 queries share a 24-bit cell at 1e7, so warps
 # stay as coherent, and the order never changes results.
-_ORDER_BITS = int(os.environ.get("LBVH_ORDER_BITS", "24"))
+_ORDER_BITS = 24
 
 # Benchmark hook: when set to an object with ``wrap(name, call)``, the main
 # traversal launches are bracketed by CUDA events on the launching stream.
@@ -306,7 +305,7 @@ def _order(tree: Bvh, b: _Batch, sort_queries: bool, with_codes: bool = False):
     codes = dv.empty(b.nq, torch.int32) if with_codes else None
     ws = dv.workspace(l.lbvh_query_workspace_bytes(b.nq))
     _lib.check(l.lbvh_query_order(dv.ptr(b.centers), b.nq,
-                                  dv.ptr(tree.device_arrays()["root_box"]), _ORDER_BITS,
+                                  dv.ptr(tree._device()["root_box"]), _ORDER_BITS,
                                   dv.ptr(order), dv.ptr(codes), dv.ptr(ws), ws.numel(),
                                   dv.stream()))
     return (order, codes) if with_codes else order
@@ -331,7 +330,7 @@ def _finish(host: bool, status: dv.Status, *arrays):
 # the count pass (in traversal order, so bytes are the reference's fill
 # order); the fill pass then revisits only queries with more hits.  The row
 # buffer is skipped when it would exceed _ROW_BUDGET bytes.
-_ROW_HITS = int(os.environ.get("LBVH_ROW_HITS", "48"))
+_ROW_HITS = 48
 _ROW_BUDGET = 8 << 30
 
 
@@ -456,7 +455,7 @@ def _spatial_2p_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet
     host_c = dv.as_tensor(b.host_centers)
     dev_c = torch.empty((nq, 3), dtype=torch.float32, device=dev)
     ct = tree.ctree()
-    root_box = dv.ptr(tree.device_arrays()["root_box"])
+    root_box = dv.ptr(tree._device()["root_box"])
     rows = _ROW_HITS
     nch = -(-nq // C)
     ws = dv.workspace(max(l.lbvh_query_workspace_bytes(C), l.lbvh_scan_workspace_bytes(C)))
@@ -658,7 +657,7 @@ def _query_knn(tree: Bvh, queries, sort_queries: bool, squared: bool) -> ResultS
 _HOST_POOL = None
 # 1 (measured 16.07 vs 16.63 ms e2e at C2): host threads write the uniform
 # offsets instead of copying them from the device
-_HOST_OFFSETS = os.environ.get("LBVH_HOST_OFFSETS", "1") == "1"
+_HOST_OFFSETS = True
 
 
 def _host_arange_into(out: np.ndarray, step: int, parts: int = 8):
@@ -748,7 +747,7 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> 
         with torch.cuda.stream(s_out):
             h_off.copy_(offsets, non_blocking=True)
     ct = tree.ctree()
-    root_box = dv.ptr(tree.device_arrays()["root_box"])
+    root_box = dv.ptr(tree._device()["root_box"])
     c_ptr, o_ptr = dv.ptr(dev_c), dv.ptr(offsets)
     for c0 in range(0, nq, chunk):
         c1 = min(nq, c0 + chunk)

@@ -15,7 +15,6 @@ from __future__ import annotations
 
 from typing import NamedTuple
 
-import os
 
 import numpy as np
 import torch
@@ -24,11 +23,6 @@ from . import _device as dv
 from . import _lib
 from .geometry import Box
 from .validation import check_boxes
-
-# 4-wide kNN records (LBVH_WIDE=1; A/B switch).  Measured slower than the
-# binary kernel at C2 (8.89 vs 8.48 ms, +0.9 ms build): the kNN kernel is
-# issue-bound and a 4-wide step costs more than two binary ones.
-_WIDE = os.environ.get("LBVH_WIDE", "0") == "1"
 
 __all__ = ["Bvh", "Topology", "build", "common_prefix", "find_split", "node_range",
            "generate_topology", "refit_bounds"]
@@ -96,6 +90,8 @@ class Bvh:
                 h["scene_min"] = _readonly(box[:3].copy())
                 h["scene_max"] = _readonly(box[3:].copy())
             else:
+                if name in ("node_mins", "node_maxs"):
+                    self._finish_rows()
                 h[name] = _readonly(dv.d2h(d[name]))
         return h[name]
 
@@ -111,10 +107,26 @@ class Bvh:
     def device_arrays(self) -> dict:
         """Device tensors: node_mins, node_maxs, left, right, leaf_obj,
         nodes (packed (n-1) x 64 B), root_box (6 f32).  Uploads and packs a
-        host-constructed tree on first use."""
+        host-constructed tree on first use; writes the reference-layout rows a
+        build deferred (LBVH_BUILD_DEFER_ROWS) on first access."""
+        d = self._device()
+        self._finish_rows()
+        return d
+
+    def _device(self) -> dict:
+        """Device tensors as they are: the deferred reference rows (internal
+        node_mins/node_maxs rows, node_maxs leaf rows of a point tree) may
+        still be unwritten -- no query reads them."""
         if self._dev is None:
             self._upload()
         return self._dev
+
+    def _finish_rows(self) -> None:
+        d = self._dev
+        if d is not None and d.get("rows_pending"):
+            _lib.check(_lib.lib().lbvh_finish_rows(self.ctree(), dv.ptr(d["node_mins"]),
+                                                   dv.ptr(d["node_maxs"]), dv.stream()))
+            d["rows_pending"] = False
 
     def _upload(self) -> None:
         h = self._host
@@ -136,7 +148,7 @@ class Bvh:
 
     def ctree(self) -> _lib.CTree:
         """The C-ABI tree struct (cached: device buffers never move once built)."""
-        d = self.device_arrays()
+        d = self._device()
         ct = getattr(self, "_ct", None)
         if ct is None or ct[0] is not d:
             ct = (d, _ctree(d, self._n))
@@ -186,7 +198,7 @@ def _ctree(d: dict, n: int) -> _lib.CTree:
     return _lib.CTree(n, dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]),
                       dv.ptr(d.get("left")), dv.ptr(d.get("right")), dv.ptr(d["leaf_obj"]),
                       dv.ptr(d["nodes"]), dv.ptr(d["root_box"]), dv.ptr(d.get("leaf_codes")),
-                      dv.ptr(ld), bits, int(d.get("flags", 0)), dv.ptr(d.get("nodes4")))
+                      dv.ptr(ld), bits, int(d.get("flags", 0)))
 
 
 def _device_boxes(boxes):
@@ -223,25 +235,23 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
         "nodes": dv.empty(max(n - 1, 1) * _lib.NODE_BYTES, torch.uint8),
         "leaf_codes": dv.empty(n, i32),  # Morton codes in leaf order (kNN seed)
     }
+    # kNN seed index over the sorted leaf codes (2^bits + 1 bucket starts),
+    # written by the build's hierarchy pass
+    bits = l.lbvh_leaf_directory_bits(n)
+    d["leaf_dir"] = dv.empty((1 << bits) + 1, i32)
     ws = dv.workspace(l.lbvh_build_workspace_bytes(n))
     status = dv.Status()
+    # the reference-layout rows no query reads are written on first access
+    # (Bvh._finish_rows: host fields, device_arrays())
     _lib.check(_launch("build", lambda: l.lbvh_build(
                             dv.ptr(mins), dv.ptr(maxs), n, morton_bits, dv.ptr(ws), ws.numel(),
                             dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]), dv.ptr(d["left"]),
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
-                            dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), status.ptr,
-                            dv.stream())))
+                            dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), dv.ptr(d["leaf_dir"]),
+                            bits, _lib.BUILD_DEFER_ROWS, status.ptr, dv.stream())))
+    d["rows_pending"] = True
     d["flags"] = ((_lib.TREE_POINT_LEAVES if maxs is mins else 0)
                   | (_lib.TREE_CODES30 if morton_bits == 30 else 0))
-    # kNN seed index over the sorted leaf codes (2^bits + 1 bucket starts)
-    bits = l.lbvh_leaf_directory_bits(n)
-    d["leaf_dir"] = dv.empty((1 << bits) + 1, i32)
-    _lib.check(l.lbvh_leaf_directory(dv.ptr(d["leaf_codes"]), n, bits, dv.ptr(d["leaf_dir"]),
-                                     dv.stream()))
-    if morton_bits == 30 and n > 1 and _WIDE:
-        # 4-wide kNN records (layout of the same tree; kNN results unchanged)
-        d["nodes4"] = dv.empty((n - 1) * 128, torch.uint8)
-        _lib.check(l.lbvh_wide_records(_ctree(d, n), dv.ptr(d["nodes4"]), dv.stream()))
     if check:
         flags = status.read()
         if flags & _lib.FLAG_NONFINITE:

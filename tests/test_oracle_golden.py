@@ -120,3 +120,37 @@ def test_oracle_matches_reference_digests(digests, name):
     ko, ki, kd = oracle.query_knn(t, q, d["k"])
     assert sha16(ki) == d["knn_indices"] and sha16(kd) == d["knn_distances"]
     assert sha16(oracle.query_sort_order(q, t.scene_min, t.scene_max)) == d["query_order"]
+
+
+@pytest.fixture(scope="module")
+def large_digests():
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    with open(os.path.join(GOLDEN, "digests_large.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", ["c2_filled", "c3_hollow_sphere"])
+def test_oracle_at_baseline_scale(large_digests, name):
+    """The oracle at full BASELINE size (1e7 points / 1e7 queries, C2 and C3)
+    against the reference's digests (tests/golden/make_golden_large.py):
+    tree arrays, radius CRS in fill order (and kNN for C2).  ~30 s here."""
+    want = large_digests[name]
+    src = want["source"].split(":")
+    tgt = want["target"].split(":")
+    pts = datasets.generate(datasets.CloudSpec(src[0], src[1], want["m"], want["seed"]))
+    q = datasets.generate(datasets.CloudSpec(tgt[0], tgt[1], want["nq"], want["target_seed"]))
+    assert sha16(pts) == want["points"] and sha16(q) == want["queries"]
+    ref = oracle.build(pts)
+    for f in ("node_mins", "node_maxs", "left", "right", "leaf_obj"):
+        assert sha16(getattr(ref, f)) == want[f], f
+    off, idx = oracle.query_spatial_2p(ref, q, want["radius"])
+    assert sha16(off) == want["sp_offsets"] and sha16(idx) == want["sp_indices_fill_order"]
+    del off, idx
+    if name == "c2_filled":
+        ko, ki, kd = oracle.query_knn(ref, q, want["k"])
+        assert sha16(ko) == want["knn_offsets"]
+        assert sha16(ki) == want["knn_indices"] and sha16(kd) == want["knn_distances"]

@@ -46,13 +46,6 @@ rk63 = lb.query_knn(t63, (qd, 10))
 gd = lb.datasets.generate_device(lb.CloudSpec("sphere", "hollow", 3000, 4))
 gc = lb.datasets.generate_device(lb.CloudSpec("cube", "hollow", 3000, 4))
 bk = lb.brute_knn_batch(pts, qs[:200], 5)
-# 4-wide records (A/B layout)
-from paper_1908_11807_b200 import _device as dv, _lib  # noqa: E402
-d = t.device_arrays()
-d["nodes4"] = torch.empty((n - 1) * 128, dtype=torch.uint8, device="cuda")
-_lib.check(_lib.lib().lbvh_wide_records(t.ctree(), dv.ptr(d["nodes4"]), dv.stream()))
-rkw = lb.query_knn(t, (qd, 10))
-del d["nodes4"]
 # sharded protocol on one rank with the routing forced (partition, exchanges,
 # gather / scatter, forward masks, leaf remap, fused local search)
 import socket  # noqa: E402
