@@ -15,13 +15,14 @@ are in ``extra``.
 ``--impl reference`` times the CPU restatement of the reference path
 (oracle/, all host threads) on a bounded sample of the same workload.
 
-Multi-GPU (torchrun): weak scaling, one process per GPU over NCCL; the
-global cloud is N*1e7 points and N*1e7 queries, rank r holds the r-th chunk
-of each; the step is the sharded search of SURVEY §8(e)
-(``distributed.query_knn_distributed``: Morton-range shards, rank-box top
-tree, all-to-all query forwarding, exact merge); time is the max over ranks.
-``BENCH_BACKEND=gloo`` runs the same protocol with CPU collectives (testing
-several ranks on one GPU).
+Multi-GPU (torchrun): one process per GPU over NCCL; the step is the
+sharded search of SURVEY §8(e) (``distributed.query_knn_distributed``:
+Morton-range shards, rank-box top tree, all-to-all query forwarding, exact
+merge); time is the max over ranks.  Default: weak scaling, the global cloud
+is N*1e7 points and N*1e7 queries, rank r holds the r-th chunk of each.
+``--global-points G`` (C4: G = 8e7): strong scaling, G points and G queries
+in total, G/N per rank.  ``BENCH_BACKEND=gloo`` runs the same protocol with
+CPU collectives (testing several ranks on one GPU).
 """
 
 from __future__ import annotations
@@ -83,7 +84,42 @@ def parse_args(argv=None):
                    help="largest n of the C5 construction sweep")
     p.add_argument("--profile", action="store_true",
                    help="short run for ncu: no clocks/cpu/e2e/extra legs")
+    p.add_argument("--global-points", type=int, default=0,
+                   help="strong scaling (C4): this many points and queries in total, "
+                        "split over the ranks")
     return p.parse_args(argv)
+
+
+def world_size(args) -> int:
+    return int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
+
+
+def shape_of(args, world: int):
+    """(points per rank, queries per rank, global points, global queries)."""
+    if args.global_points:
+        g = args.global_points
+        return g // world, g // world, g // world * world, g // world * world
+    m = args.m
+    nq = args.nq or m
+    return m, nq, world * m, world * nq
+
+
+def workload(args, world: int) -> dict:
+    """The ``config`` object both arms print (same workload, same keys)."""
+    m, nq, gm, gq = shape_of(args, world)
+    k = args.k
+    if world == 1 and not args.global_points:
+        wl = (f"C2 kNN: cube:filled m={m} seed 0 / cube:filled nq={nq} seed 1, k={k}, "
+              "query Morton pre-sort on")
+    else:
+        tag = "C4 strong" if args.global_points else "weak"
+        wl = (f"{tag} sharded kNN: global cube:filled {gm} points seed 0 / cube:filled {gq} "
+              f"queries seed 1, rank r holds the r-th contiguous chunk of each, k={k}")
+    return {"workload": wl, "m_per_gpu": m, "nq_per_gpu": nq, "k": k,
+            "global_points": gm, "global_queries": gq,
+            "l2": "flushed before every timed step (256 MiB device write)",
+            "parallelism": (f"sharded x{world}: Morton-range shards, rank-box top tree, "
+                            "NCCL all-to-all forwarding" if world > 1 else "single GPU")}
 
 
 # ---------------------------------------------------------------------------
@@ -256,8 +292,7 @@ def run_ours(args):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         return float(t.item())
 
-    m = args.m
-    nq = args.nq or m
+    m, nq, gm, gq = shape_of(args, world)
     k = args.k
     lib = _lib.lib()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -265,9 +300,9 @@ def run_ours(args):
     def flush_l2():
         flush_buf.fill_(rank & 0xFF)
 
-    # Weak scaling over one global cloud: N*m filled-box points (seed 0) and
-    # N*nq queries (seed 1), the reference bench's clouds; rank r holds the
-    # r-th contiguous chunk of each (N=1: exactly configuration C2).
+    # One global cloud of gm filled-box points (seed 0) and gq queries (seed
+    # 1), the reference bench's clouds; rank r holds the r-th contiguous chunk
+    # of each (N=1: exactly configuration C2; weak: gm = N*m; C4: gm fixed).
     if world == 1:
         pts = lb.generate(lb.CloudSpec("cube", "filled", m, 0))
         qs = lb.generate(lb.CloudSpec("cube", "filled", nq, 1))
@@ -275,9 +310,9 @@ def run_ours(args):
         # the global clouds generated on each GPU (bit-identical to numpy's)
         # and sliced; the host copies feed the e2e leg and the CPU baseline
         pts_d = lb.datasets.generate_device(
-            lb.CloudSpec("cube", "filled", world * m, 0), dev)[rank * m:(rank + 1) * m].clone()
+            lb.CloudSpec("cube", "filled", gm, 0), dev)[rank * m:(rank + 1) * m].clone()
         qs_d = lb.datasets.generate_device(
-            lb.CloudSpec("cube", "filled", world * nq, 1), dev)[rank * nq:(rank + 1) * nq].clone()
+            lb.CloudSpec("cube", "filled", gq, 1), dev)[rank * nq:(rank + 1) * nq].clone()
         torch.cuda.empty_cache()
         pts, qs = pts_d.cpu().numpy(), qs_d.cpu().numpy()
     if world == 1:
@@ -340,12 +375,23 @@ def run_ours(args):
             return D.query_knn_distributed(sharded["t"], qs_d, k)
 
     clocks = None
+    if dist_mode:
+        from paper_1908_11807_b200 import distributed as D
+    sent0 = D.STATS["a2a_bytes_sent"] if dist_mode else 0
     if args.profile:
         tot, launches, knn_ms = timed_loop(knn_step, args.steps, args.warmup, "knn")
     else:
         with ClockSampler(local) as cs:
             tot, launches, knn_ms = timed_loop(knn_step, args.steps, args.warmup, "knn")
         clocks = cs.summary()
+    if dist_mode:
+        # bytes every rank sent to the others during warm-up + timed steps,
+        # scaled to the timed steps; NVLink 5: 900 GB/s per direction per GPU
+        sent = (D.STATS["a2a_bytes_sent"] - sent0) * args.steps / (args.steps + args.warmup)
+        on_gpu = tdist.get_backend() == "nccl"
+        st = torch.tensor([float(sent)], dtype=torch.float64, device=dev if on_gpu else "cpu")
+        tdist.all_reduce(st)
+        a2a_bytes = float(st.item())
     ms_per_step = tot / args.steps
     value = world * nq * args.steps / (tot / 1e3)
 
@@ -361,30 +407,42 @@ def run_ours(args):
         "kernel_ms": round(knn_ms, 4) if knn_ms else None,
         "kernel_share_of_step": round(knn_ms / ms_per_step, 3) if knn_ms else None,
         "algorithmic_bytes_per_query": bq,
-        "bytes_model": "12 center + 8 offset + 8k idx/dist + 28 B x T box tests, "
-                       f"T={T_KNN_FILLED_1E7} (SURVEY.md 6.3, filled 1e7)",
+        "bytes_model": "modeled, not a hardware ceiling: 12 center + 8 offset + 8k idx/dist "
+                       f"+ 28 B x T box tests, T={T_KNN_FILLED_1E7} (SURVEY.md 6.3, filled 1e7), "
+                       "every box test counted as an HBM read (no cache reuse)",
         "peak_source": peak_src,
     }
+    hw = load_traffic().get("knn_hardware")
+    if hw:
+        # the measured side (ncu --set full of the same kernel, profiles/):
+        # DRAM bytes per launch over the live kernel time, and the issue /
+        # SIMT figures that actually bound it
+        hw = dict(hw)
+        if knn_ms and traffic:
+            hw["dram_gbs"] = round(traffic / (knn_ms / 1e3) / 1e9, 1)
+            hw["dram_frac"] = round(traffic / (knn_ms / 1e3) / 1e9 / peak_gbs, 4)
+        roofline["hardware"] = hw
 
     out = {
         "metric": f"knn_queries_per_sec (k={k}, {m:.0e} filled-box points, {nq:.0e} queries)",
         "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if args.global_points else "weak", "vs_baseline": None,
+        "dtype": "f32",
         "dtype_note": "fp32 box distances (reference recipe, unfused); f64 Morton normalisation",
         "data": "synthetic: paper_1908_11807_b200.datasets PCG64 clouds (reference generators)",
-        "config": {"workload": f"C2 kNN: cube:filled m={m} seed {2 * rank} / cube:filled "
-                               f"nq={nq} seed {2 * rank + 1}, k={k}, query Morton pre-sort on",
-                   "m_per_gpu": m, "nq_per_gpu": nq, "k": k,
-                   "l2": "flushed before every timed step (256 MiB device write)",
-                   "parallelism": (f"sharded x{world}: Morton-range shards, rank-box top tree, "
-                                   "NCCL all-to-all forwarding" if world > 1 else "single GPU")},
+        "config": workload(args, world),
         "roofline": roofline,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
     }
     if clocks is not None:
         out["clocks"] = clocks
+    if dist_mode:
+        out["nvlink"] = {"a2a_bytes_per_step": round(a2a_bytes / args.steps),
+                         "nvlink_frac": round(a2a_bytes / args.steps / (ms_per_step / 1e3)
+                                              / (900e9 * world), 6),
+                         "peak": "900 GB/s per direction per GPU (NVLink 5)"}
 
     if not args.profile:
         # -- e2e through the public API with pinned host buffers --------------
@@ -432,7 +490,7 @@ def run_ours(args):
         out["extra"] = extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank,
                                      dev, peak_gbs)
 
-    if rank == 0 and not args.no_cpu and not args.profile:
+    if world == 1 and not args.no_cpu and not args.profile:
         out["cpu_baseline"] = cpu_baseline(args, pts, qs, k)
 
     traversal.KERNEL_TIMER = None
@@ -547,25 +605,54 @@ def extra_metrics(args, lb, tree, pts_d, qs_d, qs, r, timed_loop, world, rank, d
 
 
 def cpu_baseline(args, pts, qs, k):
-    """Oracle port (oracle/lbvh_oracle.c, OpenMP, all host threads) on a
-    bounded sample: the full m-point tree, the first cpu_sample queries."""
+    """Oracle port (oracle/lbvh_oracle.c, OpenMP, all host threads) beside
+    every workload the GPU run reports, each on a bounded
+    sample: kNN C2 (headline, ``value``), radius 2P C2, radius 2P C3
+    (hollow-sphere sources) and the C5 construction sweep up to 1e7."""
     from oracle import oracle
+    import paper_1908_11807_b200.datasets as ds
 
     threads = host_threads(oracle)
+    sample_n = min(args.cpu_sample, qs.shape[0])
+    sample = qs[:sample_n]
     ref = oracle.build(pts, threads=threads)
-    sample = qs[: args.cpu_sample]
     oracle.query_knn(ref, sample[:1000], k, threads=threads)  # warm
     t0 = time.perf_counter()
     oracle.query_knn(ref, sample, k, threads=threads)
     dt = time.perf_counter() - t0
+    legs = {}
+    r = ds.default_radius(k)
+    t0 = time.perf_counter()
+    off, _ = oracle.query_spatial_2p(ref, sample, r, threads=threads)
+    legs["radius_2p_c2_queries_per_sec"] = round(sample_n / (time.perf_counter() - t0), 1)
+    del off, ref
     t0 = time.perf_counter()
     oracle.build(pts, threads=threads)
     bdt = time.perf_counter() - t0
-    return {"value": round(sample.shape[0] / dt, 1), "unit": "queries/s", "cores": threads,
+    hs = ds.generate(ds.CloudSpec("sphere", "hollow", pts.shape[0], 0))
+    href = oracle.build(hs, threads=threads)
+    t0 = time.perf_counter()
+    oracle.query_spatial_2p(href, sample, r, threads=threads)
+    legs["radius_2p_c3_queries_per_sec"] = round(sample_n / (time.perf_counter() - t0), 1)
+    del href, hs
+    sweep = {}
+    for n_b in (10_000, 100_000, 1_000_000, 10_000_000):
+        p_b = pts if n_b == pts.shape[0] else ds.generate(ds.CloudSpec("cube", "filled", n_b, 0))
+        reps = 5 if n_b <= 100_000 else 1
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.build(p_b, threads=threads)
+        sweep[str(n_b)] = round(n_b * reps / (time.perf_counter() - t0), 1)
+    legs["c5_build_prims_per_sec"] = sweep
+    return {"value": round(sample_n / dt, 1), "unit": "queries/s", "cores": threads,
             "kind": "port",
-            "sample": f"kNN k={k}: first {sample.shape[0]} of the {qs.shape[0]} queries "
-                      f"(Morton pre-sort included) against the full {pts.shape[0]}-point tree",
-            "build_prims_per_sec": round(pts.shape[0] / bdt, 1)}
+            "sample": f"kNN k={k}: first {sample_n} of the {qs.shape[0]} queries "
+                      f"(Morton pre-sort included) against the full {pts.shape[0]}-point tree; "
+                      f"legs: radius 2P on the same {sample_n} queries against the C2 tree and "
+                      f"the {pts.shape[0]}-point hollow-sphere (C3) tree; C5 builds 1e4-1e7 "
+                      "(1e8 omitted: ~20 s)",
+            "build_prims_per_sec": round(pts.shape[0] / bdt, 1),
+            "legs": legs}
 
 
 # ---------------------------------------------------------------------------
@@ -584,41 +671,56 @@ def host_threads(oracle) -> int:
 
 
 def run_reference(args):
+    """The reference's CPU path on this box's host cores: the oracle port
+    (OpenMP, every host thread), same workload and config as the GPU arm.  At
+    N=1 every step answers the whole C2 query batch (1e7 queries, ~2.5 s on
+    16 cores); with N>1 (rank 0 only) the global cloud is built and each step
+    answers a rotating window of cpu_sample queries of the global batch."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle
     import paper_1908_11807_b200.datasets as ds
 
-    m = args.m
-    nq = args.nq or m
+    world = world_size(args)
+    m, nq, gm, gq = shape_of(args, world)
     k = args.k
-    pts = ds.generate(ds.CloudSpec("cube", "filled", m, 0))
-    qs = ds.generate(ds.CloudSpec("cube", "filled", nq, 1))
+    pts = ds.generate(ds.CloudSpec("cube", "filled", gm, 0))
+    qs = ds.generate(ds.CloudSpec("cube", "filled", gq, 1))
     threads = host_threads(oracle)
     ref = oracle.build(pts, threads=threads)
-    sample = max(1000, min(args.cpu_sample // 4, nq))
+    sample = gq if world == 1 else max(1000, min(args.cpu_sample, gq))
+
+    def window(s):
+        lo = (s * sample) % max(1, gq - sample + 1)
+        return qs[lo:lo + sample]
+
     for w in range(args.warmup):
-        oracle.query_knn(ref, qs[:sample], k, threads=threads)
+        oracle.query_knn(ref, window(w), k, threads=threads)
     total = 0.0
     for s in range(args.steps):
-        lo = (s * sample) % max(1, nq - sample + 1)
+        q = window(args.warmup + s)
         t0 = time.perf_counter()
-        oracle.query_knn(ref, qs[lo:lo + sample], k, threads=threads)
+        oracle.query_knn(ref, q, k, threads=threads)
         total += time.perf_counter() - t0
     value = args.steps * sample / total
     out = {
         "impl": "reference",
         "metric": f"knn_queries_per_sec (k={k}, {m:.0e} filled-box points, {nq:.0e} queries)",
-        "value": round(value, 1), "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: same clouds as the GPU arm",
-        "config": {"workload": f"C2 kNN: cube:filled m={m} seed 0 / cube:filled nq={nq} seed 1, "
-                               f"k={k}", "m_per_gpu": m, "nq_per_gpu": nq, "k": k},
+        "higher_is_better": True, "scaling": "strong" if args.global_points else "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "dtype_note": "fp32 box distances (reference recipe, unfused); f64 Morton normalisation",
+        "data": "synthetic: paper_1908_11807_b200.datasets PCG64 clouds (reference generators)",
+        "config": workload(args, world),
         "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{sample} queries per step against the full {m}-point tree"},
+                         "sample": (f"every step: all {gq} queries (query Morton pre-sort "
+                                    f"included) against the full {gm}-point tree"
+                                    if sample == gq else
+                                    f"every step: a {sample}-query window of the {gq} global "
+                                    f"queries against the full {gm}-point tree")},
         "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -98,7 +98,7 @@ const char *lbvh_strerror(int code) {
 
 const char *lbvh_last_cuda_error(void) { return g_cuda_err; }
 
-int lbvh_abi_version(void) { return 3; }
+int lbvh_abi_version(void) { return 4; }
 
 uint64_t lbvh_launch_count(void) { return launch_count(); }
 

@@ -159,6 +159,14 @@ class GpuEngine:
 
 
 _COMM = {}  # group -> device collectives run on (the data device unless overridden)
+# Payload bytes this rank has sent to OTHER ranks through the all-to-alls
+# (counts exchanges excluded); bench.py reads it for nvlink_frac.
+STATS = {"a2a_bytes_sent": 0}
+
+
+def _count_sent(splits, row_bytes: int, group) -> None:
+    me = dist.get_rank(group)
+    STATS["a2a_bytes_sent"] += (sum(splits) - splits[me]) * row_bytes
 
 
 def _comm_device(group, data_dev):
@@ -188,13 +196,38 @@ def _partition(dest: torch.Tensor, world: int):
     return order, torch.bincount(dest, minlength=world).to(torch.int64)
 
 
+def _query_flags(c: torch.Tensor, r: torch.Tensor | None = None) -> torch.Tensor:
+    """This rank's batch value checks as LBVH_FLAG_* bits in a device int64
+    scalar (no host sync): non-finite centers, non-finite or negative radii."""
+    from . import _lib
+
+    f = (~torch.isfinite(c)).any().to(torch.int64) * _lib.FLAG_NONFINITE
+    if r is not None:
+        bad_r = (~torch.isfinite(r)) | (r < 0)
+        f = f | (bad_r.any().to(torch.int64) * _lib.FLAG_BAD_RADIUS)
+    return f
+
+
+def _raise_flags(flags: int) -> None:
+    if flags:
+        from .traversal import _raise_flags as raise_reference
+
+        raise_reference(flags)
+
+
 def _alltoallv(rows: torch.Tensor, dest: torch.Tensor, world: int, group=None,
-               grouped_counts=None):
+               grouped_counts=None, flags: torch.Tensor | None = None):
     """Send row i of ``rows`` to rank ``dest[i]``; returns (received rows,
     per-source counts).  Counts are exchanged first, then the payload.
     ``grouped_counts`` (list): rows are already grouped by destination with
-    these counts (``dest`` is then ignored)."""
+    these counts (``dest`` is then ignored).  ``flags`` (device int64
+    scalar, :func:`_query_flags`): this rank's input checks travel with the
+    counts, and EVERY rank raises the reference's ValueError before any
+    payload moves if any rank's batch is invalid (a rank raising alone would
+    leave the others blocked in the collective)."""
     if world == 1:
+        if flags is not None:
+            _raise_flags(int(flags))
         return rows, [int(rows.shape[0])]
     cdev = _comm_device(group, rows.device)
     if grouped_counts is not None:
@@ -204,9 +237,21 @@ def _alltoallv(rows: torch.Tensor, dest: torch.Tensor, world: int, group=None,
         order, counts = _partition(dest, world)
         send = rows[order].contiguous().to(cdev)
         counts = counts.to(cdev)
-    recv_counts = torch.empty_like(counts)
-    dist.all_to_all_single(recv_counts, counts, group=group)
-    sc, rc = counts.tolist(), recv_counts.tolist()
+    if flags is not None:
+        pair = torch.stack([counts, flags.to(cdev).expand(world)], dim=1).contiguous()
+        recv_pair = torch.empty_like(pair)
+        dist.all_to_all_single(recv_pair, pair, group=group)
+        got = recv_pair.tolist()
+        f = 0
+        for _, x in got:
+            f |= int(x)
+        _raise_flags(f)
+        sc, rc = counts.tolist(), [int(x) for x, _ in got]
+    else:
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=group)
+        sc, rc = counts.tolist(), recv_counts.tolist()
+    _count_sent(sc, rows[:1].numel() * rows.element_size() if rows.shape[0] else 0, group)
     recv = torch.empty((sum(rc),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=cdev)
     dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc,
                            group=group)
@@ -538,6 +583,8 @@ class _PendingReturn:
         self.rc = rcounts.tolist()
         self.dev = rd.device
         self.sends = (rd.contiguous().to(cdev), rg.contiguous().to(cdev))
+        for x in self.sends:
+            _count_sent(splits, x[:1].numel() * x.element_size() if x.shape[0] else 0, group)
         self.recvs = tuple(torch.empty((sum(self.rc),) + tuple(x.shape[1:]), dtype=x.dtype,
                                        device=cdev) for x in self.sends)
         self.works = [dist.all_to_all_single(r, x, output_split_sizes=self.rc,
@@ -595,7 +642,7 @@ def _query_knn_gpu(t: DistributedBvh, c: torch.Tensor, k: int):
     send = torch.empty_like(c)
     _lib.check(_lib.lib().lbvh_gather_rows3(dv.ptr(c), dv.ptr(order), nq, dv.ptr(send),
                                              dv.stream()))
-    hc, hcounts = _alltoallv(send, None, world, g, grouped_counts=sent)
+    hc, hcounts = _alltoallv(send, None, world, g, grouped_counts=sent, flags=_query_flags(c))
     hc = hc.contiguous()
     mh = int(hc.shape[0])
     # rows of origin o occupy [hstart[o], hstart[o + 1]) of hc
@@ -645,7 +692,7 @@ def query_knn_distributed(t: DistributedBvh, centers, k: int):
     rows = torch.empty((nq, 4), dtype=torch.float32, device=dev)
     rows[:, :3] = c
     rows[:, 3] = torch.arange(nq, dtype=torch.int32, device=dev).view(torch.float32)
-    hq, hcounts = _alltoallv(rows, home, world, g)
+    hq, hcounts = _alltoallv(rows, home, world, g, flags=_query_flags(c))
     origin = _source_ranks(hcounts, dev)
     hc = hq[:, :3].contiguous()
     mh = int(hc.shape[0])
@@ -786,7 +833,7 @@ def query_spatial_distributed(t: DistributedBvh, centers, radius):
     rows[:, :3] = c[qi]
     rows[:, 3] = r[qi]
     rows[:, 4] = qi.to(torch.int32).view(torch.float32)
-    rq, rcounts = _alltoallv(rows, rr, world, g)
+    rq, rcounts = _alltoallv(rows, rr, world, g, flags=_query_flags(c, r))
     src = _source_ranks(rcounts, dev)
     m = int(rq.shape[0])
     if m and t.tree is not None:

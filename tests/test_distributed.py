@@ -131,6 +131,26 @@ def _worker(rank, world, port, engine_kind, n_total, split, queue):
         # k beyond the whole cloud
         off, gid, dd = D.query_knn_distributed(t, q[:5], n_total + 3)
         assert int(off[-1]) == 5 * n_total
+        # invalid input on ONE rank: every rank raises the reference's
+        # ValueError before any payload moves (no rank left blocked)
+        bad = q[:20].copy()
+        if rank == 1:
+            bad[5, 1] = np.nan
+        rr = np.full(20, 1.0, np.float32)
+        if rank == 0:
+            rr[3] = -1.0
+        for call, msg in ((lambda: D.query_knn_distributed(t, bad, 10), "finite"),
+                          (lambda: D.query_spatial_distributed(t, bad, 1.0), "finite"),
+                          (lambda: D.query_spatial_distributed(t, q[:20], rr), "non-negative")):
+            try:
+                call()
+            except ValueError as exc:
+                assert msg in str(exc), exc
+            else:
+                raise AssertionError("invalid input accepted")
+        # the group is still usable afterwards
+        off, gid, dd = D.query_knn_distributed(t, q[:7], 3)
+        assert int(off[-1]) == 21
         dist.barrier()
         dist.destroy_process_group()
         queue.put((rank, "ok"))
@@ -165,6 +185,51 @@ def test_sharded_search_equals_single_process_gloo(split):
 @pytest.mark.parametrize("split", [0.5, 0.97, -1])
 def test_sharded_search_gpu_engine(split):
     _run("gpu", 20000, split)
+
+
+def _worker_tiny(rank, world, port, queue):
+    """One primitive per rank and k=1: the home's forwarding bound is the
+    k-th distance of a one-leaf local tree (traverse.cu n == 1 branch)."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1908_11807_b200 import distributed as D
+        from oracle import oracle
+
+        torch.cuda.set_device(0)
+        D.set_comm_device("cpu")
+        pts = np.array([[0.0, 0.0, 0.0], [10.0, 0.0, 0.0]], np.float32)
+        t = D.build_distributed(pts[rank:rank + 1], rank)
+        assert t.counts == [1, 1], t.counts
+        q = np.random.default_rng(rank).uniform(-5, 15, size=(200, 3)).astype(np.float32)
+        ref = oracle.build(pts, threads=1)
+        for k in (1, 2):
+            off, gid, dd = D.query_knn_distributed(t, torch.from_numpy(q).cuda(), k)
+            ko, ki, kd = oracle.query_knn(ref, q, k, threads=1)
+            assert np.array_equal(gid.cpu().numpy(), ki), k
+            assert dd.cpu().numpy().tobytes() == kd.tobytes(), k
+        dist.destroy_process_group()
+        queue.put((rank, "ok"))
+    except Exception:
+        import traceback
+
+        queue.put((rank, traceback.format_exc()))
+        raise
+
+
+@pytest.mark.gpu
+def test_sharded_search_one_primitive_per_rank_gpu():
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tiny, args=(r, 2, port, queue)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    msgs = dict(queue.get(timeout=5) for _ in range(2))
+    assert msgs == {0: "ok", 1: "ok"}, msgs
 
 
 def _worker_single(port, queue):

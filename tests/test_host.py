@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     lib = _lib.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.lbvh_abi_version() == 3
+    assert lib.lbvh_abi_version() == 4
     assert set(_lib.exported_symbols()) == set(header_functions())
 
 
@@ -175,3 +175,63 @@ def test_reference_module_names():
     run_chunked(lambda a, b: seen.append((a, b)), 10, 8)
     run_chunked(lambda a, b: seen.append((a, b)), 0, 8)
     assert seen == [(0, 10)]
+
+
+def header_prototypes():
+    """name -> list of C parameter types, parsed from include/lbvh_b200.h."""
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    protos = {}
+    for ret, name, params in re.findall(
+            r"(int|size_t|uint64_t|const char \*)\s*(lbvh_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text):
+        ps = [p.strip() for p in params.replace("\n", " ").split(",")]
+        protos[name] = [] if ps == ["void"] else [re.sub(r"\s*\b\w+$", "", p) for p in ps]
+    return protos
+
+
+_CTYPE = {"int": ctypes.c_int, "int32_t": ctypes.c_int32, "int64_t": ctypes.c_int64,
+          "size_t": ctypes.c_size_t, "float": ctypes.c_float, "double": ctypes.c_double,
+          "uint64_t": ctypes.c_uint64, "uint32_t": ctypes.c_uint32}
+
+
+def _same_kind(c_decl: str, ct) -> bool:
+    if "*" in c_decl:
+        return ct is ctypes.c_void_p or ct is ctypes.c_char_p or issubclass(
+            ct, ctypes._Pointer)
+    return ctypes.sizeof(ct) == ctypes.sizeof(_CTYPE[c_decl]) and (
+        issubclass(ct, ctypes.c_float) == (c_decl == "float")) and (
+        issubclass(ct, ctypes.c_double) == (c_decl == "double"))
+
+
+def test_python_binding_matches_header():
+    protos = header_prototypes()
+    assert len(protos) == len(header_functions())
+    for name, (argtypes, _) in _lib._SIGS.items():
+        assert name in protos, name
+        assert len(argtypes) == len(protos[name]), (name, len(argtypes), protos[name])
+        for c_decl, ct in zip(protos[name], argtypes):
+            assert _same_kind(c_decl, ct), (name, c_decl, ct)
+
+
+def test_integration_stub_matches_header():
+    """The ctypes stub INTEGRATION.md tells a reference maintainer to add:
+    executed against the built library, every argtypes list it declares must
+    match the header prototype parameter for parameter."""
+    md = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = next(b for b in re.findall(r"```python\n(.*?)```", md, flags=re.S)
+                 if "lbvh_build.argtypes" in b)
+    block = block.replace("import cupy as cp\n", "cp = None\n").replace(
+        '"liblbvh_b200.so"', repr(_lib.LIB_PATH))
+    ns = {}
+    exec(compile(block, "INTEGRATION.md", "exec"), ns)  # runs the ABI version assert
+    stub_lib = ns["_lib"]
+    protos = header_prototypes()
+    declared = re.findall(r"_lib\.(lbvh_[a-z0-9_]+)\.argtypes", block)
+    assert {"lbvh_build", "lbvh_knn", "lbvh_finish_rows"} <= set(declared)
+    for name in declared:
+        argtypes = getattr(stub_lib, name).argtypes
+        assert len(argtypes) == len(protos[name]), (name, len(argtypes), protos[name])
+        for c_decl, ct in zip(protos[name], argtypes):
+            assert _same_kind(c_decl, ct), (name, c_decl, ct)
+    # the stub's tree struct is the header's
+    fields = [f for f, _ in ns["LbvhTree"]._fields_]
+    assert fields == [f for f, _ in _lib.CTree._fields_]
