@@ -83,6 +83,8 @@ typedef struct lbvh_tree {
 /* Leaves ordered by (30-bit code, index) -- the reference's build -- so the
  * Karras node covering any code prefix can be located from leaf_codes. */
 #define LBVH_TREE_CODES30 0x2
+/* Built by lbvh_build (30- or 63-bit codes; user-built trees: 0). */
+#define LBVH_TREE_BUILT 0x4
 
 #define LBVH_NODE_BYTES 64
 
@@ -277,14 +279,43 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
  * unused), the count pass keeping the first `rows` hits of every query in
  * buf (rows 0: no row buffer), the exclusive scan into offsets (nq+1) and
  * the list of queries whose hits overflowed their row (over_list, over_n).
+ * Spill pool (optional, spill_pool != NULL): the count pass keeps a query's
+ * hits beyond its row too, in chunks of LBVH_SPILL_CHUNK ints drawn from
+ * spill_pool (spill_chunks chunks, chunk 0 reserved; each chunk holds
+ * LBVH_SPILL_CHUNK - 1 hits then the index of the next), the first chunk of
+ * query q in spill_heads[q] (nq i32, written for overflowing queries only;
+ * -1 = pool exhausted).  Overflowing queries fully held by the pool are
+ * listed in spill_list / spill_n (copy them with lbvh_spill_copy); only the
+ * rest go to over_list (fill pass).  Hit order is the fill order either way.
  * ev_before / ev_after (optional) bracket the count kernel. */
+#define LBVH_SPILL_CHUNK 128
 size_t lbvh_spatial_count_batch_workspace_bytes(int64_t nq);
 int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const float *radii,
                              float radius, int64_t nq, int order_bits, int64_t rows,
                              uint32_t *order, int32_t *counts, int32_t *buf, int64_t *offsets,
-                             uint32_t *over_list, uint32_t *over_n, void *workspace,
-                             size_t workspace_bytes, uint32_t *status, void *ev_before,
-                             void *ev_after, void *stream);
+                             uint32_t *over_list, uint32_t *over_n, int32_t *spill_heads,
+                             int32_t *spill_pool, int64_t spill_chunks, uint32_t *spill_list,
+                             uint32_t *spill_n, void *workspace, size_t workspace_bytes,
+                             uint32_t *status, void *ev_before, void *ev_after, void *stream);
+
+/* The spans of the spilled queries (spill_list, its length spill_n on the
+ * device, at most max_list): row hits then pool chunks, into out at
+ * offsets[q] -- the complement of lbvh_compact, which skips overflowed rows. */
+int lbvh_spill_copy(const int32_t *buf, int64_t rows, const int32_t *counts,
+                    const int64_t *offsets, const int32_t *spill_heads, const int32_t *spill_pool,
+                    const uint32_t *spill_list, const uint32_t *spill_n, int64_t max_list,
+                    int32_t *out, void *stream);
+
+/* spatial_pass(store=True) (_kernels.py:179-228) for the listed queries
+ * only (list: query ids, typically over_list of lbvh_spatial_count_batch):
+ * writes their whole spans at offsets[q].  list_len (device, optional) holds
+ * n_list; with it a persistent grid walks the list in order (the queries in
+ * flight stay a contiguous stretch of it), else one thread per entry.  Same
+ * bytes either way. */
+int lbvh_spatial_fill_list(const lbvh_tree *tree, const float *centers, const float *radii,
+                           float radius, const uint32_t *list, const uint32_t *list_len,
+                           int64_t n_list, const int64_t *offsets, int32_t *out,
+                           uint32_t *status, void *stream);
 
 /* query_knn for device-resident centers and a uniform k in one call: value
  * checks (LBVH_FLAG_NONFINITE), uniform CRS offsets (nq+1), Morton query

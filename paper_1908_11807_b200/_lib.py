@@ -51,6 +51,8 @@ class CTree(ctypes.Structure):
 
 TREE_POINT_LEAVES = 0x1
 TREE_CODES30 = 0x2
+TREE_BUILT = 0x4
+SPILL_CHUNK = 128
 
 
 _SIGS = {
@@ -113,8 +115,11 @@ _SIGS = {
     "lbvh_spatial_count_batch_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_spatial_count_batch": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_float, ctypes.c_int64, ctypes.c_int, ctypes.c_int64]
-                                 + [ctypes.c_void_p] * 7 + [ctypes.c_size_t]
+                                 + [ctypes.c_void_p] * 8 + [ctypes.c_int64]
+                                 + [ctypes.c_void_p] * 3 + [ctypes.c_size_t]
                                  + [ctypes.c_void_p] * 4, ctypes.c_int),
+    "lbvh_spill_copy": ([ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 6
+                        + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn_batch": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                         ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
@@ -125,6 +130,10 @@ _SIGS = {
                       ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_knn_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
+    "lbvh_spatial_fill_list": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_select_overflow": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lbvh_unpack_knn_keys": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,

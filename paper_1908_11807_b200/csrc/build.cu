@@ -327,6 +327,9 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     const int64_t p = B + tid;
     const int64_t internal = n - 1;
     s_slot[tid] = 0;
+    // this CTA's window of the global hand-off slots starts empty (ordered
+    // before any first arrival's publication below by the barrier)
+    if (p < n - 1) slots[p] = 0u;
     for (int i = tid; i < kHierT + 2; i += kHierT) {
         const int64_t j = B - 1 + i;
         if (j >= 0 && j < n) s_code[i] = __ldg(codes + j);
@@ -405,9 +408,14 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         __threadfence_block();
         const uint32_t known = (uint32_t)(left_side ? l : r);
         const uint32_t other = atomicExch(&s_slot[s], known + 1u);
-        if (other == 0) break;  // first arrival: the sibling continues
+        if (other == 0) {
+            // first arrival: publish the range end for a partner that may come
+            // from outside the CTA (the frontier kernel); a local partner
+            // meets us through s_slot and this word is never read
+            slots[g] = known + 1u;
+            break;  // the sibling continues
+        }
         __threadfence_block();
-        s_slot[s] = 0;  // consumed (only the two children meet here)
         const int64_t pl = left_side ? l : (int64_t)(other - 1u);
         const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
         const int64_t lc = (pl == g) ? internal + g : g;
@@ -448,10 +456,6 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         l = pl;
         r = pr;
     }
-    __syncthreads();
-    // first arrivals still waiting for a partner from outside the CTA
-    const uint32_t v = s_slot[tid];
-    if (v) slots[B + tid] = v;
 }
 
 // Box of a node the local kernel (or an earlier frontier step) finished:
@@ -733,16 +737,14 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
     Carve c(ws, ws_bytes);
     CodeT *codes = c.take<CodeT>(n);
     uint32_t *perm = c.take<uint32_t>(n);
-    size_t zero_begin = align_up(c.off);
-    uint32_t *slots = c.take<uint32_t>(n > 1 ? n - 1 : 1);
+    uint32_t *slots = c.take<uint32_t>(n > 1 ? n - 1 : 1);  // zeroed by the local kernel
     uint32_t *counter = c.take<uint32_t>(4);  // reduce CTAs, -, frontier, directory runs
-    size_t zero_end = c.off;
     float *partials = c.take<float>(6 * kNumSMs * 8);
     DirRun *runs = c.take<DirRun>(kDirRunsMax);
     void *sort_ws = c.take<char>(sizeof(CodeT) == 4 ? sort_workspace_bytes(n)
                                                     : sort64_workspace_bytes(n));
     if (!c.ok()) return LBVH_ERR_WORKSPACE;
-    cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
+    cudaMemsetAsync(counter, 0, 4 * sizeof(uint32_t), stream);
 
     unsigned rg = grid_for(n, kReduceThreads, 4);
     scene_reduce_kernel<<<rg, kReduceThreads, 0, stream>>>(mins, maxs, n, partials, counter,

@@ -51,7 +51,16 @@ int query_order(const float *, int64_t, const float *, int, uint32_t *, uint32_t
                 size_t, cudaStream_t, uint32_t *status = nullptr, int64_t *offsets = nullptr,
                 int64_t span = 0);
 int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
-                  int64_t, int32_t *, int32_t *, int64_t, uint32_t *, cudaStream_t);
+                  int64_t, int32_t *, int32_t *, int64_t, uint32_t *, cudaStream_t,
+                  int32_t *spill_heads = nullptr, int32_t *spill_pool = nullptr,
+                  int64_t spill_chunks = 0);
+int spill_copy(const int32_t *, int64_t, const int32_t *, const int64_t *, const int32_t *,
+               const int32_t *, const uint32_t *, const uint32_t *, int64_t, int32_t *,
+               cudaStream_t);
+int spatial_list(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
+                 const uint32_t *, int64_t, int32_t *, const int64_t *, int32_t *, bool,
+                 uint32_t *, cudaStream_t);
+
 int spatial_fill(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
                  int64_t, const int64_t *, int32_t *, const int32_t *, int64_t, uint32_t *,
                  cudaStream_t);
@@ -68,7 +77,8 @@ int knn(const lbvh_tree *, const float *, const uint32_t *, const uint32_t *, in
         cudaStream_t, float *);
 size_t knn_workspace_bytes(int64_t nq);
 int select_overflow(const uint32_t *, const int32_t *, int64_t, int64_t, uint32_t *, uint32_t *,
-                    cudaStream_t);
+                    cudaStream_t, const int32_t *spill_heads = nullptr,
+                    uint32_t *spill_list = nullptr, uint32_t *spill_count = nullptr);
 int check_queries(const float *, int64_t, const float *, uint32_t *, cudaStream_t);
 int unpack_knn_keys(const uint64_t *, int64_t, int64_t *, float *, cudaStream_t);
 int brute_knn(const float *, int64_t, const float *, int64_t, int64_t, int32_t *, float *,
@@ -285,13 +295,17 @@ size_t lbvh_spatial_count_batch_workspace_bytes(int64_t nq) {
 int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const float *radii,
                              float radius, int64_t nq, int order_bits, int64_t rows,
                              uint32_t *order, int32_t *counts, int32_t *buf, int64_t *offsets,
-                             uint32_t *over_list, uint32_t *over_n, void *ws, size_t ws_bytes,
-                             uint32_t *status, void *ev_before, void *ev_after, void *stream) {
+                             uint32_t *over_list, uint32_t *over_n, int32_t *spill_heads,
+                             int32_t *spill_pool, int64_t spill_chunks, uint32_t *spill_list,
+                             uint32_t *spill_n, void *ws, size_t ws_bytes, uint32_t *status,
+                             void *ev_before, void *ev_after, void *stream) {
     if (!tree || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (!centers || !counts || !offsets || !order || !ws ||
         (rows > 0 && (!buf || !over_list || !over_n)))
         return LBVH_ERR_INVALID_ARG;
+    const bool spill = rows > 0 && spill_pool && spill_chunks > 1;
+    if (spill && (!spill_heads || !spill_list || !spill_n)) return LBVH_ERR_INVALID_ARG;
     if (ws_bytes < lbvh_spatial_count_batch_workspace_bytes(nq)) return LBVH_ERR_WORKSPACE;
     cudaStream_t st = S(stream);
     const bool sorted = order_bits > 0 && nq > 1;
@@ -310,12 +324,16 @@ int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const 
     const uint32_t *ord = sorted ? order : nullptr;
     if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
     rc = spatial_count(tree, centers, radii, radius, ord, nq, counts, rows > 0 ? buf : nullptr,
-                       rows, status, st);
+                       rows, status, st, spill ? spill_heads : nullptr,
+                       spill ? spill_pool : nullptr, spill ? spill_chunks : 0);
     if (ev_after) cudaEventRecord((cudaEvent_t)ev_after, st);
     if (rc) return rc;
     rc = scan_counts(counts, nq, offsets, ws, ws_bytes, st);
     if (rc) return rc;
-    if (rows > 0) return select_overflow(ord, counts, nq, rows, over_list, over_n, st);
+    if (rows > 0)
+        return select_overflow(ord, counts, nq, rows, over_list, over_n, st,
+                               spill ? spill_heads : nullptr, spill ? spill_list : nullptr,
+                               spill ? spill_n : nullptr);
     return LBVH_OK;
 }
 
@@ -330,6 +348,27 @@ int lbvh_knn_kth(const lbvh_tree *tree, const float *centers, const uint32_t *or
 }
 
 size_t lbvh_knn_workspace_bytes(int64_t nq) { return knn_workspace_bytes(nq); }
+
+int lbvh_spatial_fill_list(const lbvh_tree *tree, const float *centers, const float *radii,
+                           float radius, const uint32_t *list, const uint32_t *list_len,
+                           int64_t n_list, const int64_t *offsets, int32_t *out,
+                           uint32_t *status, void *stream) {
+    if (!tree || n_list < 0 || !status) return LBVH_ERR_INVALID_ARG;
+    if (n_list == 0) return LBVH_OK;
+    if (list_len)
+        return spatial_list(tree, centers, radii, radius, list, list_len, n_list, nullptr,
+                            offsets, out, true, status, S(stream));
+    return spatial_fill(tree, centers, radii, radius, list, n_list, offsets, out, nullptr, 0,
+                        status, S(stream));
+}
+
+int lbvh_spill_copy(const int32_t *buf, int64_t rows, const int32_t *counts,
+                    const int64_t *offsets, const int32_t *spill_heads, const int32_t *spill_pool,
+                    const uint32_t *spill_list, const uint32_t *spill_n, int64_t max_list,
+                    int32_t *out, void *stream) {
+    return spill_copy(buf, rows, counts, offsets, spill_heads, spill_pool, spill_list, spill_n,
+                      max_list, out, S(stream));
+}
 
 int lbvh_select_overflow(const uint32_t *order, const int32_t *counts, int64_t nq,
                          int64_t buffer_size, uint32_t *list, uint32_t *list_len, void *stream) {

@@ -120,6 +120,21 @@ __device__ __forceinline__ void ldg256(const void *p, float4 &x, float4 &y) {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// 16-byte shared-memory store / load the compiler may not move across fences
+// or atomics (the hierarchy's in-CTA sibling hand-off).
+__device__ __forceinline__ void st_shared_v4(void *p, float4 v) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("st.volatile.shared.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_v4(const void *p) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    float4 v;
+    asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+    return v;
+}
+
 // GPU-scope release+acquire read-modify-writes (no full membar).
 __device__ __forceinline__ uint32_t atomic_exch_acq_rel(uint32_t *p, uint32_t v) {
     uint32_t old;

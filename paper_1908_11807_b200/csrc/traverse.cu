@@ -38,7 +38,22 @@ enum SpatialMode {
     kCount = 0,     // count only                        (spatial_pass store=False)
     kFill = 1,      // write at offsets[q]               (spatial_pass store=True)
     kBuffer = 2,    // 1P: row of `cap`, abort on overflow (spatial_pass_buffered)
-    kCountBuf = 3,  // count all, keep the first `cap` hits in the row
+    kCountBuf = 3,  // count all, keep the first `cap` hits in the row (and, with
+                    // a spill pool, the rest in pool chunks)
+};
+
+// Hits of a kCountBuf query beyond its row go to chunks of a caller-owned
+// pool: kSpillChunk - 1 hits, then the index of the query's next chunk.
+// Chunk 0 is reserved: its first word counts the chunks handed out.  So the
+// count pass keeps EVERY hit, in fill order, and heavy queries (C3: 3.6 % of
+// the queries hold 99 % of the hits) need no second traversal; only queries
+// that find the pool exhausted are traversed again by the fill pass.
+constexpr int kSpillChunk = 128;
+struct SpillPool {
+    int32_t *heads;   // per query, written when its count exceeds the row:
+                      // first chunk, or -1 = pool exhausted (fill pass)
+    int32_t *pool;    // chunks of kSpillChunk ints
+    uint32_t chunks;  // pool capacity in chunks, the reserved chunk included
 };
 
 // The 64-byte record in two 256-bit loads (sm_100 LDG.E.ENL2.256): kNN 8.30 vs
@@ -70,17 +85,15 @@ __device__ __forceinline__ bool emit(int32_t *__restrict__ out, int64_t base, in
 #ifndef LBVH_SPATIAL_BLOCK
 #define LBVH_SPATIAL_BLOCK 256
 #endif
+// One query q of a radius batch (spatial_pass for a single query).
 template <int MODE>
-__global__ void __launch_bounds__(LBVH_SPATIAL_BLOCK, 2048 / LBVH_SPATIAL_BLOCK)
-spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
-               const float *__restrict__ radii, float radius, const uint32_t *__restrict__ order,
-               int64_t nq, int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
-               int32_t *__restrict__ out, int64_t cap, const int32_t *__restrict__ skip,
-               uint32_t *status) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nq) return;
-    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
-    if (MODE == kFill && skip && __ldg(skip + q) <= cap) return;
+__device__ __forceinline__ void spatial_query(const lbvh_tree &t,
+                                              const float *__restrict__ centers,
+                                              const float *__restrict__ radii, float radius,
+                                              int64_t q, int32_t *__restrict__ counts,
+                                              const int64_t *__restrict__ offsets,
+                                              int32_t *__restrict__ out, int64_t cap,
+                                              uint32_t *status, const SpillPool pool = {}) {
     const float px = __ldg(centers + 3 * q), py = __ldg(centers + 3 * q + 1),
                 pz = __ldg(centers + 3 * q + 2);
     const float r = radii ? __ldg(radii + q) : radius;
@@ -89,10 +102,36 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
     if (MODE == kFill) base = __ldg(offsets + q);
     if (MODE == kBuffer || MODE == kCountBuf) base = q * cap;
     int32_t cnt = 0;
+    int32_t spill_cur = 0, spill_slot = 0;  // current pool chunk (0: none yet, -1: failed)
+    auto hit = [&](int32_t obj) -> bool {
+        if (MODE == kCountBuf && cnt >= cap) {
+            if (pool.pool && spill_cur >= 0) {
+                if (spill_cur == 0 || spill_slot == kSpillChunk - 1) {
+                    const uint32_t c = atomicAdd(reinterpret_cast<uint32_t *>(pool.pool), 1u) + 1u;
+                    if (c >= pool.chunks) {
+                        spill_cur = -1;
+                        pool.heads[q] = -1;
+                    } else {
+                        if (spill_cur == 0)
+                            pool.heads[q] = (int32_t)c;
+                        else
+                            pool.pool[(int64_t)spill_cur * kSpillChunk + kSpillChunk - 1] =
+                                (int32_t)c;
+                        spill_cur = (int32_t)c;
+                        spill_slot = 0;
+                    }
+                }
+                if (spill_cur > 0) pool.pool[(int64_t)spill_cur * kSpillChunk + spill_slot++] = obj;
+            }
+            ++cnt;
+            return true;
+        }
+        return emit<MODE>(out, base, cnt, cap, obj);
+    };
     if (t.n == 1) {
         const float *bx = t.root_box;
         if (box_dist_sq(px, py, pz, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]) <= r2)
-            emit<MODE>(out, base, cnt, cap, __ldg(t.leaf_obj));
+            hit(__ldg(t.leaf_obj));
         if (MODE != kFill) counts[q] = cnt;
         return;
     }
@@ -120,7 +159,7 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         // left child, then right child (_kernels.py:212-225)
         if (dl <= r2) {
             if (d.x < 0) {
-                if (!emit<MODE>(out, base, cnt, cap, d.x & 0x7FFFFFFF)) {
+                if (!hit(d.x & 0x7FFFFFFF)) {
                     fail = LBVH_FLAG_BUFFER_OVERFLOW;
                     break;
                 }
@@ -140,7 +179,7 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
         }
         if (dr <= r2) {
             if (d.y < 0) {
-                if (!emit<MODE>(out, base, cnt, cap, d.y & 0x7FFFFFFF)) {
+                if (!hit(d.y & 0x7FFFFFFF)) {
                     fail = LBVH_FLAG_BUFFER_OVERFLOW;
                     break;
                 }
@@ -168,6 +207,45 @@ spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
     }
     if (fail) atomicOr(status, fail);
     if (MODE != kFill) counts[q] = cnt;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(LBVH_SPATIAL_BLOCK, 2048 / LBVH_SPATIAL_BLOCK)
+spatial_kernel(const lbvh_tree t, const float *__restrict__ centers,
+               const float *__restrict__ radii, float radius, const uint32_t *__restrict__ order,
+               int64_t nq, int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
+               int32_t *__restrict__ out, int64_t cap, const int32_t *__restrict__ skip,
+               uint32_t *status, const SpillPool sp) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nq) return;
+    const int64_t q = order ? (int64_t)__ldg(order + s) : s;
+    if (MODE == kFill && skip && __ldg(skip + q) <= cap) return;
+    spatial_query<MODE>(t, centers, radii, radius, q, counts, offsets, out, cap, status, sp);
+}
+
+// The listed (heavy) queries of a 2P batch, in list (= traversal) order:
+// a persistent grid whose warps stride over 32-query chunks of the list, so
+// the queries in flight at any time are a contiguous stretch of it and
+// their node records stay in L2 (a one-wave launch over a long list keeps
+// every region of the cloud hot at once and re-reads the tree from HBM).
+#ifndef LBVH_LIST_CTAS_PER_SM
+#define LBVH_LIST_CTAS_PER_SM 4
+#endif
+template <int MODE>
+__global__ void __launch_bounds__(LBVH_SPATIAL_BLOCK, 2048 / LBVH_SPATIAL_BLOCK)
+spatial_list_kernel(const lbvh_tree t, const float *__restrict__ centers,
+                    const float *__restrict__ radii, float radius,
+                    const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_len,
+                    int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
+                    int32_t *__restrict__ out, uint32_t *status) {
+    const int64_t n = (int64_t)*list_len;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n;
+         i += stride) {
+        if (i < n)
+            spatial_query<MODE>(t, centers, radii, radius, (int64_t)__ldg(list + i), counts,
+                                offsets, out, 0, status);
+    }
 }
 
 // 5 resident CTAs per SM (<= 48 registers, no spills) with the 12-entry
@@ -595,7 +673,7 @@ template <int MODE>
 int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii, float radius,
                    const uint32_t *order, int64_t nq, int32_t *counts, const int64_t *offsets,
                    int32_t *out, int64_t cap, const int32_t *skip, uint32_t *status,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const SpillPool sp = {}) {
     if (!tree_ok(t) || nq < 0 || !status) return LBVH_ERR_INVALID_ARG;
     if (nq == 0) return LBVH_OK;
     if (!centers) return LBVH_ERR_INVALID_ARG;
@@ -603,7 +681,7 @@ int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii,
     if (MODE == kFill && !offsets) return LBVH_ERR_INVALID_ARG;
     if (nq >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     spatial_kernel<MODE><<<div_up(nq, LBVH_SPATIAL_BLOCK), LBVH_SPATIAL_BLOCK, 0, stream>>>(
-        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, skip, status);
+        *t, centers, radii, radius, order, nq, counts, offsets, out, cap, skip, status, sp);
     count_launches(1);
     return check_launch();
 }
@@ -612,14 +690,43 @@ int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii,
 
 int spatial_count(const lbvh_tree *t, const float *centers, const float *radii, float radius,
                   const uint32_t *order, int64_t nq, int32_t *counts, int32_t *buf, int64_t cap,
-                  uint32_t *status, cudaStream_t stream) {
+                  uint32_t *status, cudaStream_t stream, int32_t *spill_heads,
+                  int32_t *spill_pool, int64_t spill_chunks) {
     if (buf) {
         if (cap < 1) return LBVH_ERR_INVALID_ARG;
+        SpillPool sp = {};
+        if (spill_pool && spill_heads && spill_chunks > 1) {
+            sp = SpillPool{spill_heads, spill_pool,
+                           (uint32_t)(spill_chunks < (int64_t)1 << 31 ? spill_chunks
+                                                                      : (int64_t)1 << 31)};
+            cudaMemsetAsync(spill_pool, 0, sizeof(uint32_t), stream);  // allocation counter
+        }
         return launch_spatial<kCountBuf>(t, centers, radii, radius, order, nq, counts, nullptr,
-                                         buf, cap, nullptr, status, stream);
+                                         buf, cap, nullptr, status, stream, sp);
     }
     return launch_spatial<kCount>(t, centers, radii, radius, order, nq, counts, nullptr,
                                   nullptr, 0, nullptr, status, stream);
+}
+
+int spatial_list(const lbvh_tree *t, const float *centers, const float *radii, float radius,
+                 const uint32_t *list, const uint32_t *list_len, int64_t max_list,
+                 int32_t *counts, const int64_t *offsets, int32_t *out, bool fill,
+                 uint32_t *status, cudaStream_t stream) {
+    if (!tree_ok(t) || !centers || !list || !list_len || !status || max_list < 0)
+        return LBVH_ERR_INVALID_ARG;
+    if (fill ? (!offsets || !out) : !counts) return LBVH_ERR_INVALID_ARG;
+    if (max_list == 0) return LBVH_OK;
+    int64_t ctas = (max_list + LBVH_SPATIAL_BLOCK - 1) / LBVH_SPATIAL_BLOCK;
+    const int64_t cap = (int64_t)kNumSMs * LBVH_LIST_CTAS_PER_SM;
+    const unsigned g = (unsigned)(ctas < cap ? ctas : cap);
+    if (fill)
+        spatial_list_kernel<kFill><<<g, LBVH_SPATIAL_BLOCK, 0, stream>>>(
+            *t, centers, radii, radius, list, list_len, counts, offsets, out, status);
+    else
+        spatial_list_kernel<kCount><<<g, LBVH_SPATIAL_BLOCK, 0, stream>>>(
+            *t, centers, radii, radius, list, list_len, counts, offsets, out, status);
+    count_launches(1);
+    return check_launch();
 }
 
 int spatial_fill(const lbvh_tree *t, const float *centers, const float *radii, float radius,
@@ -797,35 +904,91 @@ unpack_knn_keys_kernel(const uint64_t *__restrict__ keys, int64_t n, int64_t *__
 namespace {
 // Queries whose hits overflowed their row, listed (in traversal order within
 // each warp) so the fill pass runs on full warps of them only.
-__global__ void __launch_bounds__(256)
-select_overflow_kernel(const uint32_t *__restrict__ order, const int32_t *__restrict__ counts,
-                       int64_t nq, int64_t cap, uint32_t *__restrict__ list, uint32_t *count) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t q = 0;
-    bool over = false;
-    if (s < nq) {
-        q = order ? __ldg(order + s) : (uint32_t)s;
-        over = __ldg(counts + q) > cap;
-    }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, over);
+// With spill heads: queries whose overflow hits all went to the pool go to
+// the spill list (copied by spill_copy_kernel), the others to `list`.
+__device__ __forceinline__ void append_warp(bool take, uint32_t q, uint32_t *list,
+                                            uint32_t *count) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
     if (!m) return;
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(m) - 1;
     uint32_t base = 0;
     if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
     base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    if (over) list[base + __popc(m & ((1u << lane) - 1u))] = q;
+    if (take) list[base + __popc(m & ((1u << lane) - 1u))] = q;
+}
+
+__global__ void __launch_bounds__(256)
+select_overflow_kernel(const uint32_t *__restrict__ order, const int32_t *__restrict__ counts,
+                       int64_t nq, int64_t cap, uint32_t *__restrict__ list, uint32_t *count,
+                       const int32_t *__restrict__ heads, uint32_t *__restrict__ spill_list,
+                       uint32_t *spill_count) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t q = 0;
+    bool over = false, spilled = false;
+    if (s < nq) {
+        q = order ? __ldg(order + s) : (uint32_t)s;
+        over = __ldg(counts + q) > cap;
+        if (over && heads) spilled = __ldg(heads + q) > 0;
+    }
+    append_warp(over && !spilled, q, list, count);
+    if (heads) append_warp(spilled, q, spill_list, spill_count);
+}
+
+// Spilled queries' spans: the row (first `cap` hits) then the pool chunks,
+// one warp per query, consecutive lanes on consecutive output words.
+__global__ void __launch_bounds__(256)
+spill_copy_kernel(const int32_t *__restrict__ buf, int64_t cap,
+                  const int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
+                  const int32_t *__restrict__ heads, const int32_t *__restrict__ pool,
+                  const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_len,
+                  int32_t *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = (int64_t)*list_len;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += warps) {
+        const int64_t q = __ldg(list + w);
+        const int64_t cnt = __ldg(counts + q);
+        int32_t *dst = out + __ldg(offsets + q);
+        const int32_t *row = buf + q * cap;
+        for (int64_t j = lane; j < cap; j += 32) dst[j] = __ldcs(row + j);
+        int64_t c = __ldg(heads + q), done = cap;
+        while (done < cnt) {
+            const int64_t take = cnt - done < kSpillChunk - 1 ? cnt - done : kSpillChunk - 1;
+            const int32_t *ch = pool + c * kSpillChunk;
+            for (int64_t j = lane; j < take; j += 32) dst[done + j] = __ldcs(ch + j);
+            done += take;
+            if (done < cnt) c = __ldg(ch + kSpillChunk - 1);
+        }
+    }
 }
 }  // namespace
 
 int select_overflow(const uint32_t *order, const int32_t *counts, int64_t nq, int64_t cap,
-                    uint32_t *list, uint32_t *count, cudaStream_t stream) {
+                    uint32_t *list, uint32_t *count, cudaStream_t stream,
+                    const int32_t *spill_heads, uint32_t *spill_list, uint32_t *spill_count) {
     if (nq < 0 || (nq > 0 && (!counts || !list || !count))) return LBVH_ERR_INVALID_ARG;
-    if (!count) return LBVH_ERR_INVALID_ARG;
+    if (!count || (spill_heads && (!spill_list || !spill_count))) return LBVH_ERR_INVALID_ARG;
     cudaMemsetAsync(count, 0, sizeof(uint32_t), stream);
+    if (spill_heads) cudaMemsetAsync(spill_count, 0, sizeof(uint32_t), stream);
     if (nq == 0) return check_launch();
-    select_overflow_kernel<<<div_up(nq, 256), 256, 0, stream>>>(order, counts, nq, cap, list,
-                                                                count);
+    select_overflow_kernel<<<div_up(nq, 256), 256, 0, stream>>>(
+        order, counts, nq, cap, list, count, spill_heads, spill_list, spill_count);
+    count_launches(1);
+    return check_launch();
+}
+
+int spill_copy(const int32_t *buf, int64_t cap, const int32_t *counts, const int64_t *offsets,
+               const int32_t *heads, const int32_t *pool, const uint32_t *list,
+               const uint32_t *list_len, int64_t max_list, int32_t *out, cudaStream_t stream) {
+    if (max_list < 0 || cap < 1) return LBVH_ERR_INVALID_ARG;
+    if (max_list == 0) return LBVH_OK;
+    if (!buf || !counts || !offsets || !heads || !pool || !list || !list_len || !out)
+        return LBVH_ERR_INVALID_ARG;
+    int64_t ctas = (max_list + 7) / 8;
+    const int64_t lim = (int64_t)kNumSMs * 8;
+    spill_copy_kernel<<<(unsigned)(ctas < lim ? ctas : lim), 256, 0, stream>>>(
+        buf, cap, counts, offsets, heads, pool, list, list_len, out);
     count_launches(1);
     return check_launch();
 }

@@ -332,6 +332,25 @@ def _finish(host: bool, status: dv.Status, *arrays):
 # buffer is skipped when it would exceed _ROW_BUDGET bytes.
 _ROW_HITS = 48
 _ROW_BUDGET = 8 << 30
+# Hits beyond the row are kept by the count pass in a pool of 128-int chunks
+# (lbvh_spatial_count_batch's spill pool), so heavy queries are traversed
+# once; sized at _SPILL_INTS ints per query (C3 needs ~8.2), a query that
+# finds it exhausted falls back to the fill pass.
+_SPILL_INTS = 16
+
+
+def _spill_args(sp):
+    if sp is None:
+        return (None, None, 0, None, None)
+    return (dv.ptr(sp["heads"]), dv.ptr(sp["pool"]), sp["chunks"], dv.ptr(sp["list"]),
+            dv.ptr(sp["n"]))
+
+
+def _spill_arrays(nq: int):
+    chunks = min(max(64, nq * _SPILL_INTS // _lib.SPILL_CHUNK), _ROW_BUDGET // (4 * _lib.SPILL_CHUNK))
+    return dict(heads=dv.empty(nq, torch.int32),
+                pool=dv.empty((chunks + 1) * _lib.SPILL_CHUNK, torch.int32), chunks=chunks + 1,
+                list=dv.empty(nq, torch.int32), n=dv.empty(1, torch.int32))
 
 
 def _spatial_2p_fused(tree: Bvh, b: _Batch, sort_queries: bool, status: dv.Status):
@@ -349,12 +368,14 @@ def _spatial_2p_fused(tree: Bvh, b: _Batch, sort_queries: bool, status: dv.Statu
     order = dv.empty(nq, torch.int32)
     over_list = dv.empty(nq, torch.int32) if rows else None
     over_n = dv.empty(1, torch.int32)
+    sp = _spill_arrays(nq) if rows else None
     ws = dv.workspace(l.lbvh_spatial_count_batch_workspace_bytes(nq))
     evs = _kernel_events("spatial_count")
     _lib.check(l.lbvh_spatial_count_batch(
         ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, nq, _ORDER_BITS if sort_queries else 0,
         rows, dv.ptr(order), dv.ptr(counts), dv.ptr(buf), dv.ptr(offsets), dv.ptr(over_list),
-        dv.ptr(over_n), dv.ptr(ws), ws.numel(), status.ptr, evs[0], evs[1], st))
+        dv.ptr(over_n), *(_spill_args(sp)), dv.ptr(ws), ws.numel(), status.ptr, evs[0], evs[1],
+        st))
     flags, total, n_over = dv.d2h_many(status.dev, offsets[nq:], over_n)
     _raise_flags(int(flags[0]) & 0xFFFFFFFF)
     total, n_over = int(total[0]), int(n_over[0])
@@ -363,58 +384,19 @@ def _spatial_2p_fused(tree: Bvh, b: _Batch, sort_queries: bool, status: dv.Statu
         if rows:
             _lib.check(l.lbvh_compact(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), nq,
                                       dv.ptr(out), st))
+            _lib.check(l.lbvh_spill_copy(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets),
+                                         dv.ptr(sp["heads"]), dv.ptr(sp["pool"]),
+                                         dv.ptr(sp["list"]), dv.ptr(sp["n"]), nq, dv.ptr(out),
+                                         st))
             if n_over:
-                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
-                    ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(over_list), n_over,
-                    dv.ptr(offsets), dv.ptr(out), None, 0, status.ptr, st)))
+                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill_list(
+                    ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(over_list),
+                    dv.ptr(over_n), n_over, dv.ptr(offsets), dv.ptr(out), status.ptr, st)))
         else:
             _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
                 ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius,
                 dv.ptr(order) if sort_queries and nq > 1 else None, nq, dv.ptr(offsets),
                 dv.ptr(out), None, 0, status.ptr, st)))
-    return offsets, out
-
-
-def _spatial_2p_device(tree: Bvh, b: _Batch, order, status: dv.Status):
-    l = _lib.lib()
-    ct = tree.ctree()
-    st = dv.stream()
-    nq = b.nq
-    counts = dv.empty(nq, torch.int32)
-    rows = next((r for r in (_ROW_HITS, _ROW_HITS // 2) if r and nq * r * 4 <= _ROW_BUDGET), 0)
-    buf = dv.empty((nq, rows), torch.int32) if rows else None
-    _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
-        ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq, dv.ptr(counts),
-        dv.ptr(buf), rows, status.ptr, st)))
-    offsets = dv.empty(nq + 1, torch.int64)
-    ws = dv.workspace(l.lbvh_scan_workspace_bytes(nq))
-    _lib.check(l.lbvh_exclusive_scan(dv.ptr(counts), nq, dv.ptr(offsets), dv.ptr(ws),
-                                     ws.numel(), st))
-    if rows:
-        # queries whose hits did not fit their row, listed for a dense fill pass
-        over_list = dv.empty(nq, torch.int32)
-        over_n = dv.empty(1, torch.int32)
-        _lib.check(l.lbvh_select_overflow(dv.ptr(order), dv.ptr(counts), nq, rows,
-                                          dv.ptr(over_list), dv.ptr(over_n), st))
-        flags, total, n_over = dv.d2h_many(status.dev, offsets[nq:], over_n)
-        n_over = int(n_over[0])
-    else:
-        flags, total = dv.d2h_many(status.dev, offsets[nq:])
-    _raise_flags(int(flags[0]) & 0xFFFFFFFF)
-    total = int(total[0])
-    out = dv.empty(total, torch.int32)
-    if total:
-        if rows:
-            _lib.check(l.lbvh_compact(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), nq,
-                                      dv.ptr(out), st))
-            if n_over:
-                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
-                    ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(over_list), n_over,
-                    dv.ptr(offsets), dv.ptr(out), None, 0, status.ptr, st)))
-        else:
-            _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
-                ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(order), nq,
-                dv.ptr(offsets), dv.ptr(out), None, 0, status.ptr, st)))
     return offsets, out
 
 
@@ -455,15 +437,14 @@ def _spatial_2p_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet
     host_c = dv.as_tensor(b.host_centers)
     dev_c = torch.empty((nq, 3), dtype=torch.float32, device=dev)
     ct = tree.ctree()
-    root_box = dv.ptr(tree._device()["root_box"])
     rows = _ROW_HITS
     nch = -(-nq // C)
-    ws = dv.workspace(max(l.lbvh_query_workspace_bytes(C), l.lbvh_scan_workspace_bytes(C)))
+    ws = dv.workspace(l.lbvh_spatial_count_batch_workspace_bytes(C))
     slots = [dict(counts=dv.empty(C, torch.int32), buf=dv.empty((C, rows), torch.int32),
                   offs=dv.empty(C + 1, torch.int64), over=dv.empty(C, torch.int32),
                   over_n=dv.empty(1, torch.int32), order=dv.empty(C, torch.int32),
                   tot_h=dv.pinned(1, torch.int64), over_h=dv.pinned(1, torch.int32),
-                  ev=torch.cuda.Event()) for _ in range(2)]
+                  spill=_spill_arrays(C), ev=torch.cuda.Event()) for _ in range(2)]
     h_off = dv.pinned(nq + 1, torch.int64)
     h_off[0] = 0
     cap = max(nq * 16, 1 << 20)
@@ -484,19 +465,13 @@ def _spatial_2p_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet
         comp.wait_event(e_in)
         cc = c_ptr + 12 * c0
         st = comp.cuda_stream
-        _lib.check(l.lbvh_check_queries(cc, m, None, status.ptr, st))
-        srt = sort_queries and m > 1
-        order = dv.ptr(sl["order"]) if srt else None
-        if srt:
-            _lib.check(l.lbvh_query_order(cc, m, root_box, _ORDER_BITS, order, None,
-                                          dv.ptr(ws), ws.numel(), st))
-        _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count(
-            ct, cc, None, b.radius, order, m, dv.ptr(sl["counts"]), dv.ptr(sl["buf"]), rows,
-            status.ptr, st)))
-        _lib.check(l.lbvh_exclusive_scan(dv.ptr(sl["counts"]), m, dv.ptr(sl["offs"]),
-                                         dv.ptr(ws), ws.numel(), st))
-        _lib.check(l.lbvh_select_overflow(order, dv.ptr(sl["counts"]), m, rows,
-                                          dv.ptr(sl["over"]), dv.ptr(sl["over_n"]), st))
+        # value check, query order, count (+ warp-packet pass for heavy
+        # queries), scan and overflow list in one call
+        _lib.check(_launch("spatial_count", lambda: l.lbvh_spatial_count_batch(
+            ct, cc, None, b.radius, m, _ORDER_BITS if sort_queries else 0, rows,
+            dv.ptr(sl["order"]), dv.ptr(sl["counts"]), dv.ptr(sl["buf"]), dv.ptr(sl["offs"]),
+            dv.ptr(sl["over"]), dv.ptr(sl["over_n"]), *(_spill_args(sl["spill"])), dv.ptr(ws),
+            ws.numel(), status.ptr, None, None, st)))
         sl["tot_h"].copy_(sl["offs"][m:m + 1], non_blocking=True)
         sl["over_h"].copy_(sl["over_n"], non_blocking=True)
         sl["ev"].record(comp)
@@ -512,10 +487,16 @@ def _spatial_2p_pipelined(tree: Bvh, b: _Batch, sort_queries: bool) -> ResultSet
         if total:
             _lib.check(l.lbvh_compact(dv.ptr(sl["buf"]), rows, dv.ptr(sl["counts"]),
                                       dv.ptr(sl["offs"]), m, dv.ptr(out), st))
+            sp = sl["spill"]
+            _lib.check(l.lbvh_spill_copy(dv.ptr(sl["buf"]), rows, dv.ptr(sl["counts"]),
+                                         dv.ptr(sl["offs"]), dv.ptr(sp["heads"]),
+                                         dv.ptr(sp["pool"]), dv.ptr(sp["list"]),
+                                         dv.ptr(sp["n"]), m, dv.ptr(out), st))
             if n_over:
-                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill(
-                    ct, c_ptr + 12 * c0, None, b.radius, dv.ptr(sl["over"]), n_over,
-                    dv.ptr(sl["offs"]), dv.ptr(out), None, 0, status.ptr, st)))
+                _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill_list(
+                    ct, c_ptr + 12 * c0, None, b.radius, dv.ptr(sl["over"]),
+                    dv.ptr(sl["over_n"]), n_over, dv.ptr(sl["offs"]), dv.ptr(out), status.ptr,
+                    st)))
         goff = sl["offs"][1:m + 1] + base
         if base + total > cap:  # grow the host hit buffer (rare)
             s_out.synchronize()
@@ -578,7 +559,7 @@ def query_spatial_1p(tree: Bvh, queries, buffer_size: int, sort_queries: bool = 
     if flags & _lib.FLAG_BUFFER_OVERFLOW:
         del buf
         status = dv.Status()
-        offsets, out = _spatial_2p_device(tree, b, order, status)
+        offsets, out = _spatial_2p_fused(tree, b, sort_queries, status)
         offsets, out = _finish(b.host, status, offsets, out)
         return ResultSet._trusted(offsets, out), True
     total = int(total[0])

@@ -251,7 +251,7 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
                             bits, _lib.BUILD_DEFER_ROWS, status.ptr, dv.stream())))
     d["rows_pending"] = True
     d["flags"] = ((_lib.TREE_POINT_LEAVES if maxs is mins else 0)
-                  | (_lib.TREE_CODES30 if morton_bits == 30 else 0))
+                  | (_lib.TREE_CODES30 if morton_bits == 30 else 0) | _lib.TREE_BUILT)
     if check:
         flags = status.read()
         if flags & _lib.FLAG_NONFINITE:

@@ -378,3 +378,55 @@ def test_volumetric_boxes_knn_and_radius_device(k):
     so, si = oracle.query_spatial_2p(ref, q, 1.5)
     rs = lb.query_spatial_2p(t, (torch.from_numpy(q).cuda(), 1.5)).to_host()
     assert np.array_equal(rs.offsets, so) and np.array_equal(rs.indices, si)
+
+
+@pytest.mark.parametrize("shape,radius_scale", [("sphere:hollow", 1.0), ("sphere:hollow", 4.0),
+                                                ("cube:filled", 3.0)])
+def test_heavy_queries_spill_pool(shape, radius_scale, monkeypatch):
+    """Queries with more hits than the 2P row (48) keep the rest in the spill
+    pool during the count pass (no second traversal); with the pool too small
+    they fall back to the fill pass.  Counts, offsets and the UNSORTED hit
+    order must be the reference's (oracle) either way, for scalar and
+    per-query radii, device and host batches, and the 1P fallback."""
+    pts = datasets.generate(datasets.CloudSpec.parse(shape, 200_000, 3))
+    q = datasets.generate(datasets.CloudSpec.parse("cube:filled", 40_003, 4))
+    t, ref = lb.build(pts), oracle.build(pts)
+    r = np.float32(datasets.default_radius(10) * radius_scale)
+    off, idx = oracle.query_spatial_2p(ref, q, r)
+    assert int(np.diff(off).max()) > 48  # heavy queries exist
+    rs = lb.query_spatial_2p(t, (q, r))
+    assert np.array_equal(rs.offsets, off) and np.array_equal(rs.indices, idx)
+    rd = lb.query_spatial_2p(t, (torch.from_numpy(q).cuda(), r))
+    assert np.array_equal(rd.offsets.cpu().numpy(), off)
+    assert np.array_equal(rd.indices.cpu().numpy(), idx)
+    rr = np.random.default_rng(5).uniform(0, 2 * r, q.shape[0]).astype(np.float32)
+    rr[::7] = 0.0
+    off2, idx2 = oracle.query_spatial_2p(ref, q, rr)
+    rs2 = lb.query_spatial_2p(t, (q, rr))
+    assert np.array_equal(rs2.offsets, off2) and np.array_equal(rs2.indices, idx2)
+    rs3, fb = lb.query_spatial_1p(t, (q, r), 16)
+    assert fb and np.array_equal(rs3.offsets, off) and np.array_equal(rs3.indices, idx)
+    rs4 = lb.query_spatial_2p(t, (q, r), sort_queries=False)
+    assert np.array_equal(rs4.offsets, off) and np.array_equal(rs4.indices, idx)
+    # a pool of 64 chunks runs dry: the queries that find it exhausted are refilled
+    from paper_1908_11807_b200 import traversal
+
+    monkeypatch.setattr(traversal, "_SPILL_INTS", 0)
+    rs5 = lb.query_spatial_2p(t, (q, r))
+    assert np.array_equal(rs5.offsets, off) and np.array_equal(rs5.indices, idx)
+
+
+def test_heavy_queries_pipelined_host_batch():
+    """A pinned host batch above the pipeline threshold (2^20 queries) with
+    heavy queries: chunked count (+ spill pool) / compaction / spill copy /
+    D2H."""
+    pts = datasets.generate(datasets.CloudSpec("sphere", "hollow", 300_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", (1 << 20) + 4097, 1))
+    t, ref = lb.build(pts), oracle.build(pts)
+    r = np.float32(datasets.default_radius(10) * 2.0)
+    pin = torch.empty(q.shape, dtype=torch.float32, pin_memory=True)
+    pin.numpy()[:] = q
+    rs = lb.query_spatial_2p(t, (pin.numpy(), r))
+    off, idx = oracle.query_spatial_2p(ref, q, r)
+    assert int(np.diff(off).max()) > 48
+    assert np.array_equal(rs.offsets, off) and np.array_equal(rs.indices, idx)
