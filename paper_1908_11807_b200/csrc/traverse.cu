@@ -936,13 +936,16 @@ select_overflow_kernel(const uint32_t *__restrict__ order, const int32_t *__rest
 }
 
 // Spilled queries' spans: the row (first `cap` hits) then the pool chunks,
-// one warp per query, consecutive lanes on consecutive output words.
+// one warp per query, consecutive lanes on consecutive output words; each
+// lane has all of its loads of a chunk in flight before it stores, and the
+// next chunk's index is read with them.
 __global__ void __launch_bounds__(256)
 spill_copy_kernel(const int32_t *__restrict__ buf, int64_t cap,
                   const int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
                   const int32_t *__restrict__ heads, const int32_t *__restrict__ pool,
                   const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_len,
                   int32_t *__restrict__ out) {
+    constexpr int kPer = (kSpillChunk + 31) / 32;  // words per lane per chunk
     const int lane = threadIdx.x & 31;
     const int64_t n = (int64_t)*list_len;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -950,15 +953,39 @@ spill_copy_kernel(const int32_t *__restrict__ buf, int64_t cap,
         const int64_t q = __ldg(list + w);
         const int64_t cnt = __ldg(counts + q);
         int32_t *dst = out + __ldg(offsets + q);
+        int64_t c = __ldg(heads + q);
         const int32_t *row = buf + q * cap;
-        for (int64_t j = lane; j < cap; j += 32) dst[j] = __ldcs(row + j);
-        int64_t c = __ldg(heads + q), done = cap;
+        for (int64_t j0 = 0; j0 < cap; j0 += 32 * kPer) {
+            int32_t v[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int64_t j = j0 + u * 32 + lane;
+                v[u] = j < cap ? __ldcs(row + j) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int64_t j = j0 + u * 32 + lane;
+                if (j < cap) dst[j] = v[u];
+            }
+        }
+        int64_t done = cap;
         while (done < cnt) {
             const int64_t take = cnt - done < kSpillChunk - 1 ? cnt - done : kSpillChunk - 1;
             const int32_t *ch = pool + c * kSpillChunk;
-            for (int64_t j = lane; j < take; j += 32) dst[done + j] = __ldcs(ch + j);
+            int32_t v[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int j = u * 32 + lane;
+                v[u] = j < kSpillChunk ? __ldcs(ch + j) : 0;  // slot 127: the next chunk
+            }
+            const int64_t next = __shfl_sync(0xFFFFFFFFu, v[kPer - 1], 31);
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int j = u * 32 + lane;
+                if (j < take) dst[done + j] = v[u];
+            }
             done += take;
-            if (done < cnt) c = __ldg(ch + kSpillChunk - 1);
+            c = next;
         }
     }
 }

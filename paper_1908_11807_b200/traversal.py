@@ -376,18 +376,20 @@ def _spatial_2p_fused(tree: Bvh, b: _Batch, sort_queries: bool, status: dv.Statu
         rows, dv.ptr(order), dv.ptr(counts), dv.ptr(buf), dv.ptr(offsets), dv.ptr(over_list),
         dv.ptr(over_n), *(_spill_args(sp)), dv.ptr(ws), ws.numel(), status.ptr, evs[0], evs[1],
         st))
-    flags, total, n_over = dv.d2h_many(status.dev, offsets[nq:], over_n)
+    flags, total, n_over, n_spill = dv.d2h_many(status.dev, offsets[nq:], over_n,
+                                                sp["n"] if sp else over_n)
     _raise_flags(int(flags[0]) & 0xFFFFFFFF)
-    total, n_over = int(total[0]), int(n_over[0])
+    total, n_over, n_spill = int(total[0]), int(n_over[0]), int(n_spill[0]) if sp else 0
     out = dv.empty(total, torch.int32)
     if total:
         if rows:
             _lib.check(l.lbvh_compact(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), nq,
                                       dv.ptr(out), st))
-            _lib.check(l.lbvh_spill_copy(dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets),
-                                         dv.ptr(sp["heads"]), dv.ptr(sp["pool"]),
-                                         dv.ptr(sp["list"]), dv.ptr(sp["n"]), nq, dv.ptr(out),
-                                         st))
+            if n_spill:
+                _lib.check(l.lbvh_spill_copy(
+                    dv.ptr(buf), rows, dv.ptr(counts), dv.ptr(offsets), dv.ptr(sp["heads"]),
+                    dv.ptr(sp["pool"]), dv.ptr(sp["list"]), dv.ptr(sp["n"]), n_spill,
+                    dv.ptr(out), st))
             if n_over:
                 _lib.check(_launch("spatial_fill", lambda: l.lbvh_spatial_fill_list(
                     ct, dv.ptr(b.centers), dv.ptr(b.radii), b.radius, dv.ptr(over_list),
