@@ -121,6 +121,11 @@ size_t lbvh_sort_workspace_bytes(int64_t n);
  * (bit-identical) when the caller first needs the reference layout.  The
  * packed records, node_mins leaf rows, left/right and leaf_obj are always
  * written.
+ * leaf_ids (optional, may be NULL): n i32 ordinals in [0, 2^31) reported for
+ * the inputs -- leaf_obj[p] and the packed leaf links hold leaf_ids[index]
+ * instead of the index (a shard of a distributed cloud reports global
+ * ordinals; ties still break by input index, which must then follow the
+ * ordinals' order).
  * morton_bits: 30 = the reference's codes (bit-exact tree); 63 = 21 bits per
  * axis, the same recipe (north_star "30/63-bit"; not in the reference, so
  * its parity is pinned only by the oracle restatement).  Leaves are then
@@ -130,7 +135,7 @@ int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
                void *workspace, size_t workspace_bytes, float *node_mins, float *node_maxs,
                int32_t *left, int32_t *right, int32_t *leaf_obj, float *root_box,
                void *nodes, uint32_t *sorted_codes, uint32_t *leaf_dir, int leaf_dir_bits,
-               int flags, uint32_t *status, void *stream);
+               int flags, const int32_t *leaf_ids, uint32_t *status, void *stream);
 #define LBVH_BUILD_DEFER_ROWS 0x1
 
 /* The rows an LBVH_BUILD_DEFER_ROWS build left out (internal rows from the

@@ -70,7 +70,8 @@ _SIGS = {
     "lbvh_scan_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "lbvh_build": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                     ctypes.c_void_p, ctypes.c_size_t] + [ctypes.c_void_p] * 9
-                   + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+                   + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p], ctypes.c_int),
     "lbvh_finish_rows": ([ctypes.POINTER(CTree), ctypes.c_void_p, ctypes.c_void_p,
                           ctypes.c_void_p], ctypes.c_int),
     "lbvh_morton_codes": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,

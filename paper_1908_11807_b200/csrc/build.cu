@@ -315,7 +315,7 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
                        float *__restrict__ root_box, uint32_t *__restrict__ leaf_codes,
                        uint32_t *__restrict__ leaf_dir, int dir_bits, DirRun *runs,
                        uint32_t *run_count, uint2 *__restrict__ frontier,
-                       uint32_t *frontier_count) {
+                       uint32_t *frontier_count, const int32_t *__restrict__ leaf_ids) {
     __shared__ uint32_t s_slot[kHierT];
     __shared__ float s_box[2][6][kHierT];
     __shared__ int32_t s_link[2][kHierT];
@@ -364,7 +364,9 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
                         run_count);
         }
         const uint32_t obj = __ldg(perm + p);
-        leaf_obj[p] = (int32_t)obj;
+        // the ordinal this leaf reports: its input index, or leaf_ids[index]
+        const uint32_t gobj = leaf_ids ? (uint32_t)__ldg(leaf_ids + obj) : obj;
+        leaf_obj[p] = (int32_t)gobj;
         const bool same = (mins == maxs);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -376,7 +378,7 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
             node_mins[3 * (internal + p) + a] = mine.lo[a];
             if (leaf_maxs_rows) node_maxs[3 * (internal + p) + a] = mine.hi[a];
         }
-        my_link = (int32_t)(obj | kLeafTag);
+        my_link = (int32_t)(gobj | kLeafTag);
         if (n == 1) {  // leaf-only tree (tree.py:177-209 with n == 1)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -483,7 +485,7 @@ __device__ __forceinline__ void frontier_box(const PackedNode *nodes, const floa
 
 template <typename CodeT>
 __global__ void __launch_bounds__(256)
-hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__restrict__ perm,
+hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const int32_t *__restrict__ leaf_obj,
                           int64_t n, uint32_t *slots, const float *node_mins,
                           const float *node_maxs, bool leaf_maxs_rows,
                           int32_t *__restrict__ left, int32_t *__restrict__ right,
@@ -510,7 +512,7 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__res
         if (l == r) {  // a leaf (row written by the local kernel)
             frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, internal + l,
                          mine);
-            my_link = (int32_t)(__ldg(perm + l) | kLeafTag);
+            my_link = (int32_t)((uint32_t)__ldg(leaf_obj + l) | kLeafTag);
         } else {       // an internal node built by the local kernel
             const int64_t id = is_left_child(codes, n, l, r) ? r : l;
             frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, id, mine);
@@ -540,7 +542,8 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const uint32_t *__res
             frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, sib, sb);
             const int32_t sib_link = sib < internal
                                          ? (int32_t)sib
-                                         : (int32_t)(__ldg(perm + (sib - internal)) | kLeafTag);
+                                         : (int32_t)((uint32_t)__ldg(leaf_obj + (sib - internal)) |
+                                                     kLeafTag);
             const Box &L = left_side ? mine : sb;
             const Box &R = left_side ? sb : mine;
             Box P;
@@ -732,8 +735,8 @@ template <typename CodeT>
 int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t ws_bytes,
                float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
                int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
-               uint32_t *leaf_dir, int dir_bits, int flags, uint32_t *status,
-               cudaStream_t stream) {
+               uint32_t *leaf_dir, int dir_bits, int flags, const int32_t *leaf_ids,
+               uint32_t *status, cudaStream_t stream) {
     Carve c(ws, ws_bytes);
     CodeT *codes = c.take<CodeT>(n);
     uint32_t *perm = c.take<uint32_t>(n);
@@ -763,9 +766,9 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
     hierarchy_local_kernel<CodeT><<<div_up(n, kHierT), kHierT, 0, stream>>>(
         codes, perm, mins, maxs, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
         leaf_obj, (PackedNode *)nodes, root_box, sorted_codes, leaf_dir, dir_bits, runs,
-        counter + 3, frontier, counter + 2);
+        counter + 3, frontier, counter + 2, leaf_ids);
     hierarchy_frontier_kernel<CodeT><<<grid_for(n / 64 + 1, 256, 8), 256, 0, stream>>>(
-        codes, perm, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
+        codes, leaf_obj, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
         (PackedNode *)nodes, root_box, frontier, counter + 2, leaf_dir, runs, counter + 3);
     count_launches(2);
     if (!defer && n > 1) {
@@ -780,8 +783,8 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
 int build(const float *mins, const float *maxs, int64_t n, int morton_bits, void *ws,
           size_t ws_bytes, float *node_mins, float *node_maxs, int32_t *left, int32_t *right,
           int32_t *leaf_obj, float *root_box, void *nodes, uint32_t *sorted_codes,
-          uint32_t *leaf_dir, int leaf_dir_bits, int flags, uint32_t *status,
-          cudaStream_t stream) {
+          uint32_t *leaf_dir, int leaf_dir_bits, int flags, const int32_t *leaf_ids,
+          uint32_t *status, cudaStream_t stream) {
     if (n == 0) return LBVH_ERR_EMPTY_SCENE;
     if (n < 0 || !mins || !maxs || !node_mins || !node_maxs || !leaf_obj || !root_box ||
         !status || (morton_bits != 30 && morton_bits != 63))
@@ -794,10 +797,10 @@ int build(const float *mins, const float *maxs, int64_t n, int morton_bits, void
     if (morton_bits == 63)
         return build_impl<uint64_t>(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left,
                                     right, leaf_obj, root_box, nodes, sorted_codes, leaf_dir,
-                                    leaf_dir_bits, flags, status, stream);
+                                    leaf_dir_bits, flags, leaf_ids, status, stream);
     return build_impl<uint32_t>(mins, maxs, n, ws, ws_bytes, node_mins, node_maxs, left, right,
                                 leaf_obj, root_box, nodes, sorted_codes, leaf_dir,
-                                leaf_dir_bits, flags, status, stream);
+                                leaf_dir_bits, flags, leaf_ids, status, stream);
 }
 
 int finish_rows(const lbvh_tree *t, float *node_mins, float *node_maxs, cudaStream_t stream) {

@@ -34,7 +34,7 @@ int check_launch() {
 size_t build_workspace_bytes(int64_t n);
 int build(const float *, const float *, int64_t, int, void *, size_t, float *, float *,
           int32_t *, int32_t *, int32_t *, float *, void *, uint32_t *, uint32_t *, int, int,
-          uint32_t *, cudaStream_t);
+          const int32_t *, uint32_t *, cudaStream_t);
 int finish_rows(const lbvh_tree *, float *, float *, cudaStream_t);
 size_t topology_workspace_bytes(int64_t n);
 int generate_topology(const uint32_t *, int64_t, int32_t *, int32_t *, int32_t *, void *, size_t,
@@ -122,10 +122,10 @@ int lbvh_build(const float *mins, const float *maxs, int64_t n, int morton_bits,
                size_t ws_bytes, float *node_mins, float *node_maxs, int32_t *left,
                int32_t *right, int32_t *leaf_obj, float *root_box, void *nodes,
                uint32_t *sorted_codes, uint32_t *leaf_dir, int leaf_dir_bits, int flags,
-               uint32_t *status, void *stream) {
+               const int32_t *leaf_ids, uint32_t *status, void *stream) {
     return build(mins, maxs, n, morton_bits, ws, ws_bytes, node_mins, node_maxs, left, right,
                  leaf_obj, root_box, nodes, sorted_codes, leaf_dir, leaf_dir_bits, flags,
-                 status, S(stream));
+                 leaf_ids, status, S(stream));
 }
 
 int lbvh_finish_rows(const lbvh_tree *tree, float *node_mins, float *node_maxs, void *stream) {

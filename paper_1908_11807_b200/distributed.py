@@ -91,10 +91,14 @@ class GpuEngine:
                                                         dv.stream()))
         return codes
 
-    def build(self, pts: torch.Tensor):
-        from .tree import build
+    def build(self, pts: torch.Tensor, gids: torch.Tensor | None = None):
+        """Local BVH; with ``gids`` its leaves report those (global) ordinals."""
+        from .tree import build, build_device
 
-        return build(pts.contiguous())
+        if gids is None:
+            return build(pts.contiguous())
+        p = pts.contiguous()
+        return build_device(p, p, leaf_ids=gids.to(torch.int32).contiguous())
 
     def box(self, tree) -> torch.Tensor:
         return tree._device()["root_box"].clone()
@@ -266,6 +270,8 @@ def _all_reduce(x: torch.Tensor, op, group):
 
 
 def _all_gather(x: torch.Tensor, world: int, group):
+    if world == 1:  # nothing to exchange
+        return [x]
     cdev = _comm_device(group, x.device)
     y = x.to(cdev)
     out = [torch.empty_like(y) for _ in range(world)]
@@ -330,62 +336,97 @@ def build_distributed(local_points, global_offset: int, engine=None, group=None,
     engine = engine or GpuEngine()
     dev = engine.device
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    pts = torch.as_tensor(local_points, dtype=torch.float32).to(dev).reshape(-1, 3)
+    pts = torch.as_tensor(local_points, dtype=torch.float32).to(dev).reshape(-1, 3).contiguous()
     n = int(pts.shape[0])
-    # 1. global scene box
-    if n:
-        lo, hi = pts.min(dim=0).values, pts.max(dim=0).values
+    # every rank's ordinal range: the total, the payload width, and whether
+    # received primitives arrive in global ordinal order
+    ranges = _all_gather(torch.tensor([int(global_offset), n], dtype=torch.int64, device=dev),
+                         world, group)
+    ranges = ([(int(global_offset), n)] if world == 1 else
+              [(int(r[0]), int(r[1])) for r in torch.stack(ranges).cpu()])
+    total = sum(c for _, c in ranges)
+    # GPU engine: the local build writes global ordinals straight into its
+    # leaves (lbvh_build leaf_ids), so local searches report -- and break
+    # distance ties by -- global ordinals
+    global_ids = hasattr(engine, "globalize") and total < 2 ** 31
+    gdt = torch.int32 if global_ids else torch.int64
+    gids = torch.arange(int(global_offset), int(global_offset) + n, dtype=gdt, device=dev)
+    scene_lo = scene_hi = None
+    if world > 1:
+        # 1. global scene box: one all-reduce (MAX) of (-min, max)
+        if n:
+            box = torch.cat([-pts.amin(dim=0), pts.amax(dim=0)])
+        else:
+            box = torch.full((6,), -math.inf, device=dev)
+        box = _all_reduce(box, dist.ReduceOp.MAX, group)
+        scene = torch.cat([-box[:3], box[3:]]).contiguous()
+        scene_h = scene.cpu().numpy().astype(np.float64)
+        scene_lo, scene_hi = scene_h[:3], scene_h[3:]
+        # 2. keys on the global grid: (30-bit code << 32) | global ordinal
+        if hasattr(engine, "morton32"):  # f32 points on a device box: no f64 staging
+            codes = engine.morton32(pts, scene).to(torch.int64)
+        else:
+            codes = engine.morton(pts, scene_lo, scene_hi)
+        keys = (codes << 32) | gids.to(torch.int64)
+        # 3. splitters from a strided sample of the (unsorted) keys: exact
+        #    results for any splitters, the sample only sets the balance
+        s = samples_per_rank
+        if n:
+            pick = torch.linspace(0, n - 1, s, device=dev).round().to(torch.int64)
+            sample = keys[pick]
+        else:
+            sample = torch.full((s,), torch.iinfo(torch.int64).max, dtype=torch.int64,
+                                device=dev)
+        gathered = _all_gather(sample, world, group)
+        allsamp = torch.sort(torch.cat(gathered)).values
+        cut = [allsamp[(i * allsamp.numel()) // world] for i in range(1, world)]
+        splitters = torch.stack(cut)
+        dest = torch.searchsorted(splitters, keys, right=True)
+        # primitives travel as 32-bit words: f32 x, y, z and the global
+        # ordinal (one word below 2^31, else two)
+        wide = max(o + c for o, c in ranges) > 2 ** 31 - 1
+        rows = torch.empty((n, 5 if wide else 4), dtype=torch.int32, device=dev)
+        rows[:, :3] = pts.view(torch.int32)
+        if wide:
+            rows[:, 3:5] = gids.to(torch.int64).view(torch.int32).reshape(n, 2)
+        else:
+            rows[:, 3] = gids.to(torch.int32)
+        recv, _ = _alltoallv(rows, dest, world, group)
+        rpts = recv[:, :3].contiguous().view(torch.float32)
+        rgids = (recv[:, 3:5].contiguous().view(torch.int64).reshape(-1) if wide
+                 else recv[:, 3].to(gdt))
+        # sources arrive in rank order, each in its own ordinal order (the
+        # partition is stable): already sorted when the ranks' ordinal ranges
+        # increase with the rank; otherwise sort (the local kNN breaks
+        # distance ties by local ordinal, _kernels.py:293-296)
+        live = [(o, c) for o, c in ranges if c]
+        if any(live[i][0] + live[i][1] > live[i + 1][0] for i in range(len(live) - 1)):
+            gorder = torch.argsort(rgids)
+            rgids = rgids[gorder]
+            rpts = rpts[gorder].contiguous()
     else:
-        lo = torch.full((3,), math.inf, device=dev)
-        hi = torch.full((3,), -math.inf, device=dev)
-    lo = _all_reduce(lo, dist.ReduceOp.MIN, group)
-    hi = _all_reduce(hi, dist.ReduceOp.MAX, group)
-    scene_lo = lo.cpu().numpy().astype(np.float64)
-    scene_hi = hi.cpu().numpy().astype(np.float64)
-    # 2. keys on the global grid
-    codes = engine.morton(pts, scene_lo, scene_hi)
-    gids = torch.arange(n, dtype=torch.int64, device=dev) + int(global_offset)
-    keys = (codes << 32) | gids
-    # 3. splitters from a gathered sample of sorted keys
-    skeys = torch.sort(keys).values
-    s = samples_per_rank
-    if n:
-        pick = torch.linspace(0, n - 1, s, device=dev).round().to(torch.int64)
-        sample = skeys[pick]
-    else:
-        sample = torch.full((s,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
-    gathered = _all_gather(sample, world, group)
-    allsamp = torch.sort(torch.cat(gathered)).values
-    cut = [allsamp[(i * allsamp.numel()) // world] for i in range(1, world)]
-    splitters = torch.stack(cut) if cut else torch.empty(0, dtype=torch.int64, device=dev)
-    dest = torch.searchsorted(splitters, keys, right=True)
-    # exchange primitives with their global ordinals (f64 rows: exact for both)
-    payload = torch.cat([pts.to(torch.float64), gids.to(torch.float64)[:, None]], dim=1)
-    recv, _ = _alltoallv(payload, dest, world, group)
-    rpts = recv[:, :3].to(torch.float32).contiguous()
-    rgids = recv[:, 3].to(torch.int64)
-    # local ordinal order must be global ordinal order: the local kNN breaks
-    # distance ties by local ordinal (_kernels.py:293-296)
-    gorder = torch.argsort(rgids)
-    rgids = rgids[gorder]
-    rpts = rpts[gorder].contiguous()
+        splitters = torch.empty(0, dtype=torch.int64, device=dev)
+        rpts, rgids = pts, gids
     # 4. local build
     m = int(rpts.shape[0])
-    tree = engine.build(rpts) if m else None
-    box = engine.box(tree).to(dev) if m else torch.tensor(
-        [math.inf] * 3 + [-math.inf] * 3, dtype=torch.float32, device=dev)
-    # 5. top tree
-    boxes = _all_gather(box.to(torch.float32), world, group)
-    cnts = _all_gather(torch.tensor([m], dtype=torch.int64, device=dev), world, group)
-    monotone = bool((rgids[1:] > rgids[:-1]).all().item()) if m > 1 else True
-    counts = [int(c.item()) for c in cnts]
-    global_leaves = False
-    if hasattr(engine, "globalize") and sum(counts) < 2 ** 31:
-        if tree is not None:
-            engine.globalize(tree, rgids)
-        global_leaves = True
-    return DistributedBvh(engine, tree, rgids, torch.stack(boxes), counts, splitters >> 32,
-                          scene_lo, scene_hi, world, rank, group, monotone, global_leaves)
+    if m:
+        tree = engine.build(rpts, rgids) if global_ids else engine.build(rpts)
+        box = engine.box(tree).to(dev)
+    else:
+        tree = None
+        box = torch.tensor([math.inf] * 3 + [-math.inf] * 3, dtype=torch.float32, device=dev)
+    # 5. top tree: rank boxes and primitive counts in one gather
+    top = _all_gather(torch.cat([box.to(torch.float32),
+                                 torch.tensor([m], dtype=torch.int32,
+                                              device=dev).view(torch.float32)]), world, group)
+    top = torch.stack(top)
+    boxes = top[:, :6].contiguous()
+    counts = [m] if world == 1 else top[:, 6].contiguous().view(torch.int32).tolist()
+    if scene_lo is None:  # one rank: the scene box is the local tree's
+        scene_h = boxes[0].cpu().numpy().astype(np.float64)
+        scene_lo, scene_hi = scene_h[:3], scene_h[3:]
+    return DistributedBvh(engine, tree, rgids, boxes, counts, splitters >> 32, scene_lo,
+                          scene_hi, world, rank, group, True, global_ids)
 
 
 def _local_knn(t: DistributedBvh, centers: torch.Tensor, k: int):

@@ -213,9 +213,11 @@ def _device_boxes(boxes):
 
 
 def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
-                 morton_bits: int = 30) -> Bvh:
+                 morton_bits: int = 30, leaf_ids: torch.Tensor | None = None) -> Bvh:
     """Build from device-resident (n, 3) f32 ``mins``/``maxs`` (``maxs`` may
-    be ``mins`` for point input).  The device-resident entry of :func:`build`."""
+    be ``mins`` for point input).  The device-resident entry of :func:`build`.
+    ``leaf_ids`` (optional, n i32 on the device): the ordinals the leaves
+    report instead of their input index (a shard's global ordinals)."""
     n = int(mins.shape[0])
     if n == 0:
         raise ValueError("empty scene")
@@ -248,7 +250,9 @@ def build_device(mins: torch.Tensor, maxs: torch.Tensor, check: bool = True,
                             dv.ptr(d["node_mins"]), dv.ptr(d["node_maxs"]), dv.ptr(d["left"]),
                             dv.ptr(d["right"]), dv.ptr(d["leaf_obj"]), dv.ptr(d["root_box"]),
                             dv.ptr(d["nodes"]), dv.ptr(d["leaf_codes"]), dv.ptr(d["leaf_dir"]),
-                            bits, _lib.BUILD_DEFER_ROWS, status.ptr, dv.stream())))
+                            bits, _lib.BUILD_DEFER_ROWS,
+                            dv.ptr(leaf_ids) if leaf_ids is not None else None, status.ptr,
+                            dv.stream())))
     d["rows_pending"] = True
     d["flags"] = ((_lib.TREE_POINT_LEAVES if maxs is mins else 0)
                   | (_lib.TREE_CODES30 if morton_bits == 30 else 0) | _lib.TREE_BUILT)

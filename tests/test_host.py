@@ -50,9 +50,9 @@ def test_leaf_directory_bits():
 def test_library_rejects_bad_arguments_without_touching_the_device():
     lib = _lib.load_library()
     # empty scene and null pointers are rejected before any launch
-    assert lib.lbvh_build(None, None, 0, 30, None, 0, *([None] * 9), 0, 0, None, None) == 4
-    assert lib.lbvh_build(None, None, 5, 30, None, 0, *([None] * 9), 0, 0, None, None) == 1
-    assert lib.lbvh_build(None, None, 5, 31, None, 0, *([None] * 9), 0, 0, None, None) == 1
+    assert lib.lbvh_build(None, None, 0, 30, None, 0, *([None] * 9), 0, 0, None, None, None) == 4
+    assert lib.lbvh_build(None, None, 5, 30, None, 0, *([None] * 9), 0, 0, None, None, None) == 1
+    assert lib.lbvh_build(None, None, 5, 31, None, 0, *([None] * 9), 0, 0, None, None, None) == 1
     assert lib.lbvh_sort_pairs(None, None, 10, 30, None, 0, None) == 1
     assert lib.lbvh_compact(None, 0, None, None, 1, None, None) == 1
 
