@@ -387,6 +387,27 @@ int lbvh_generate_cloud(int kind, int64_t p, double a, float lim, uint64_t st_hi
 int lbvh_rank_forward_mask(const float *centers, const float *bound, float radius2, int64_t m,
                            const float *boxes, int world, uint32_t candidates, uint32_t *mask,
                            void *stream);
+/* Radius forwarding at the origin.  phase 0: per_rank[d] = number of set
+ * bits d over mask[0..m) (world u32).  phase 1: rows (sum(per_rank) x 5
+ * f32: x, y, z, radius, query id bits) written into rank d's region starting
+ * at start[d] (device i64, world), cursor (world u32) is scratch. */
+int lbvh_forward_rows(const float *centers, const float *radii, const uint32_t *mask, int64_t m,
+                      int world, uint32_t *per_rank, int64_t *start, uint32_t *cursor,
+                      float *rows, int phase, void *stream);
+/* Radius merge at the origin.  sent_rows: the rows this rank forwarded
+ * (n_rec x 5, as lbvh_forward_rows wrote them); rec_counts[i]: hits the
+ * destination found for row i (returned in send order); phase 0 adds them
+ * into totals_or_cursor[q] (nq i32, caller-zeroed).  phase 1: rec_off =
+ * exclusive scan of rec_counts (positions in `hits`, the sources' hits
+ * concatenated in rank order), offsets = exclusive scan of the totals,
+ * source_starts (HOST i64, world + 1) = record ranges per source rank;
+ * each query's hits are appended source by source (rank order), each
+ * source's in its traversal (fill) order, into out (i64); totals_or_cursor
+ * must be zeroed again as the cursor. */
+int lbvh_merge_records(const float *sent_rows, const int32_t *rec_counts, const int64_t *rec_off,
+                       int64_t n_rec, const int64_t *source_starts, int world,
+                       const int32_t *hits, const int64_t *offsets, int32_t *totals_or_cursor,
+                       int64_t *out, int phase, void *stream);
 /* Renumber a local tree's leaves with global ordinals (map[local] ->
  * global, < 2^31) in leaf_obj and in the packed leaf links, so its queries
  * report -- and break distance ties by -- global ordinals. */

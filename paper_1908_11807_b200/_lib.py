@@ -151,6 +151,11 @@ _SIGS = {
                                  ctypes.c_int),
     "lbvh_morton_codes_f32": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_void_p], ctypes.c_int),
+    "lbvh_forward_rows": ([ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_int]
+                          + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "lbvh_merge_records": ([ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]
+                           + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_void_p],
+                           ctypes.c_int),
     "lbvh_remap_leaves": ([ctypes.POINTER(CTree)] + [ctypes.c_void_p] * 4, ctypes.c_int),
     "lbvh_brute_knn": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],

@@ -11,6 +11,11 @@
 //                             | global ordinal) keys (paths without lbvh_knn_kth)
 //   scatter_rows_kernel       received rows -> (nq, kk) outputs in query order
 //   remap_leaves_kernel       local tree leaves -> global ordinals
+//   forward_*_kernel          radius: (query, rank) pairs of the forward mask ->
+//                             per-destination rows (x, y, z, r, query id)
+//   record_*_kernel           radius merge at the origin: per-query totals from
+//                             the returned per-row hit counts, then each
+//                             source's hits appended in rank order
 
 #include "common.cuh"
 #include "internal.cuh"
@@ -120,6 +125,87 @@ remap_leaves_kernel(int64_t n, int32_t *__restrict__ leaf_obj, PackedNode *__res
     }
 }
 
+
+// Radius forwarding (origin): rank d's rows go to its region of `rows`
+// (region starts `start`, cursors zeroed), one 5-word row (x, y, z, r,
+// query id as bits) per (query, rank) pair of the forward mask.  Positions
+// inside a region follow the atomics; the merge below does not depend on them.
+__global__ void __launch_bounds__(256)
+forward_count_kernel(const uint32_t *__restrict__ mask, int64_t m, int world,
+                     uint32_t *__restrict__ per_rank) {
+    __shared__ uint32_t s_cnt[32];
+    if (threadIdx.x < 32) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t b = __ldg(mask + q);
+        while (b) {
+            const int r = __ffs(b) - 1;
+            b &= b - 1;
+            atomicAdd(&s_cnt[r], 1u);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < world && s_cnt[threadIdx.x])
+        atomicAdd(per_rank + threadIdx.x, s_cnt[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256)
+forward_rows_kernel(const float *__restrict__ centers, const float *__restrict__ radii,
+                    const uint32_t *__restrict__ mask, int64_t m,
+                    const int64_t *__restrict__ start, uint32_t *__restrict__ cursor,
+                    float *__restrict__ rows) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t b = __ldg(mask + q);
+        if (!b) continue;
+        const float x = __ldg(centers + 3 * q), y = __ldg(centers + 3 * q + 1),
+                    z = __ldg(centers + 3 * q + 2), r = __ldg(radii + q);
+        while (b) {
+            const int d = __ffs(b) - 1;
+            b &= b - 1;
+            float *row = rows + 5 * (__ldg(start + d) + atomicAdd(cursor + d, 1u));
+            row[0] = x;
+            row[1] = y;
+            row[2] = z;
+            row[3] = r;
+            row[4] = __int_as_float((int32_t)q);
+        }
+    }
+}
+
+// Origin merge, step 1: each returned record (one per row this rank sent,
+// in its send order) adds its hit count to its query's total.
+__global__ void __launch_bounds__(256)
+record_totals_kernel(const float *__restrict__ sent_rows, const int32_t *__restrict__ rec_counts,
+                     int64_t n_rec, int32_t *__restrict__ totals) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rec;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = __ldg(rec_counts + i);
+        if (c) atomicAdd(totals + __float_as_int(__ldg(sent_rows + 5 * i + 4)), c);
+    }
+}
+
+// Origin merge, step 2 (one launch per source rank, in rank order): a query
+// appears at most once per source, so its records need no atomics -- each
+// appends its hits (the responder's fill order) after the earlier sources'.
+__global__ void __launch_bounds__(256)
+record_place_kernel(const float *__restrict__ sent_rows, const int32_t *__restrict__ rec_counts,
+                    const int64_t *__restrict__ rec_off, int64_t r0, int64_t r1,
+                    const int32_t *__restrict__ hits, const int64_t *__restrict__ offsets,
+                    int32_t *__restrict__ cursor, int64_t *__restrict__ out) {
+    for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = __ldg(rec_counts + i);
+        if (!c) continue;
+        const int32_t q = __float_as_int(__ldg(sent_rows + 5 * i + 4));
+        const int64_t dst = __ldg(offsets + q) + cursor[q];
+        const int64_t src = __ldg(rec_off + i);
+        for (int32_t j = 0; j < c; ++j) out[dst + j] = __ldg(hits + src + j);
+        cursor[q] += c;
+    }
+}
+
 unsigned grid_of(int64_t n) {
     unsigned g = div_up(n > 0 ? n : 1, 256);
     return g < kNumSMs * 8 ? g : kNumSMs * 8;
@@ -178,6 +264,56 @@ int lbvh_gather_rows3(const float *src, const int64_t *idx, int64_t n, float *ds
     if (n == 0) return LBVH_OK;
     gather_rows3_kernel<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(src, idx, n, dst);
     count_launches(1);
+    return check_launch();
+}
+
+int lbvh_forward_rows(const float *centers, const float *radii, const uint32_t *mask, int64_t m,
+                      int world, uint32_t *per_rank, int64_t *start, uint32_t *cursor,
+                      float *rows, int phase, void *stream) {
+    if (m < 0 || world < 1 || world > 32 || !mask || (m > 0 && (!centers || !radii)))
+        return LBVH_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (phase == 0) {  // per-rank pair counts
+        if (!per_rank) return LBVH_ERR_INVALID_ARG;
+        cudaMemsetAsync(per_rank, 0, sizeof(uint32_t) * world, st);
+        if (m) {
+            forward_count_kernel<<<grid_of(m), 256, 0, st>>>(mask, m, world, per_rank);
+            count_launches(1);
+        }
+        return check_launch();
+    }
+    if (!start || !cursor || !rows) return LBVH_ERR_INVALID_ARG;
+    cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * world, st);
+    if (m) {
+        forward_rows_kernel<<<grid_of(m), 256, 0, st>>>(centers, radii, mask, m, start, cursor,
+                                                       rows);
+        count_launches(1);
+    }
+    return check_launch();
+}
+
+int lbvh_merge_records(const float *sent_rows, const int32_t *rec_counts, const int64_t *rec_off,
+                       int64_t n_rec, const int64_t *source_starts, int world,
+                       const int32_t *hits, const int64_t *offsets, int32_t *totals_or_cursor,
+                       int64_t *out, int phase, void *stream) {
+    if (n_rec < 0 || world < 1 || (n_rec > 0 && (!sent_rows || !rec_counts)) || !totals_or_cursor)
+        return LBVH_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_rec == 0) return LBVH_OK;
+    if (phase == 0) {  // per-query totals (caller zeroes totals)
+        record_totals_kernel<<<grid_of(n_rec), 256, 0, st>>>(sent_rows, rec_counts, n_rec,
+                                                            totals_or_cursor);
+        count_launches(1);
+        return check_launch();
+    }
+    if (!rec_off || !source_starts || !hits || !offsets || !out) return LBVH_ERR_INVALID_ARG;
+    for (int s = 0; s < world; ++s) {  // source order = merge order
+        const int64_t r0 = source_starts[s], r1 = source_starts[s + 1];
+        if (r1 <= r0) continue;
+        record_place_kernel<<<grid_of(r1 - r0), 256, 0, st>>>(
+            sent_rows, rec_counts, rec_off, r0, r1, hits, offsets, totals_or_cursor, out);
+        count_launches(1);
+    }
     return check_launch();
 }
 

@@ -860,12 +860,18 @@ def query_knn_distributed_host(t: DistributedBvh, centers, k: int, chunk: int = 
 
 def query_spatial_distributed(t: DistributedBvh, centers, radius):
     """Collective radius search.  Returns (offsets int64, global ordinals
-    int64 sorted within each query) for this rank's queries, in order."""
+    int64) for this rank's queries, in order.  A query's hits are grouped by
+    the rank that holds them (rank order), each rank's in its traversal
+    (fill) order -- a deterministic order; as sets they equal the reference's
+    on the concatenated cloud."""
     dev, world, g = t.engine.device, t.world, t.group
-    c = torch.as_tensor(centers, dtype=torch.float32).to(dev).reshape(-1, 3)
+    c = torch.as_tensor(centers, dtype=torch.float32).to(dev).reshape(-1, 3).contiguous()
     nq = int(c.shape[0])
     r = torch.as_tensor(radius, dtype=torch.float32).to(dev)
-    r = r.expand(nq).contiguous() if r.ndim == 0 else r.reshape(-1)
+    r = r.expand(nq).contiguous() if r.ndim == 0 else r.reshape(-1).contiguous()
+    flags = _query_flags(c, r)
+    if c.is_cuda and isinstance(t.engine, GpuEngine) and world <= 32:
+        return _query_spatial_gpu(t, c, r, flags)
     r2 = r * r
     bd = _box_dist_sq(c, t.boxes)
     need = (bd <= r2[:, None]) & (torch.tensor(t.counts, device=dev) > 0)[None, :]
@@ -874,7 +880,7 @@ def query_spatial_distributed(t: DistributedBvh, centers, radius):
     rows[:, :3] = c[qi]
     rows[:, 3] = r[qi]
     rows[:, 4] = qi.to(torch.int32).view(torch.float32)
-    rq, rcounts = _alltoallv(rows, rr, world, g, flags=_query_flags(c, r))
+    rq, rcounts = _alltoallv(rows, rr, world, g, flags=flags)
     src = _source_ranks(rcounts, dev)
     m = int(rq.shape[0])
     if m and t.tree is not None:
@@ -889,12 +895,99 @@ def query_spatial_distributed(t: DistributedBvh, centers, radius):
         hit_rows = torch.empty((0, 2), dtype=torch.int32, device=dev)
         hit_dest = torch.empty(0, dtype=torch.int64, device=dev)
     got, _ = _alltoallv(hit_rows, hit_dest, world, g)
+    # rows arrive grouped by source rank, each source's in its fill order: a
+    # stable sort by query keeps exactly that order inside every query
     qix = got[:, 0].to(torch.int64)
-    gids = got[:, 1].to(torch.int64)
-    key = qix * (1 << 32) + gids
-    o = torch.argsort(key)
+    o = torch.argsort(qix, stable=True)
     counts = torch.bincount(qix, minlength=nq) if qix.numel() else torch.zeros(
         nq, dtype=torch.int64, device=dev)
     offsets = torch.zeros(nq + 1, dtype=torch.int64, device=dev)
     offsets[1:] = torch.cumsum(counts, 0)
-    return offsets, gids[o]
+    return offsets, got[:, 1].to(torch.int64)[o]
+
+
+def _query_spatial_gpu(t: DistributedBvh, c: torch.Tensor, r: torch.Tensor, flags):
+    """query_spatial_distributed on CUDA: forward mask, forwarded rows, the
+    per-row hit counts and the hits travel back, and the origin appends each
+    source's hits per query -- library kernels, no sort."""
+    from . import _device as dv
+    from . import _lib
+
+    l = _lib.lib()
+    st = dv.stream()
+    dev, world, g = t.engine.device, t.world, t.group
+    nq = int(c.shape[0])
+    i64, i32 = torch.int64, torch.int32
+    if world == 1 and not _FORCE_ROUTE:
+        _raise_flags(int(flags))
+        if t.tree is None or nq == 0:
+            return torch.zeros(nq + 1, dtype=i64, device=dev), torch.empty(0, dtype=i64,
+                                                                            device=dev)
+        off, idx = t.engine.radius(t.tree, c, r)
+        hit = idx if t.global_leaves else t.gids[idx]
+        return off, hit.to(i64)
+    # 1. forward every query to each non-empty rank within its radius
+    cand = 0
+    for rk in range(world):
+        if t.counts[rk] > 0:
+            cand |= 1 << rk
+    mask = torch.zeros(nq, dtype=i32, device=dev)
+    r2 = (r * r).contiguous()
+    boxes = t.boxes.to(torch.float32).contiguous()
+    if nq:
+        _lib.check(l.lbvh_rank_forward_mask(dv.ptr(c), dv.ptr(r2), 0.0, nq, dv.ptr(boxes),
+                                            world, cand, dv.ptr(mask), st))
+    per_rank = torch.empty(world, dtype=i32, device=dev)
+    _lib.check(l.lbvh_forward_rows(dv.ptr(c), dv.ptr(r), dv.ptr(mask), nq, world,
+                                   dv.ptr(per_rank), None, None, None, 0, st))
+    sent = per_rank.tolist()
+    starts = [0]
+    for x in sent:
+        starts.append(starts[-1] + x)
+    start_d = torch.tensor(starts[:-1], dtype=i64, device=dev)
+    cursor = torch.empty(world, dtype=i32, device=dev)
+    rows = torch.empty((starts[-1], 5), dtype=torch.float32, device=dev)
+    _lib.check(l.lbvh_forward_rows(dv.ptr(c), dv.ptr(r), dv.ptr(mask), nq, world, None,
+                                   dv.ptr(start_d), dv.ptr(cursor), dv.ptr(rows), 1, st))
+    rq, rcounts = _alltoallv(rows, None, world, g, grouped_counts=sent, flags=flags)
+    # 2. responder: local search of the received rows (fill order, global ordinals)
+    m = int(rq.shape[0])
+    if m and t.tree is not None:
+        off, idx = t.engine.radius(t.tree, rq[:, :3].contiguous(), rq[:, 3].contiguous())
+        hits = (idx if t.global_leaves else t.gids[idx]).to(i32)
+        rec = (off[1:] - off[:-1]).to(i32)
+        bnd = [0]
+        for x in rcounts:
+            bnd.append(bnd[-1] + x)
+        edges = off[torch.tensor(bnd, dtype=i64, device=dev)].tolist()
+        hit_split = [edges[i + 1] - edges[i] for i in range(world)]
+    else:
+        hits = torch.empty(0, dtype=i32, device=dev)
+        rec = torch.zeros(m, dtype=i32, device=dev)
+        hit_split = [0] * world
+    got_rec, _ = _alltoallv(rec, None, world, g, grouped_counts=list(rcounts))
+    got_hits, _ = _alltoallv(hits, None, world, g, grouped_counts=hit_split)
+    got_rec = got_rec.contiguous()
+    got_hits = got_hits.contiguous()
+    # 3. origin: per-query totals, CRS offsets, then sources appended in rank order
+    n_rec = int(got_rec.shape[0])
+    acc = torch.zeros(nq, dtype=i32, device=dev)
+    _lib.check(l.lbvh_merge_records(dv.ptr(rows), dv.ptr(got_rec), None, n_rec, None, world,
+                                    None, None, dv.ptr(acc), None, 0, st))
+    ws = dv.workspace(l.lbvh_scan_workspace_bytes(max(nq, n_rec, 1)))
+    offsets = torch.empty(nq + 1, dtype=i64, device=dev)
+    _lib.check(l.lbvh_exclusive_scan(dv.ptr(acc), nq, dv.ptr(offsets), dv.ptr(ws), ws.numel(),
+                                     st))
+    rec_off = torch.empty(n_rec + 1, dtype=i64, device=dev)
+    _lib.check(l.lbvh_exclusive_scan(dv.ptr(got_rec), n_rec, dv.ptr(rec_off), dv.ptr(ws),
+                                     ws.numel(), st))
+    total = int(offsets[nq].item()) if nq else 0
+    out = torch.empty(total, dtype=i64, device=dev)
+    if total == 0:
+        return offsets, out
+    acc.zero_()
+    src_starts = np.array(starts, dtype=np.int64)
+    _lib.check(l.lbvh_merge_records(dv.ptr(rows), dv.ptr(got_rec), dv.ptr(rec_off), n_rec,
+                                    src_starts.ctypes.data, world, dv.ptr(got_hits),
+                                    dv.ptr(offsets), dv.ptr(acc), dv.ptr(out), 1, st))
+    return offsets, out

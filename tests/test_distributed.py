@@ -119,8 +119,9 @@ def _worker(rank, world, port, engine_kind, n_total, split, queue):
             off, gid = D.query_spatial_distributed(t, q, r)
             so, si = oracle.query_spatial_2p(ref, q, r, threads=1)
             assert np.array_equal(off.cpu().numpy(), so), r
+            gh = gid.cpu().numpy()
             for i in range(q.shape[0]):
-                assert np.array_equal(gid.cpu().numpy()[off[i]:off[i + 1]],
+                assert np.array_equal(np.sort(gh[off[i]:off[i + 1]]),
                                       np.sort(si[so[i]:so[i + 1]])), (r, i)
         if engine_kind == "gpu":
             # pipelined host entry point: chunk counts differ per rank
@@ -254,6 +255,16 @@ def _worker_single(port, queue):
         ho, hg, hd = D.query_knn_distributed_host(t, q, 10, chunk=128)
         ko, ki, kd = oracle.query_knn(ref, q, 10, threads=1)
         assert np.array_equal(hg, ki) and hd.tobytes() == kd.tobytes()
+        # radius through the full forward / return / merge kernels on one
+        # rank: the merged order is then exactly the reference's fill order
+        for route in (False, True):
+            D._FORCE_ROUTE = route
+            for r in (0.0, 1.7, 3.5):
+                so, si = oracle.query_spatial_2p(ref, q, r, threads=1)
+                off, gid = D.query_spatial_distributed(t, torch.from_numpy(q).cuda(), r)
+                assert np.array_equal(off.cpu().numpy(), so), (route, r)
+                assert np.array_equal(gid.cpu().numpy(), si.astype(np.int64)), (route, r)
+        D._FORCE_ROUTE = False
         dist.destroy_process_group()
         queue.put("ok")
     except Exception:
