@@ -84,14 +84,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
-def build_variant(name: str, defines: list) -> str:
-    """A/B build with extra -D defines into _lib/variants/<name>.so (load it
-    with LBVH_LIB=<path>); used only for kernel experiments."""
+def build_variant(name: str, defines: list, csrc: str = None) -> str:
+    """A/B build with extra -D defines (and optionally another source tree,
+    e.g. a git checkout of csrc/) into _lib/variants/<name>.so (load it with
+    LBVH_LIB=<path>); used only for kernel experiments."""
     vdir = os.path.join(OUT_DIR, "variants", name)
     os.makedirs(vdir, exist_ok=True)
     cc = nvcc()
     objs = []
-    for src in _sources():
+    for src in (sorted(glob.glob(os.path.join(csrc, "*.cu"))) if csrc else _sources()):
         obj = os.path.join(vdir, os.path.basename(src).replace(".cu", ".o"))
         subprocess.run([cc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o",
                         obj], check=True)
@@ -105,6 +106,11 @@ def build_variant(name: str, defines: list) -> str:
 if __name__ == "__main__":
     if "--variant" in sys.argv:
         i = sys.argv.index("--variant")
-        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+        csrc = None
+        if "--csrc" in sys.argv:
+            j = sys.argv.index("--csrc")
+            csrc = sys.argv[j + 1]
+            del sys.argv[j:j + 2]
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:], csrc))
     else:
         print(build(force="--force" in sys.argv, verbose=True))

@@ -31,5 +31,6 @@ S = sum(x[2] for x in lines) or 1
 I = sum(x[3] for x in lines) or 1
 T = sum(x[4] for x in lines) or 1
 print(f"samples {S}  warp-inst {I}  thread-inst/warp-inst {T / I:.2f}")
-for ln, src, s, i, t in sorted(lines, key=lambda x: -x[2])[:top]:
+key = 3 if "--by-inst" in sys.argv else 2
+for ln, src, s, i, t in sorted(lines, key=lambda x: -x[key])[:top]:
     print(f"{ln:5d} {100 * s / S:5.1f}% stall {100 * i / I:5.1f}% inst {t / max(i, 1):5.1f} thr  {src.strip()[:80]}")
