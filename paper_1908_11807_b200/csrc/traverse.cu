@@ -323,9 +323,15 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     uint32_t fail = 0;
     int sp = 0;
     int32_t node = 0;  // the root; never pruned (the list is empty)
+#ifdef LBVH_KNN_COUNT_VISITS  // instrumentation builds (tools/knn_visits.py)
+    int visits = 0;
+#endif
     while (true) {
         float4 a, b, c;
         int4 dd;
+#ifdef LBVH_KNN_COUNT_VISITS
+        ++visits;
+#endif
         load_node(nodes, node, a, b, c, dd);
         const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
         const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
@@ -368,6 +374,10 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         node = next;
     }
     if (fail) atomicOr(status, fail);
+#ifdef LBVH_KNN_COUNT_VISITS  // node visits in place of the nearest distance
+    top.key[0] = ((uint64_t)__float_as_uint((float)visits * (float)visits) << 32) |
+                 (top.key[0] & 0xFFFFFFFFull);
+#endif
     // the k-th squared distance (exact; the sharded search's forwarding bound)
     if (kth) kth[q] = top.dist(K - 1);
     // Spans are written even after a failure; the driver raises anyway.
