@@ -284,7 +284,10 @@ topology_kernel(const uint32_t *__restrict__ codes, int64_t n, uint32_t *slots,
 // indistinguishable from a global one, so the meeting rule is unchanged.
 // It also writes the leaf-directory runs the local kernel deferred.
 // ---------------------------------------------------------------------------
-constexpr int kHierT = 256;
+#ifndef LBVH_HIER_T
+#define LBVH_HIER_T 256
+#endif
+constexpr int kHierT = LBVH_HIER_T;
 // Leaf-directory runs longer than this (empty buckets between two adjacent
 // leaves: clustered clouds) are deferred to the frontier kernel, where the
 // whole grid writes them.
@@ -460,15 +463,58 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     }
 }
 
+// Memory-scope helpers of the frontier handshake: GPU scope when climbers
+// run in many CTAs, CTA scope for the single-CTA top stage (no L2 round
+// trips for fences, records read through L1).
+template <bool CTA>
+__device__ __forceinline__ uint32_t exch_release(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    if (CTA)
+        asm volatile("atom.release.cta.global.exch.b32 %0, [%1], %2;"
+                     : "=r"(old) : "l"(p), "r"(v) : "memory");
+    else
+        asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;"
+                     : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+template <bool CTA>
+__device__ __forceinline__ void fence_acq_rel() {
+    if (CTA)
+        asm volatile("fence.acq_rel.cta;" ::: "memory");
+    else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+template <bool CTA>
+__device__ __forceinline__ float ld_rlx(const float *p) {
+    float v;
+    if (CTA)
+        asm volatile("ld.relaxed.cta.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+template <bool CTA>
+__device__ __forceinline__ float4 ld_rlx(const float4 *p) {
+    float4 v;
+    if (CTA)
+        asm volatile("ld.relaxed.cta.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+    return v;
+}
+
 // Box of a node the local kernel (or an earlier frontier step) finished:
 // a leaf's row, or the union of an internal node's packed child boxes
-// (same left-first fold as the refit).  Strong loads: written by other CTAs.
+// (same left-first fold as the refit).  Strong loads: written by other threads.
+template <bool CTA>
 __device__ __forceinline__ void frontier_box(const PackedNode *nodes, const float *node_mins,
                                              const float *node_maxs, bool leaf_maxs_rows,
                                              int64_t internal, int64_t id, Box &b) {
     if (id < internal) {
         const PackedNode *pn = nodes + id;
-        const float4 a = ld_relaxed(&pn->a), c = ld_relaxed(&pn->b), e = ld_relaxed(&pn->c);
+        const float4 a = ld_rlx<CTA>(&pn->a), c = ld_rlx<CTA>(&pn->b), e = ld_rlx<CTA>(&pn->c);
         b.lo[0] = min_left(a.x, c.z); b.lo[1] = min_left(a.y, c.w);
         b.lo[2] = min_left(a.z, e.x);
         b.hi[0] = max_left(a.w, e.y); b.hi[1] = max_left(c.x, e.z);
@@ -477,14 +523,25 @@ __device__ __forceinline__ void frontier_box(const PackedNode *nodes, const floa
         const float *hi = leaf_maxs_rows ? node_maxs : node_mins;  // point leaves: hi == lo
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            b.lo[a] = ld_relaxed(node_mins + 3 * id + a);
-            b.hi[a] = ld_relaxed(hi + 3 * id + a);
+            b.lo[a] = ld_rlx<CTA>(node_mins + 3 * id + a);
+            b.hi[a] = ld_rlx<CTA>(hi + 3 * id + a);
         }
     }
 }
 
-template <typename CodeT>
-__global__ void __launch_bounds__(256)
+// The frontier climb.  Stage 1 (CTA = false, many CTAs, GPU-scope
+// handshakes) climbs until a node spans >= stop_len leaves and defers it to
+// stage 2; stage 2 (CTA = true, one CTA, CTA-scope handshakes) finishes the
+// top levels -- few nodes, but a chain of dependent handshakes whose GPU-scope
+// fences would cost L2 round trips each.  Small trees go to stage 2 directly.
+constexpr int kTopThreads = 1024;
+#ifndef LBVH_TOP_SPAN_BITS
+#define LBVH_TOP_SPAN_BITS 16
+#endif
+constexpr int64_t kTopSpan = (int64_t)1 << LBVH_TOP_SPAN_BITS;  // stage 1 defers nodes spanning >= this
+
+template <typename CodeT, bool CTA>
+__global__ void __launch_bounds__(CTA ? kTopThreads : 256)
 hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const int32_t *__restrict__ leaf_obj,
                           int64_t n, uint32_t *slots, const float *node_mins,
                           const float *node_maxs, bool leaf_maxs_rows,
@@ -492,7 +549,8 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const int32_t *__rest
                           PackedNode *nodes, float *__restrict__ root_box,
                           const uint2 *__restrict__ frontier, const uint32_t *frontier_count,
                           uint32_t *__restrict__ leaf_dir, const DirRun *__restrict__ runs,
-                          const uint32_t *run_count) {
+                          const uint32_t *run_count, int64_t stop_len, uint2 *deferred,
+                          uint32_t *deferred_count) {
     const int64_t internal = n - 1;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -510,24 +568,28 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const int32_t *__rest
         Box mine;
         int32_t my_link;
         if (l == r) {  // a leaf (row written by the local kernel)
-            frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, internal + l,
-                         mine);
+            frontier_box<CTA>(nodes, node_mins, node_maxs, leaf_maxs_rows, internal,
+                              internal + l, mine);
             my_link = (int32_t)((uint32_t)__ldg(leaf_obj + l) | kLeafTag);
-        } else {       // an internal node built by the local kernel
+        } else {       // an internal node built by the local kernel or stage 1
             const int64_t id = is_left_child(codes, n, l, r) ? r : l;
-            frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, id, mine);
+            frontier_box<CTA>(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, id, mine);
             my_link = (int32_t)id;
         }
         bool left_side = is_left_child(codes, n, l, r);
         while (true) {
+            if (!CTA && r - l + 1 >= stop_len) {  // the top levels: stage 2
+                deferred[atomicAdd(deferred_count, 1u)] = make_uint2((uint32_t)l, (uint32_t)r);
+                break;
+            }
             const int64_t g = left_side ? r : l - 1;
             const uint32_t known = (uint32_t)(left_side ? l : r);
             // release: this subtree's record is visible to whoever arrives second
-            const uint32_t other = atomic_exch_release(slots + g, known + 1u);
+            const uint32_t other = exch_release<CTA>(slots + g, known + 1u);
             if (other == 0) break;  // first arrival: sibling subtree not done
             // second arrival: the exchange read the partner's release; the
             // fence completes the acquire pattern before its record is read
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            fence_acq_rel<CTA>();
             const int64_t pl = left_side ? l : (int64_t)(other - 1u);
             const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
             const int64_t lc = (pl == g) ? internal + g : g;
@@ -539,7 +601,7 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const int32_t *__rest
             right[pid] = (int32_t)rc;
             const int64_t sib = left_side ? rc : lc;
             Box sb;
-            frontier_box(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, sib, sb);
+            frontier_box<CTA>(nodes, node_mins, node_maxs, leaf_maxs_rows, internal, sib, sb);
             const int32_t sib_link = sib < internal
                                          ? (int32_t)sib
                                          : (int32_t)((uint32_t)__ldg(leaf_obj + (sib - internal)) |
@@ -767,9 +829,25 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
         codes, perm, mins, maxs, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
         leaf_obj, (PackedNode *)nodes, root_box, sorted_codes, leaf_dir, dir_bits, runs,
         counter + 3, frontier, counter + 2, leaf_ids);
-    hierarchy_frontier_kernel<CodeT><<<grid_for(n / 64 + 1, 256, 8), 256, 0, stream>>>(
-        codes, leaf_obj, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
-        (PackedNode *)nodes, root_box, frontier, counter + 2, leaf_dir, runs, counter + 3);
+    // stage 1 only when the frontier is too large for one CTA; its deferred
+    // list lives after the frontier list (at most 2n / kTopSpan + 2 entries)
+    uint2 *deferred = frontier + n;
+    if (n > 4 * kTopSpan) {
+        hierarchy_frontier_kernel<CodeT, false><<<grid_for(n / 64 + 1, 256, 8), 256, 0, stream>>>(
+            codes, leaf_obj, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
+            (PackedNode *)nodes, root_box, frontier, counter + 2, leaf_dir, runs, counter + 3,
+            kTopSpan, deferred, counter + 1);
+        hierarchy_frontier_kernel<CodeT, true><<<1, kTopThreads, 0, stream>>>(
+            codes, leaf_obj, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
+            (PackedNode *)nodes, root_box, deferred, counter + 1, nullptr, runs, counter + 3,
+            0, nullptr, nullptr);
+        count_launches(1);
+    } else {
+        hierarchy_frontier_kernel<CodeT, true><<<1, kTopThreads, 0, stream>>>(
+            codes, leaf_obj, n, slots, node_mins, node_maxs, leaf_maxs_rows, left, right,
+            (PackedNode *)nodes, root_box, frontier, counter + 2, leaf_dir, runs, counter + 3,
+            0, nullptr, nullptr);
+    }
     count_launches(2);
     if (!defer && n > 1) {
         finish_rows_kernel<<<grid_for(n - 1, 256, 16), 256, 0, stream>>>(

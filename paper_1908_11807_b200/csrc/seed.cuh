@@ -5,6 +5,10 @@
 
 namespace lbvh {
 
+#ifndef LBVH_SEED_WINDOW
+#define LBVH_SEED_WINDOW 2  // leaves per k in the Morton window
+#endif
+
 // Search-radius seed for one query: the kk-th smallest distance^2 among the
 // 2*kk leaves that neighbour the query's Morton code in leaf order (a real
 // upper bound of the true k-th distance).  Leaves are found by a lower_bound
@@ -28,8 +32,8 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
         else
             hi = mid;
     }
-    const int64_t w = 2 * (int64_t)kk;
-    int64_t w0 = lo - kk;
+    const int64_t w = LBVH_SEED_WINDOW * (int64_t)kk;
+    int64_t w0 = lo - w / 2;
     w0 = w0 < 0 ? 0 : w0;
     w0 = (w0 + w > n) ? (n - w > 0 ? n - w : 0) : w0;
     const int64_t w1 = (w0 + w < n) ? w0 + w : n;

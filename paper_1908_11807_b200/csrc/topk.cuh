@@ -21,6 +21,9 @@ __device__ __forceinline__ bool lex_less(float d1, int32_t i1, float d2, int32_t
 template <int K>
 struct TopK {
     uint64_t key[K];
+#ifdef LBVH_KNN_COUNT_VISITS
+    int kept = 0;  // instrumentation: insertions that displaced the k-th
+#endif
 
     // `bound` (optional, may be NaN = none): a distance^2 known to have at
     // least kk candidates at or below it.  Empty slots then carry
@@ -47,6 +50,9 @@ struct TopK {
     __device__ __forceinline__ void offer(float cd, int32_t obj) { offer_key(make(cd, obj)); }
     __device__ __forceinline__ void offer_key(const uint64_t c) {
         if (!(c < key[K - 1])) return;
+#ifdef LBVH_KNN_COUNT_VISITS
+        ++kept;
+#endif
         bool lt[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) lt[j] = key[j] < c;

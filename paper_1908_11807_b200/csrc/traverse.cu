@@ -302,9 +302,14 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     }
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
     TopK<K> top;
+#ifdef LBVH_KNN_BOUND_FROM_KTH  // instrumentation: start from a given bound (e.g. the exact k-th)
+    const float bound = kth ? __ldg(kth + q) : __int_as_float(0x7FFFFFFF);
+    kth = nullptr;
+#else
     const float bound = (qcodes && t.leaf_codes)
                             ? seed_bound<K>(t, __ldg(qcodes + s), kk, px, py, pz)
                             : __int_as_float(0x7FFFFFFF);
+#endif
     top.init(kk, bound);
     // Reference node order: push farther, push nearer, pop (_kernels.py:363-403).
     // The nearer child stays in a register (`next`) instead of a push/pop
@@ -374,9 +379,11 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         node = next;
     }
     if (fail) atomicOr(status, fail);
-#ifdef LBVH_KNN_COUNT_VISITS  // node visits in place of the nearest distance
+#ifdef LBVH_KNN_COUNT_VISITS  // node visits / kept offers in place of the two nearest distances
     top.key[0] = ((uint64_t)__float_as_uint((float)visits * (float)visits) << 32) |
                  (top.key[0] & 0xFFFFFFFFull);
+    top.key[1] = ((uint64_t)__float_as_uint((float)top.kept * (float)top.kept) << 32) |
+                 (top.key[1] & 0xFFFFFFFFull);
 #endif
     // the k-th squared distance (exact; the sharded search's forwarding bound)
     if (kth) kth[q] = top.dist(K - 1);

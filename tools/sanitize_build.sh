@@ -6,7 +6,7 @@ import sys; sys.path.insert(0,'.')
 import torch, numpy as np
 import paper_1908_11807_b200 as lb
 from oracle import oracle
-for n in (300, 700, 5000, 100000):
+for n in (300, 700, 5000, 100000, 300000):
     pts = lb.generate(lb.CloudSpec("cube","filled",n,0))
     t = lb.build(torch.from_numpy(pts).cuda())
     ref = oracle.build(pts)
