@@ -127,11 +127,21 @@ __device__ __forceinline__ void encode(double x, double y, double z, const doubl
 
 // K2: codes of the f64 box centroids on the scene grid, plus iota values.
 // CodeT = uint32_t: the reference's 30-bit codes; uint64_t: 63-bit codes.
+#ifndef LBVH_MORTON_CTAS
+#define LBVH_MORTON_CTAS 4  // resident CTAs per SM of the fused Morton + histogram pass
+#endif
+// hist (30-bit codes, optional): the digit histograms of the 4-pass sort
+// that follows (sort_prepare), so it needs no histogram pass of its own.
 template <typename CodeT>
 __global__ void __launch_bounds__(256)
 morton_kernel(const float *__restrict__ mins, const float *__restrict__ maxs, int64_t n,
               const float *__restrict__ scene, CodeT *__restrict__ codes,
-              uint32_t *__restrict__ iota) {
+              uint32_t *__restrict__ iota, uint32_t *__restrict__ hist = nullptr) {
+    __shared__ uint32_t s_hist[4][kSortDigits];
+    if (hist) {
+        for (int i = threadIdx.x; i < 4 * kSortDigits; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+        __syncthreads();
+    }
     double lo[3], ext[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -152,6 +162,11 @@ morton_kernel(const float *__restrict__ mins, const float *__restrict__ maxs, in
         encode(c[0], c[1], c[2], lo, ext, code);
         codes[i] = code;
         if (iota) iota[i] = (uint32_t)i;
+        if (sizeof(CodeT) == 4 && hist) hist_accumulate(s_hist, (uint32_t)code, 0, 4);
+    }
+    if (hist) {
+        __syncthreads();
+        hist_flush(s_hist, 4, hist);
     }
 }
 
@@ -554,11 +569,12 @@ hierarchy_frontier_kernel(const CodeT *__restrict__ codes, const int32_t *__rest
     const int64_t internal = n - 1;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if (leaf_dir) {  // long leaf-directory runs, written by the whole grid
+    if (leaf_dir) {  // long leaf-directory runs (> kDirInline buckets): one warp per run
         const uint32_t nr = *run_count;
-        for (uint32_t k = 0; k < nr; ++k) {
+        const int64_t lane = threadIdx.x & 31;
+        for (int64_t k = tid >> 5; k < (int64_t)nr; k += stride >> 5) {
             const DirRun e = runs[k];
-            for (int64_t b = e.lo + tid; b < (int64_t)e.hi; b += stride) leaf_dir[b] = e.value;
+            for (int64_t b = e.lo + lane; b < (int64_t)e.hi; b += 32) leaf_dir[b] = e.value;
         }
     }
     const int64_t count = (int64_t)*frontier_count;
@@ -814,10 +830,22 @@ int build_impl(const float *mins, const float *maxs, int64_t n, void *ws, size_t
     unsigned rg = grid_for(n, kReduceThreads, 4);
     scene_reduce_kernel<<<rg, kReduceThreads, 0, stream>>>(mins, maxs, n, partials, counter,
                                                            root_box, status);
-    unsigned mg = grid_for(n, 256, 16);
-    morton_kernel<CodeT><<<mg, 256, 0, stream>>>(mins, maxs, n, root_box, codes, perm);
-    count_launches(2);
-    int rc = sort_codes(codes, perm, n, sort_ws, stream);
+    int rc;
+    if (sizeof(CodeT) == 4) {
+        // the sort's digit histograms come from the Morton pass, its input
+        // values are the positions: no histogram pass, no iota array
+        uint32_t *hist = sort_prepare(sort_ws, sort_workspace_bytes(n), n, stream);
+        morton_kernel<CodeT><<<grid_for(n, 256, LBVH_MORTON_CTAS), 256, 0, stream>>>(
+            mins, maxs, n, root_box, codes, nullptr, hist);
+        count_launches(2);
+        rc = sort_pairs_prepared(reinterpret_cast<uint32_t *>(codes), perm, n, 30, sort_ws,
+                                 sort_workspace_bytes(n), stream, 0, false);
+    } else {
+        morton_kernel<CodeT><<<grid_for(n, 256, 16), 256, 0, stream>>>(mins, maxs, n, root_box,
+                                                                       codes, perm);
+        count_launches(2);
+        rc = sort_codes(codes, perm, n, sort_ws, stream);
+    }
     if (rc != LBVH_OK) return rc;
     // point input with deferred rows: node_maxs leaf rows (== node_mins rows)
     // are written by lbvh_finish_rows, the frontier reads node_mins for both
@@ -974,9 +1002,13 @@ namespace {
 // leaves gives a valid seed -- nor, measurably, coherence).
 __global__ void __launch_bounds__(256)
 query_morton_kernel(const float *__restrict__ centers, int64_t n, const float *__restrict__ scene,
-                    uint32_t *__restrict__ codes, uint32_t *__restrict__ iota,
-                    uint32_t *status = nullptr, int64_t *__restrict__ offsets = nullptr,
+                    uint32_t *__restrict__ codes, uint32_t *__restrict__ hist, int first_bit,
+                    int passes, uint32_t *status = nullptr, int64_t *__restrict__ offsets = nullptr,
                     int64_t span = 0) {
+    // the digit histograms of the order's sort (sort_prepare)
+    __shared__ uint32_t s_hist[4][kSortDigits];
+    for (int i = threadIdx.x; i < 4 * kSortDigits; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
     // optional fused batch prologue: the value check of the centers
     // (check_queries_kernel) and uniform CRS offsets (uniform_offsets_kernel)
     uint32_t bad = 0;
@@ -998,10 +1030,13 @@ query_morton_kernel(const float *__restrict__ centers, int64_t n, const float *_
             t = fminf(fmaxf(t, 0.0f), 1023.0f);  // NaN -> 0 (flagged by the value check)
             g[a] = (uint32_t)t;
         }
-        codes[i] = (spread_bits(g[0]) << 2) | (spread_bits(g[1]) << 1) | spread_bits(g[2]);
-        iota[i] = (uint32_t)i;
+        const uint32_t code = (spread_bits(g[0]) << 2) | (spread_bits(g[1]) << 1) | spread_bits(g[2]);
+        codes[i] = code;
+        hist_accumulate(s_hist, code, first_bit, passes);
         if (offsets) offsets[i] = i * span;
     }
+    __syncthreads();
+    hist_flush(s_hist, passes, hist);
     if (offsets && blockIdx.x == 0 && threadIdx.x == 0) offsets[n] = n * span;
     if (status) {
         bad = __reduce_or_sync(0xFFFFFFFFu, bad);
@@ -1023,18 +1058,21 @@ int query_order(const float *centers, int64_t nq, const float *scene, int order_
     void *sort_ws = c.take<char>(sort_workspace_bytes(nq));
     // odd pass counts: encode straight into the sort's ping-pong buffers so
     // the last pass writes (codes, order) -- no copy-back
-    const bool odd = (sort_pass_count(30, 30 - order_bits) & 1) != 0;
+    const int first_bit = 30 - order_bits;
+    const int passes = sort_pass_count(30, first_bit);
+    const bool odd = (passes & 1) != 0;
     uint32_t *kin = codes, *vin = order;
     if (odd) sort_alt_buffers(sort_ws, sort_workspace_bytes(nq), nq, &kin, &vin);
+    uint32_t *hist = sort_prepare(sort_ws, sort_workspace_bytes(nq), nq, stream);
     // fp32 codes on the tree's grid: an ordering choice only (results never
-    // depend on it); query_sort_order keeps the exact f64 recipe
-    query_morton_kernel<<<grid_for(nq, 256, 16), 256, 0, stream>>>(centers, nq, scene, kin, vin,
-                                                                  status, offsets, span);
+    // depend on it); query_sort_order keeps the exact f64 recipe.  The values
+    // sorted along are the positions, implicit in the first pass.
+    query_morton_kernel<<<grid_for(nq, 256, 4), 256, 0, stream>>>(centers, nq, scene, kin, hist,
+                                                                 first_bit, passes, status,
+                                                                 offsets, span);
     count_launches(1);
-    int rc = odd ? sort_pairs_from_alt(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq),
-                                       stream, 30 - order_bits)
-                 : sort_pairs(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
-                              30 - order_bits);
+    int rc = sort_pairs_prepared(codes, order, nq, 30, sort_ws, sort_workspace_bytes(nq), stream,
+                                 first_bit, odd);
     if (rc != LBVH_OK) return rc;
     return check_launch();
 }

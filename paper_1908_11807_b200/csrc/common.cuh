@@ -177,6 +177,24 @@ __device__ __forceinline__ T ld_volatile(const T *p) {
     return *reinterpret_cast<const volatile T *>(p);
 }
 
+// Digit histograms of the sort's passes (8-bit digits from first_bit) built
+// by the kernel that produces the keys: shared-memory counts per CTA, one
+// global add per non-empty bin (sort_prepare / sort_pairs_prepared).
+constexpr int kSortDigits = 256;
+__device__ __forceinline__ void hist_accumulate(uint32_t (*s)[kSortDigits], uint32_t key,
+                                                int first_bit, int passes) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+        if (p < passes) atomicAdd(&s[p][(key >> (first_bit + 8 * p)) & (kSortDigits - 1)], 1u);
+}
+__device__ __forceinline__ void hist_flush(const uint32_t (*s)[kSortDigits], int passes,
+                                           uint32_t *hist) {
+    for (int i = threadIdx.x; i < passes * kSortDigits; i += blockDim.x) {
+        const uint32_t c = s[i / kSortDigits][i % kSortDigits];
+        if (c) atomicAdd(hist + i, c);
+    }
+}
+
 inline unsigned int div_up(int64_t a, int64_t b) { return (unsigned int)((a + b - 1) / b); }
 
 // Tuning knob read once from the environment (development A/B switches).

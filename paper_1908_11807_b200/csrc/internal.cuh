@@ -24,6 +24,14 @@ void sort_alt_buffers(void *ws, size_t ws_bytes, int64_t n, uint32_t **k_alt, ui
 int sort_pass_count(int key_bits, int first_bit);
 int sort_pairs_from_alt(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                         size_t ws_bytes, cudaStream_t stream, int first_bit);
+// Fused producers (u32 keys, 8-bit digits): sort_prepare zeroes the sort
+// state and returns the digit-histogram array (4 x 256 counts) that a
+// producer kernel fills while it writes the keys (hist_accumulate /
+// hist_flush); sort_pairs_prepared then sorts with the values implicitly
+// 0..n-1 (argsort: `vals` is written, not read).
+uint32_t *sort_prepare(void *ws, size_t ws_bytes, int64_t n, cudaStream_t stream);
+int sort_pairs_prepared(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+                        size_t ws_bytes, cudaStream_t stream, int first_bit, bool from_alt);
 size_t sort64_workspace_bytes(int64_t n);
 int sort_pairs64(uint64_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                  size_t ws_bytes, cudaStream_t stream);

@@ -123,7 +123,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // One digit pass.  Tiles are claimed in order through `tile_counter`, so a
 // tile only ever waits on tiles already owned by running CTAs.
-template <typename KeyT>
+template <typename KeyT, bool IOTA>
 __global__ void __launch_bounds__(kSortThreads, sizeof(KeyT) == 4 ? LBVH_SORT_MINBLOCKS : 1)
 onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                 KeyT *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t n,
@@ -161,7 +161,8 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
         int64_t i = warp_base + j * 32 + lane;
         bool ok = i < n;
         key[j] = ok ? __ldcs(keys_in + i) : ~(KeyT)0;  // pads sort last
-        val[j] = ok ? __ldcs(vals_in + i) : 0u;
+        // IOTA: no value array, the input values are the positions (argsort)
+        val[j] = ok ? (IOTA ? (uint32_t)i : __ldcs(vals_in + i)) : 0u;
     }
 #if LBVH_SORT_EARLY_AGG
 #pragma unroll
@@ -340,11 +341,24 @@ size_t sort_ws_bytes(int64_t n) {
 // from_alt: the input pairs were written to the workspace's ping-pong buffers
 // (sort_alt_buffers) -- with an odd pass count the result then lands in
 // (keys, vals) without the final device copies.
+// hist_given: sort_prepare() zeroed the state and a producer kernel filled the
+// digit histograms; iota: the input values are the positions 0..n-1 (not read).
 template <typename KeyT>
 int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, size_t ws_bytes,
-              cudaStream_t stream, int first_bit, bool from_alt = false) {
+              cudaStream_t stream, int first_bit, bool from_alt = false, bool hist_given = false,
+              bool iota = false) {
     using C = SortCfg<KeyT>;
-    if (n <= 1) return LBVH_OK;
+    if (n <= 1) {  // nothing to order; the pair may still have to land in place
+        if (n == 1 && from_alt) {
+            Carve c(ws, ws_bytes);
+            KeyT *k_alt = c.take<KeyT>(n);
+            uint32_t *v_alt = c.take<uint32_t>(n);
+            cudaMemcpyAsync(keys, k_alt, sizeof(KeyT), cudaMemcpyDeviceToDevice, stream);
+            if (!iota) cudaMemcpyAsync(vals, v_alt, 4, cudaMemcpyDeviceToDevice, stream);
+        }
+        if (n == 1 && iota) cudaMemsetAsync(vals, 0, 4, stream);
+        return check_launch();
+    }
     if (n >= LBVH_MAX_ITEMS) return LBVH_ERR_TOO_LARGE;
     if (key_bits < 1 || key_bits > (int)(8 * sizeof(KeyT)) || first_bit < 0 ||
         first_bit >= key_bits)
@@ -361,7 +375,7 @@ int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, siz
     uint32_t *lookback = c.take<uint32_t>((size_t)C::kMaxPasses * tiles * kRadix);
     uint32_t *counters = c.take<uint32_t>(C::kMaxPasses);
     size_t zero_end = c.off;
-    cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
+    if (!hist_given) cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
     if (LBVH_SORT_HIST_STRIDE && hist_blocks > (unsigned)(kNumSMs * LBVH_SORT_HIST_STRIDE))
@@ -372,15 +386,22 @@ int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, siz
         ks = k_alt; kd = keys;
         vs = v_alt; vd = vals;
     }
-    histogram_kernel<KeyT><<<hist_blocks, kHistThreads, 0, stream>>>(ks, n, passes, first_bit,
-                                                                      hist);
+    if (!hist_given) {
+        histogram_kernel<KeyT><<<hist_blocks, kHistThreads, 0, stream>>>(ks, n, passes, first_bit,
+                                                                          hist);
+        count_launches(1);
+    }
     exclusive_hist_kernel<<<passes, 32, 0, stream>>>(hist, passes);
-    count_launches(2);
+    count_launches(1);
 
     for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, stream>>>(
-            ks, vs, kd, vd, n, first_bit + p * kRadixBits, hist + p * kRadix,
-            lookback + (size_t)p * tiles * kRadix, counters + p);
+        if (iota && p == 0)
+            onesweep_kernel<KeyT, true><<<(unsigned)tiles, kSortThreads, 0, stream>>>(
+                ks, nullptr, kd, vd, n, first_bit, hist, lookback, counters);
+        else
+            onesweep_kernel<KeyT, false><<<(unsigned)tiles, kSortThreads, 0, stream>>>(
+                ks, vs, kd, vd, n, first_bit + p * kRadixBits, hist + p * kRadix,
+                lookback + (size_t)p * tiles * kRadix, counters + p);
         count_launches(1);
         KeyT *tk = ks; ks = kd; kd = tk;
         uint32_t *tv = vs; vs = vd; vd = tv;
@@ -415,6 +436,26 @@ int sort_pass_count(int key_bits, int first_bit) {
 int sort_pairs_from_alt(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
                         size_t ws_bytes, cudaStream_t stream, int first_bit) {
     return sort_impl<uint32_t>(keys, vals, n, key_bits, ws, ws_bytes, stream, first_bit, true);
+}
+
+uint32_t *sort_prepare(void *ws, size_t ws_bytes, int64_t n, cudaStream_t stream) {
+    using C = SortCfg<uint32_t>;
+    const int64_t tiles = (n + C::kTile - 1) / C::kTile;
+    Carve c(ws, ws_bytes);
+    c.take<uint32_t>(n);
+    c.take<uint32_t>(n);
+    const size_t zero_begin = align_up(c.off);
+    uint32_t *hist = c.take<uint32_t>(C::kMaxPasses * kRadix);
+    c.take<uint32_t>((size_t)C::kMaxPasses * tiles * kRadix);
+    c.take<uint32_t>(C::kMaxPasses);
+    cudaMemsetAsync(c.base + zero_begin, 0, c.off - zero_begin, stream);
+    return hist;
+}
+
+int sort_pairs_prepared(uint32_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,
+                        size_t ws_bytes, cudaStream_t stream, int first_bit, bool from_alt) {
+    return sort_impl<uint32_t>(keys, vals, n, key_bits, ws, ws_bytes, stream, first_bit, from_alt,
+                               true, true);
 }
 
 int sort_pairs64(uint64_t *keys, uint32_t *vals, int64_t n, int key_bits, void *ws,

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 
 import paper_1908_11807_b200 as lb  # noqa: E402
 
-for n in (10_000, 100_000):
+for n in [int(x) for x in (sys.argv[1:] or ["10000", "100000"])]:
     pts = torch.from_numpy(lb.generate(lb.CloudSpec("cube", "filled", n, 0))).cuda()
     for _ in range(5):
         lb.build(pts)
