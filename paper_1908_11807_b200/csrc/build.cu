@@ -348,6 +348,22 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     // this CTA's window of the global hand-off slots starts empty (ordered
     // before any first arrival's publication below by the barrier)
     if (p < n - 1) slots[p] = 0u;
+    // leaf p's box, gathered through the sorted permutation: issued first so
+    // its two dependent loads overlap the code loads and barriers below
+    bool active = p < n;
+    Box mine;
+    uint32_t gobj = 0;
+    if (active) {
+        const uint32_t obj = __ldg(perm + p);
+        // the ordinal this leaf reports: its input index, or leaf_ids[index]
+        gobj = leaf_ids ? (uint32_t)__ldg(leaf_ids + obj) : obj;
+        const bool same = (mins == maxs);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mine.lo[a] = __ldg(mins + 3 * (int64_t)obj + a);
+            mine.hi[a] = same ? mine.lo[a] : __ldg(maxs + 3 * (int64_t)obj + a);
+        }
+    }
     for (int i = tid; i < kHierT + 2; i += kHierT) {
         const int64_t j = B - 1 + i;
         if (j >= 0 && j < n) s_code[i] = __ldg(codes + j);
@@ -363,8 +379,6 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         if (r == n - 1) return false;
         return s_delta[r - B + 1] > s_delta[l - B];
     };
-    bool active = p < n;
-    Box mine;
     int32_t my_link = 0;
     int64_t l = p, r = p;
     if (active) {
@@ -381,16 +395,7 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
                 dir_run(leaf_dir, cb + 1, ((int64_t)1 << dir_bits) + 1, (uint32_t)n, runs,
                         run_count);
         }
-        const uint32_t obj = __ldg(perm + p);
-        // the ordinal this leaf reports: its input index, or leaf_ids[index]
-        const uint32_t gobj = leaf_ids ? (uint32_t)__ldg(leaf_ids + obj) : obj;
         leaf_obj[p] = (int32_t)gobj;
-        const bool same = (mins == maxs);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            mine.lo[a] = __ldg(mins + 3 * (int64_t)obj + a);
-            mine.hi[a] = same ? mine.lo[a] : __ldg(maxs + 3 * (int64_t)obj + a);
-        }
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             node_mins[3 * (internal + p) + a] = mine.lo[a];
@@ -406,8 +411,10 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
             active = false;
         }
     }
+    // side of the current node; the parent's side is computed with the
+    // parent and carried into the next step (one prefix test per level)
+    bool left_side = active && left_child(l, r);
     while (active) {
-        const bool left_side = left_child(l, r);
         const int64_t g = left_side ? r : l - 1;
         if (g < B || g >= E) {  // the parent's other child may lie outside the CTA
             const uint32_t at = atomicAdd(frontier_count, 1u);
@@ -441,7 +448,8 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         const int64_t lc = (pl == g) ? internal + g : g;
         const int64_t rc = (g + 1 == pr) ? internal + g + 1 : g + 1;
         const bool root = (pl == 0 && pr == n - 1);
-        const int64_t pid = root ? 0 : (left_child(pl, pr) ? pr : pl);
+        const bool parent_left = !root && left_child(pl, pr);
+        const int64_t pid = root ? 0 : (parent_left ? pr : pl);
         left[pid] = (int32_t)lc;
         right[pid] = (int32_t)rc;
         Box sb;
@@ -475,6 +483,7 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         }
         l = pl;
         r = pr;
+        left_side = parent_left;
     }
 }
 

@@ -197,12 +197,6 @@ __device__ __forceinline__ void hist_flush(const uint32_t (*s)[kSortDigits], int
 
 inline unsigned int div_up(int64_t a, int64_t b) { return (unsigned int)((a + b - 1) / b); }
 
-// Tuning knob read once from the environment (development A/B switches).
-inline int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
-
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Bump allocator over a caller-owned workspace.
