@@ -430,3 +430,39 @@ def test_heavy_queries_pipelined_host_batch():
     off, idx = oracle.query_spatial_2p(ref, q, r)
     assert int(np.diff(off).max()) > 48
     assert np.array_equal(rs.offsets, off) and np.array_equal(rs.indices, idx)
+
+
+@pytest.mark.parametrize("n", [262_144, 262_145, 300_001])
+def test_frontier_stages_around_the_threshold(n):
+    """Trees up to 4 * 2^16 leaves finish the frontier in one CTA (CTA-scope
+    handshakes), larger ones climb at GPU scope first and defer nodes spanning
+    2^16 leaves to it: byte-identical to the oracle on both sides, for uniform
+    and for clustered codes (many equal Morton codes and long empty leaf-
+    directory runs)."""
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", n, 7))
+    rng = np.random.default_rng(n)
+    clustered = (rng.normal(0.0, 1.0, size=(n, 3)) * rng.choice([0.01, 50.0], size=(n, 1)))
+    for cloud in (pts, clustered.astype(np.float32)):
+        t, ref = lb.build(cloud), oracle.build(cloud)
+        for f in ("node_mins", "node_maxs", "left", "right", "leaf_obj"):
+            assert getattr(t, f).tobytes() == getattr(ref, f).tobytes(), (n, f)
+
+
+@pytest.mark.parametrize("nq", [1, 2, 4095, 4096, 4097, 12_289])
+def test_query_order_sizes_with_implicit_positions(nq):
+    """The query ordering sort takes its digit histograms from the query
+    Morton pass and the positions as implicit values (1 pair and tile-edge
+    batches included): results equal the oracle's, unsorted CRS included."""
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", 20_000, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", nq, 5))
+    t, ref = lb.build(pts), oracle.build(pts)
+    rk = lb.query_knn(t, (q, 10))
+    ko, ki, kd = oracle.query_knn(ref, q, 10)
+    assert np.array_equal(rk.indices, ki) and rk.distances.tobytes() == kd.tobytes()
+    r = datasets.default_radius(10)
+    rs = lb.query_spatial_2p(t, (q, r))
+    off, idx = oracle.query_spatial_2p(ref, q, r)
+    assert np.array_equal(rs.offsets, off) and np.array_equal(rs.indices, idx)
+    qd = torch.from_numpy(q).cuda()
+    rd = lb.query_knn(t, (qd, 10)).to_host()
+    assert np.array_equal(rd.indices, ki)
