@@ -38,9 +38,6 @@ __device__ __forceinline__ void warp_minmax(float v[6]) {
     }
 }
 
-#ifndef LBVH_REDUCE_VEC
-#define LBVH_REDUCE_VEC 1  // point clouds: 3 float4 loads per 4 points (build 1.44 vs 1.46 ms)
-#endif
 // K1: scene box (exact min/max) and the check_boxes value checks.  The last
 // CTA to finish folds the per-CTA partials (threadfence reduction).
 __global__ void __launch_bounds__(kReduceThreads)
@@ -51,9 +48,9 @@ scene_reduce_kernel(const float *__restrict__ mins, const float *__restrict__ ma
     uint32_t bad = 0;
     const bool same = (mins == maxs);
     int64_t first = 0;
-#if LBVH_REDUCE_VEC
     if (same && (reinterpret_cast<uintptr_t>(mins) & 15) == 0) {
         // points: 4 points = 3 float4 per step, axes in a fixed pattern
+        // (build 1.44 vs 1.46 ms against scalar loads)
         const float4 *m4 = reinterpret_cast<const float4 *>(mins);
         const int64_t chunks = n / 4;
         for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks;
@@ -70,7 +67,6 @@ scene_reduce_kernel(const float *__restrict__ mins, const float *__restrict__ ma
         }
         first = chunks * 4;
     }
-#endif
     for (int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll

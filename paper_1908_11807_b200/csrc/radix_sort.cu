@@ -24,31 +24,19 @@ constexpr int kSortWarps = kSortThreads / 32;
 #ifndef LBVH_SORT_ITEMS
 #define LBVH_SORT_ITEMS 16
 #endif
-// Ballot ranking + 4 CTAs/SM (64 registers) measured 9.5% faster builds at
-// 1e7 (1.73 vs 1.91 ms) than MATCH.ANY ranking at 3 CTAs/SM.
-#ifndef LBVH_SORT_BALLOT_RANK
-#define LBVH_SORT_BALLOT_RANK 1
-#endif
+// Measured at 1e7: ballot ranking + 4 CTAs/SM (64
+// registers) 9.5 % faster builds than MATCH.ANY ranking at 3 CTAs/SM; the
+// look-back reads W = 8 predecessors per round trip (0.339 ms vs 0.382 at
+// W = 1, 0.353 at 16, 0.40 at 32); a tile publishes its digit counts right
+// after its loads, before ranking (0.339 vs 0.398 ms); the histogram pass is a
+// grid-stride loop at 2 CTAs/SM (21.7 vs 33 us for one CTA per 8192 keys).
 #ifndef LBVH_SORT_MINBLOCKS
 #define LBVH_SORT_MINBLOCKS 4
 #endif
-// Look-back reads of W predecessors per round trip (with LBVH_SORT_EARLY_AGG:
-// 30-bit sort of 1e7 pairs 0.339 ms at W=8 vs 0.382 (W=1), 0.353 (16), 0.40 (32)).
 #ifndef LBVH_SORT_LOOKBACK_W
 #define LBVH_SORT_LOOKBACK_W 8
 #endif
-// 1: a tile counts its digits with shared-memory atomics right after its
-// loads and publishes the aggregate before ranking, so successors never spin
-// on a predecessor that is still ranking (with W=8: 0.339 vs 0.398 ms).
-#ifndef LBVH_SORT_EARLY_AGG
-#define LBVH_SORT_EARLY_AGG 1
-#endif
-
-// > 0: the digit histogram kernel runs at most this many CTAs per SM over a
-// grid-stride loop (0: one CTA per 8192 keys).
-#ifndef LBVH_SORT_HIST_STRIDE
-#define LBVH_SORT_HIST_STRIDE 2  // 1e7 keys: 21.7 vs 33 us (2 vs 4: same)
-#endif
+constexpr int kHistCtasPerSm = 2;
 
 template <typename KeyT>
 struct SortCfg {
@@ -73,7 +61,6 @@ histogram_kernel(const KeyT *__restrict__ keys, int64_t n, int passes, int first
     __shared__ uint32_t s_hist[P][kRadix];
     for (int i = threadIdx.x; i < P * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
-#if LBVH_SORT_HIST_STRIDE
     // grid-stride over 8192-key chunks, the chunk's loads issued together;
     // a grid of a few CTAs per SM keeps the final global atomics few
     for (int64_t base = (int64_t)blockIdx.x * kHistThreads * kHistItems; base < n;
@@ -95,19 +82,6 @@ histogram_kernel(const KeyT *__restrict__ keys, int64_t n, int passes, int first
                               1u);
         }
     }
-#else
-    int64_t base = (int64_t)blockIdx.x * kHistThreads * kHistItems;
-    for (int j = 0; j < kHistItems; ++j) {
-        int64_t i = base + (int64_t)j * kHistThreads + threadIdx.x;
-        if (i < n) {
-            const KeyT k = __ldcs(keys + i);
-            for (int p = 0; p < passes; ++p)
-                atomicAdd(&s_hist[p][(uint32_t)(k >> (first_bit + p * kRadixBits)) &
-                                     (kRadix - 1)],
-                          1u);
-        }
-    }
-#endif
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
         uint32_t c = (&s_hist[0][0])[i];
@@ -138,7 +112,7 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
     __shared__ int64_t s_global[kRadix];             // global dest of tile position 0 of digit
     __shared__ uint32_t s_scan[kSortWarps];
     __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_cnt[LBVH_SORT_EARLY_AGG ? kRadix : 1];
+    __shared__ uint32_t s_cnt[kRadix];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -146,7 +120,7 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
 
     if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&s_warp[0][0])[i] = 0;
-    if (LBVH_SORT_EARLY_AGG) s_cnt[tid] = 0;
+    s_cnt[tid] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     const int64_t tile_base = (int64_t)tile * kTile;
@@ -164,18 +138,15 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
         // IOTA: no value array, the input values are the positions (argsort)
         val[j] = ok ? (IOTA ? (uint32_t)i : __ldcs(vals_in + i)) : 0u;
     }
-#if LBVH_SORT_EARLY_AGG
 #pragma unroll
     for (int j = 0; j < kItems; ++j) atomicAdd(&s_cnt[(uint32_t)(key[j] >> shift) & (kRadix - 1)], 1u);
     __syncthreads();
     atomicExch(lookback + (size_t)tile * kRadix + tid,
                (tile == 0 ? kFlagPrefix : kFlagAgg) | s_cnt[tid]);
-#endif
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         uint32_t d = (uint32_t)(key[j] >> shift) & (kRadix - 1);
-#if LBVH_SORT_BALLOT_RANK
         // lanes holding the same digit: AND of one ballot per digit bit
         // (independent votes, no MATCH.ANY latency chain)
         uint32_t peers = 0xFFFFFFFFu;
@@ -190,18 +161,6 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
         if ((peers >> lane) == 1u) s_warp[warp][d] = before + __popc(peers);
         rank[j] = before + __popc(peers & lt);
         __syncwarp();
-#else
-        uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-        int leader = __ffs(peers) - 1;
-        uint32_t before = 0;
-        if (lane == leader) {
-            before = s_warp[warp][d];
-            s_warp[warp][d] = before + __popc(peers);
-        }
-        before = __shfl_sync(0xFFFFFFFFu, before, leader);
-        rank[j] = before + __popc(peers & lt);
-        __syncwarp();
-#endif
     }
     __syncthreads();
 
@@ -214,14 +173,8 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
         s_warp[w][d] = total;
         total += c;
     }
-    // Publish the tile aggregate (tile 0 publishes its inclusive prefix).
+    // (the tile aggregate was published right after the loads)
     uint32_t *my_slot = lookback + (size_t)tile * kRadix + d;
-    if (!LBVH_SORT_EARLY_AGG) {
-        if (tile == 0)
-            atomicExch(my_slot, kFlagPrefix | total);
-        else
-            atomicExch(my_slot, kFlagAgg | total);
-    }
 
     // Block-wide exclusive scan of digit totals -> tile-local digit starts.
     uint32_t incl = total;
@@ -242,7 +195,6 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
     uint32_t excl = 0;
     if (tile > 0) {
         int64_t t = (int64_t)tile - 1;
-#if LBVH_SORT_LOOKBACK_W > 1
         // W predecessors per round trip: the loads are independent, so a walk
         // over aggregates costs one L2 latency per W tiles instead of per tile
         constexpr int W = LBVH_SORT_LOOKBACK_W;
@@ -262,15 +214,6 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
                 if (v[i] & kFlagPrefix) done = true;
             }
         }
-#else
-        while (true) {
-            uint32_t v = ld_volatile(lookback + (size_t)t * kRadix + d);
-            if ((v & ~kCountMask) == 0) continue;  // not yet published
-            excl += v & kCountMask;
-            if (v & kFlagPrefix) break;
-            --t;
-        }
-#endif
         atomicExch(my_slot, kFlagPrefix | (excl + total));
     }
     s_global[d] = (int64_t)hist[d] + excl - local_start;
@@ -378,8 +321,7 @@ int sort_impl(KeyT *keys, uint32_t *vals, int64_t n, int key_bits, void *ws, siz
     if (!hist_given) cudaMemsetAsync(c.base + zero_begin, 0, zero_end - zero_begin, stream);
 
     unsigned hist_blocks = div_up(n, (int64_t)kHistThreads * kHistItems);
-    if (LBVH_SORT_HIST_STRIDE && hist_blocks > (unsigned)(kNumSMs * LBVH_SORT_HIST_STRIDE))
-        hist_blocks = kNumSMs * LBVH_SORT_HIST_STRIDE;
+    if (hist_blocks > (unsigned)(kNumSMs * kHistCtasPerSm)) hist_blocks = kNumSMs * kHistCtasPerSm;
     KeyT *ks = keys, *kd = k_alt;
     uint32_t *vs = vals, *vd = v_alt;
     if (from_alt) {
