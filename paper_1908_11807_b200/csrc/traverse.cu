@@ -20,6 +20,8 @@
 
 #include <float.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "internal.cuh"
 #include "topk.cuh"
@@ -877,11 +879,16 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     // shared-memory heap up to 400 slots per query (64 threads x 8 B x k <= 200 KB)
     const size_t smem = (size_t)kHeapThreads * 8 * (size_t)max_span;
     if (max_span <= 400) {
-        static size_t opted = 0;
-        if (smem > opted) {
+        // the opt-in is per device context: remember it per device (atomically,
+        // host threads may launch concurrently)
+        static std::atomic<uint32_t> opted{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint32_t bit = 1u << (dev & 31);
+        if (smem > 48 * 1024 && !(opted.load() & bit)) {
             cudaFuncSetAttribute(knn_smem_heap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(kHeapThreads * 8 * 400));
-            opted = (size_t)kHeapThreads * 8 * 400;
+            opted.fetch_or(bit);
         }
         knn_smem_heap_kernel<<<div_up(nq, kHeapThreads), kHeapThreads, smem, stream>>>(
             *t, centers, order, nq, offsets, out_idx, out_dist, squared, status);
