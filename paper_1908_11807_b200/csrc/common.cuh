@@ -135,6 +135,18 @@ __device__ __forceinline__ float4 ld_shared_v4(const void *p) {
     return v;
 }
 
+// Plain 32-bit shared-memory accesses through a shared-window address (the
+// kNN stack): volatile so they stay ordered with each other like the array
+// accesses they replace.
+__device__ __forceinline__ void st_shared_s32(uint32_t addr, int32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_shared_s32(uint32_t addr) {
+    int32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 // GPU-scope release+acquire read-modify-writes (no full membar).
 __device__ __forceinline__ uint32_t atomic_exch_acq_rel(uint32_t *p, uint32_t v) {
     uint32_t old;

@@ -315,7 +315,10 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     static_assert(SMS > 0 && SMS <= kStack, "shared-memory stack depth");
     int32_t lstack[kStack];
     __shared__ int32_t sst[SMS * LBVH_KNN_BLOCK];
-    int32_t *const sbase = sst + (threadIdx.x % LBVH_KNN_BLOCK);
+    // 32-bit shared-window address of this lane's column, formed once: through
+    // a generic pointer every push re-derived it (S2UR/ULEA, ~10 instructions)
+    uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sst + (threadIdx.x % LBVH_KNN_BLOCK));
+    asm volatile("" : "+r"(sbase));  // opaque: kept in a register, not re-derived per push
     uint32_t fail = 0;
     int sp = 0;
     int32_t node = 0;  // the root; never pruned (the list is empty)
@@ -345,7 +348,7 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
                     break;
                 }
                 if (sp < SMS)
-                    sbase[sp * LBVH_KNN_BLOCK] = fl;
+                    st_shared_s32(sbase + sp * (4 * LBVH_KNN_BLOCK), fl);
                 else
                     lstack[sp] = fl;
                 ++sp;
@@ -365,7 +368,7 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         if (next < 0) {
             if (sp == 0) break;
             --sp;
-            next = sp < SMS ? sbase[sp * LBVH_KNN_BLOCK] : lstack[sp];
+            next = sp < SMS ? ld_shared_s32(sbase + sp * (4 * LBVH_KNN_BLOCK)) : lstack[sp];
         }
         node = next;
     }
