@@ -68,12 +68,14 @@ __device__ __forceinline__ void load_node(const PackedNode *__restrict__ nodes, 
 }
 
 // One hit (leaf ordinal `obj`); returns false when the 1P row overflows.
+// `dst` is the query's span / row (out + its base), `cap` its width: 32-bit
+// compares and addressing on the per-hit path.
 template <int MODE>
-__device__ __forceinline__ bool emit(int32_t *__restrict__ out, int64_t base, int32_t &cnt,
-                                     int64_t cap, int32_t obj) {
+__device__ __forceinline__ bool emit(int32_t *__restrict__ dst, int32_t &cnt, int32_t cap,
+                                     int32_t obj) {
     if (MODE == kBuffer && cnt >= cap) return false;
-    if (MODE == kFill || MODE == kBuffer) out[base + cnt] = obj;
-    if (MODE == kCountBuf && cnt < cap) out[base + cnt] = obj;
+    if (MODE == kFill || MODE == kBuffer) dst[cnt] = obj;
+    if (MODE == kCountBuf && cnt < cap) dst[cnt] = obj;
     ++cnt;
     return true;
 }
@@ -101,9 +103,11 @@ __device__ __forceinline__ void spatial_query(const lbvh_tree &t,
     if (MODE == kFill) base = __ldg(offsets + q);
     if (MODE == kBuffer || MODE == kCountBuf) base = q * cap;
     int32_t cnt = 0;
+    int32_t *const dst = out + base;
+    const int32_t cap32 = (int32_t)cap;  // row widths and 1P buffers are < 2^31
     int32_t spill_cur = 0, spill_slot = 0;  // current pool chunk (0: none yet, -1: failed)
     auto hit = [&](int32_t obj) -> bool {
-        if (MODE == kCountBuf && cnt >= cap) {
+        if (MODE == kCountBuf && cnt >= cap32) {
             if (pool.pool && spill_cur >= 0) {
                 if (spill_cur == 0 || spill_slot == kSpillChunk - 1) {
                     const uint32_t c = atomicAdd(reinterpret_cast<uint32_t *>(pool.pool), 1u) + 1u;
@@ -125,7 +129,7 @@ __device__ __forceinline__ void spatial_query(const lbvh_tree &t,
             ++cnt;
             return true;
         }
-        return emit<MODE>(out, base, cnt, cap, obj);
+        return emit<MODE>(dst, cnt, cap32, obj);
     };
     if (t.n == 1) {
         const float *bx = t.root_box;
