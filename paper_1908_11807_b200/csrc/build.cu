@@ -336,17 +336,20 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     __shared__ CodeT s_code[kHierT + 2];     // codes[B - 1 + i]
     __shared__ uint8_t s_delta[kHierT + 1];  // delta(B - 1 + i)
     const int tid = threadIdx.x;
-    const int64_t B = (int64_t)blockIdx.x * kHierT;
-    const int64_t E = (B + kHierT < n ? B + kHierT : n) - 1;
-    const int64_t p = B + tid;
-    const int64_t internal = n - 1;
+    // 32-bit indices throughout (trees hold < 2^30 leaves): the climb's
+    // range and node arithmetic stays single-instruction
+    const int32_t nn = (int32_t)n;
+    const int32_t B = (int32_t)blockIdx.x * kHierT;
+    const int32_t E = (B + kHierT < nn ? B + kHierT : nn) - 1;
+    const int32_t p = B + tid;
+    const int32_t internal = nn - 1;
     s_slot[tid] = 0;
     // this CTA's window of the global hand-off slots starts empty (ordered
     // before any first arrival's publication below by the barrier)
-    if (p < n - 1) slots[p] = 0u;
+    if (p < nn - 1) slots[p] = 0u;
     // leaf p's box, gathered through the sorted permutation: issued first so
     // its two dependent loads overlap the code loads and barriers below
-    bool active = p < n;
+    bool active = p < nn;
     Box mine;
     uint32_t gobj = 0;
     if (active) {
@@ -361,22 +364,22 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
         }
     }
     for (int i = tid; i < kHierT + 2; i += kHierT) {
-        const int64_t j = B - 1 + i;
-        if (j >= 0 && j < n) s_code[i] = __ldg(codes + j);
+        const int32_t j = B - 1 + i;
+        if (j >= 0 && j < nn) s_code[i] = __ldg(codes + j);
     }
     __syncthreads();
-    if (p < n - 1) s_delta[tid + 1] = (uint8_t)delta_of(s_code[tid + 1], s_code[tid + 2], p);
+    if (p < nn - 1) s_delta[tid + 1] = (uint8_t)delta_of(s_code[tid + 1], s_code[tid + 2], p);
     if (tid == 0 && B > 0) s_delta[0] = (uint8_t)delta_of(s_code[0], s_code[1], B - 1);
     __syncthreads();
     // is_left_child over the CTA's range: l >= B and r <= E, so both prefixes
     // delta(r) and delta(l - 1) are in s_delta
-    auto left_child = [&](int64_t l, int64_t r) -> bool {
+    auto left_child = [&](int32_t l, int32_t r) -> bool {
         if (l == 0) return true;
-        if (r == n - 1) return false;
+        if (r == nn - 1) return false;
         return s_delta[r - B + 1] > s_delta[l - B];
     };
     int32_t my_link = 0;
-    int64_t l = p, r = p;
+    int32_t l = p, r = p;
     if (active) {
         const uint32_t c30 = code30(s_code[tid + 1]);
         if (leaf_codes) leaf_codes[p] = c30;
@@ -387,18 +390,18 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
             const int64_t cb = (int64_t)(c30 >> sh);
             const int64_t pb = p == 0 ? -1 : (int64_t)(code30(s_code[tid]) >> sh);
             dir_run(leaf_dir, pb + 1, cb + 1, (uint32_t)p, runs, run_count);
-            if (p == n - 1)
+            if (p == nn - 1)
                 dir_run(leaf_dir, cb + 1, ((int64_t)1 << dir_bits) + 1, (uint32_t)n, runs,
                         run_count);
         }
         leaf_obj[p] = (int32_t)gobj;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            node_mins[3 * (internal + p) + a] = mine.lo[a];
-            if (leaf_maxs_rows) node_maxs[3 * (internal + p) + a] = mine.hi[a];
+            node_mins[3 * (int64_t)(internal + p) + a] = mine.lo[a];
+            if (leaf_maxs_rows) node_maxs[3 * (int64_t)(internal + p) + a] = mine.hi[a];
         }
         my_link = (int32_t)(gobj | kLeafTag);
-        if (n == 1) {  // leaf-only tree (tree.py:177-209 with n == 1)
+        if (nn == 1) {  // leaf-only tree (tree.py:177-209 with n == 1)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 root_box[a] = mine.lo[a];
@@ -411,13 +414,13 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
     // parent and carried into the next step (one prefix test per level)
     bool left_side = active && left_child(l, r);
     while (active) {
-        const int64_t g = left_side ? r : l - 1;
+        const int32_t g = left_side ? r : l - 1;
         if (g < B || g >= E) {  // the parent's other child may lie outside the CTA
             const uint32_t at = atomicAdd(frontier_count, 1u);
             frontier[at] = make_uint2((uint32_t)l, (uint32_t)r);
             break;
         }
-        const int s = (int)(g - B);
+        const int s = g - B;
         const int side = left_side ? 0 : 1;
         // hand-off slots are accessed only through shared-memory atomics (the
         // fence + exchange below orders them; atomics also keep racecheck exact)
@@ -439,13 +442,13 @@ hierarchy_local_kernel(const CodeT *__restrict__ codes, const uint32_t *__restri
             break;  // the sibling continues
         }
         __threadfence_block();
-        const int64_t pl = left_side ? l : (int64_t)(other - 1u);
-        const int64_t pr = left_side ? (int64_t)(other - 1u) : r;
-        const int64_t lc = (pl == g) ? internal + g : g;
-        const int64_t rc = (g + 1 == pr) ? internal + g + 1 : g + 1;
-        const bool root = (pl == 0 && pr == n - 1);
+        const int32_t pl = left_side ? l : (int32_t)(other - 1u);
+        const int32_t pr = left_side ? (int32_t)(other - 1u) : r;
+        const int32_t lc = (pl == g) ? internal + g : g;
+        const int32_t rc = (g + 1 == pr) ? internal + g + 1 : g + 1;
+        const bool root = (pl == 0 && pr == nn - 1);
         const bool parent_left = !root && left_child(pl, pr);
-        const int64_t pid = root ? 0 : (parent_left ? pr : pl);
+        const int32_t pid = root ? 0 : (parent_left ? pr : pl);
         left[pid] = (int32_t)lc;
         right[pid] = (int32_t)rc;
         Box sb;
