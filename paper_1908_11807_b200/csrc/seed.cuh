@@ -41,13 +41,24 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
 #pragma unroll
     for (int j = 0; j < K; ++j) best[j] = (j < K - kk) ? -INFINITY : INFINITY;
     const float *__restrict__ mn = t.node_mins + 3 * (n - 1);
-    // point leaves: maxs == mins (a deferred build leaves node_maxs leaf rows unwritten)
-    const float *__restrict__ mx =
-        (t.flags & LBVH_TREE_POINT_LEAVES) ? mn : t.node_maxs + 3 * (n - 1);
+    // point leaves: maxs == mins (a deferred build leaves node_maxs leaf rows
+    // unwritten), three loads per leaf, and the box distance of a point box is
+    // bit for bit the sum of squared differences (the gap is |v - x| either
+    // way round, rounded the same)
+    const bool points = (t.flags & LBVH_TREE_POINT_LEAVES) != 0;
+    const float *__restrict__ mx = points ? mn : t.node_maxs + 3 * (n - 1);
     for (int64_t p = w0; p < w1; ++p) {
-        const float d = box_dist_sq(px, py, pz, __ldg(mn + 3 * p), __ldg(mn + 3 * p + 1),
-                                    __ldg(mn + 3 * p + 2), __ldg(mx + 3 * p),
-                                    __ldg(mx + 3 * p + 1), __ldg(mx + 3 * p + 2));
+        float d;
+        if (points) {
+            const float dx = __fsub_rn(px, __ldg(mn + 3 * p));
+            const float dy = __fsub_rn(py, __ldg(mn + 3 * p + 1));
+            const float dz = __fsub_rn(pz, __ldg(mn + 3 * p + 2));
+            d = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+        } else {
+            d = box_dist_sq(px, py, pz, __ldg(mn + 3 * p), __ldg(mn + 3 * p + 1),
+                            __ldg(mn + 3 * p + 2), __ldg(mx + 3 * p), __ldg(mx + 3 * p + 1),
+                            __ldg(mx + 3 * p + 2));
+        }
         if (d < best[K - 1]) {
             bool lt[K];
 #pragma unroll
