@@ -151,6 +151,7 @@ __device__ __forceinline__ void spatial_query(const lbvh_tree &t,
     // testing for an empty stack (C3 4.23 -> 4.13 ms; an unconditional push
     // as well cost C2 1 %).
     int32_t mem[kStack];
+    mem[0] = 0;  // the dummy: defined, never used
     int32_t stop = 0;
     int sp = 0;
     int32_t node = 0;
