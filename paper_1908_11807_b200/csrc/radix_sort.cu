@@ -109,7 +109,7 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
     __shared__ uint32_t s_vals[kTile];
     __shared__ uint32_t s_warp[kSortWarps][kRadix];  // counts -> warp exclusive offsets
     __shared__ uint32_t s_local[kRadix];             // digit start within the tile
-    __shared__ int64_t s_global[kRadix];             // global dest of tile position 0 of digit
+    __shared__ uint32_t s_global[kRadix];            // global dest of tile position 0 of digit
     __shared__ uint32_t s_scan[kSortWarps];
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_cnt[kRadix];
@@ -123,8 +123,10 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
     s_cnt[tid] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
-    const int64_t tile_base = (int64_t)tile * kTile;
-    const int64_t warp_base = tile_base + (int64_t)warp * 32 * kItems;
+    // 32-bit positions (sorts hold < 2^30 pairs): single-instruction index math
+    const uint32_t nn = (uint32_t)n;
+    const uint32_t tile_base = tile * kTile;
+    const uint32_t warp_base = tile_base + warp * 32 * kItems;
 
     // Warp-striped load: item j of a lane sits at warp_base + j*32 + lane, so
     // (j, lane) order is position order and the ranking below is stable.
@@ -132,8 +134,8 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
     uint32_t val[kItems], rank[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-        int64_t i = warp_base + j * 32 + lane;
-        bool ok = i < n;
+        const uint32_t i = warp_base + j * 32 + lane;
+        const bool ok = i < nn;
         key[j] = ok ? __ldcs(keys_in + i) : ~(KeyT)0;  // pads sort last
         // IOTA: no value array, the input values are the positions (argsort)
         val[j] = ok ? (IOTA ? (uint32_t)i : __ldcs(vals_in + i)) : 0u;
@@ -216,7 +218,7 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
         }
         atomicExch(my_slot, kFlagPrefix | (excl + total));
     }
-    s_global[d] = (int64_t)hist[d] + excl - local_start;
+    s_global[d] = hist[d] + excl - local_start;  // wraps back into range at use
     __syncthreads();
 
     // Scatter into shared memory in tile-sorted order.
@@ -230,12 +232,12 @@ onesweep_kernel(const KeyT *__restrict__ keys_in, const uint32_t *__restrict__ v
     __syncthreads();
 
     // Pads (all-ones keys, positions >= n) are last in tile order.
-    const int64_t valid = (n - tile_base) < kTile ? (n - tile_base) : kTile;
+    const uint32_t valid = (nn - tile_base) < (uint32_t)kTile ? (nn - tile_base) : (uint32_t)kTile;
 #pragma unroll 4
     for (int i = tid; i < kTile; i += kSortThreads) {
-        if (i < valid) {
+        if ((uint32_t)i < valid) {
             const KeyT k = s_keys[i];
-            int64_t dst = s_global[(uint32_t)(k >> shift) & (kRadix - 1)] + i;
+            const uint32_t dst = s_global[(uint32_t)(k >> shift) & (kRadix - 1)] + (uint32_t)i;
             keys_out[dst] = k;
             vals_out[dst] = s_vals[i];
         }
