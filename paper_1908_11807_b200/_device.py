@@ -20,9 +20,17 @@ _NP2T = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float6
          np.dtype(np.uint8): torch.uint8, np.dtype(np.uint32): torch.uint32}
 
 
+_DEVICES = {}  # current device index -> torch.device (the library checked once)
+
+
 def device() -> torch.device:
-    _lib.lib()  # asserts CUDA + library
-    return torch.device("cuda", torch.cuda.current_device())
+    if not _DEVICES:
+        _lib.lib()  # asserts CUDA + library (the reference's errors without them)
+    idx = torch.cuda.current_device()
+    d = _DEVICES.get(idx)
+    if d is None:
+        d = _DEVICES[idx] = torch.device("cuda", idx)
+    return d
 
 
 _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
