@@ -89,25 +89,36 @@ scan_kernel(In in, int64_t n, int64_t *__restrict__ offsets, uint64_t *lookback,
         warp_off += (w < warp) ? t : 0;
         tile_total += t;
     }
-    if (tid == 0) {
+    // Publish the aggregate, then warp 0 walks back 32 predecessors per round
+    // trip: the nearest lane holding an inclusive prefix ends the walk, the
+    // lanes before it add their aggregates (tiles before 0 read as prefix 0).
+    if (warp == 0) {
         uint64_t *slot = lookback + tile;
         int64_t excl = 0;
         if (tile == 0) {
-            atomicExch((unsigned long long *)slot, kPrefix | (uint64_t)tile_total);
+            if (lane == 0) atomicExch((unsigned long long *)slot, kPrefix | (uint64_t)tile_total);
         } else {
-            atomicExch((unsigned long long *)slot, kAgg | (uint64_t)tile_total);
-            int64_t t = tile - 1;
+            if (lane == 0) atomicExch((unsigned long long *)slot, kAgg | (uint64_t)tile_total);
+            int64_t t = tile - 1 - lane;
             while (true) {
-                uint64_t v = ld_volatile(lookback + t);
-                if ((v & ~kValMask) == 0) continue;
-                excl += (int64_t)(v & kValMask);
-                if (v & kPrefix) break;
-                --t;
+                const uint64_t v = t >= 0 ? ld_volatile(lookback + t) : kPrefix;
+                if (!__all_sync(0xFFFFFFFFu, (v & ~kValMask) != 0)) continue;  // not all published
+                const uint32_t pm = __ballot_sync(0xFFFFFFFFu, (v & kPrefix) != 0);
+                const int stop = pm ? __ffs(pm) - 1 : 31;
+                int64_t part = lane <= stop ? (int64_t)(v & kValMask) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+                excl += part;
+                if (pm) break;
+                t -= 32;
             }
-            atomicExch((unsigned long long *)slot, kPrefix | (uint64_t)(excl + tile_total));
+            if (lane == 0)
+                atomicExch((unsigned long long *)slot, kPrefix | (uint64_t)(excl + tile_total));
         }
-        s_prefix = excl;
-        if (tile == 0) offsets[0] = 0;
+        if (lane == 0) {
+            s_prefix = excl;
+            if (tile == 0) offsets[0] = 0;
+        }
     }
     __syncthreads();
     // Inclusive results back through shared memory, then coalesced stores
