@@ -53,7 +53,9 @@ int query_order(const float *, int64_t, const float *, int, uint32_t *, uint32_t
 int spatial_count(const lbvh_tree *, const float *, const float *, float, const uint32_t *,
                   int64_t, int32_t *, int32_t *, int64_t, uint32_t *, cudaStream_t,
                   int32_t *spill_heads = nullptr, int32_t *spill_pool = nullptr,
-                  int64_t spill_chunks = 0);
+                  int64_t spill_chunks = 0, uint32_t *over_list = nullptr,
+                  uint32_t *over_n = nullptr, uint32_t *spill_list = nullptr,
+                  uint32_t *spill_n = nullptr);
 int spill_copy(const int32_t *, int64_t, const int32_t *, const int64_t *, const int32_t *,
                const int32_t *, const uint32_t *, const uint32_t *, int64_t, int32_t *,
                cudaStream_t);
@@ -323,18 +325,16 @@ int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const 
     }
     const uint32_t *ord = sorted ? order : nullptr;
     if (ev_before) cudaEventRecord((cudaEvent_t)ev_before, st);
+    // the overflow (fill) and spill lists are appended as queries finish:
+    // the fill pass and the spill copy take queries in any order
     rc = spatial_count(tree, centers, radii, radius, ord, nq, counts, rows > 0 ? buf : nullptr,
                        rows, status, st, spill ? spill_heads : nullptr,
-                       spill ? spill_pool : nullptr, spill ? spill_chunks : 0);
+                       spill ? spill_pool : nullptr, spill ? spill_chunks : 0,
+                       rows > 0 ? over_list : nullptr, rows > 0 ? over_n : nullptr,
+                       spill ? spill_list : nullptr, spill ? spill_n : nullptr);
     if (ev_after) cudaEventRecord((cudaEvent_t)ev_after, st);
     if (rc) return rc;
-    rc = scan_counts(counts, nq, offsets, ws, ws_bytes, st);
-    if (rc) return rc;
-    if (rows > 0)
-        return select_overflow(ord, counts, nq, rows, over_list, over_n, st,
-                               spill ? spill_heads : nullptr, spill ? spill_list : nullptr,
-                               spill ? spill_n : nullptr);
-    return LBVH_OK;
+    return scan_counts(counts, nq, offsets, ws, ws_bytes, st);
 }
 
 int lbvh_knn_kth(const lbvh_tree *tree, const float *centers, const uint32_t *order,

@@ -53,7 +53,26 @@ struct SpillPool {
                       // first chunk, or -1 = pool exhausted (fill pass)
     int32_t *pool;    // chunks of kSpillChunk ints
     uint32_t chunks;  // pool capacity in chunks, the reserved chunk included
+    // Optional lists built as queries finish (warp-aggregated appends):
+    // queries whose hits overflowed the row and are not all in the pool (the
+    // fill pass revisits them), and queries whose overflow is all in the pool
+    // (spill_copy).  Counters zeroed by the caller.
+    uint32_t *over_list, *over_n, *spill_list, *spill_n;
 };
+
+// Append q to list if `take`, one atomic per converged group of lanes.
+__device__ __forceinline__ void append_active(bool take, uint32_t q, uint32_t *list,
+                                              uint32_t *count) {
+    const unsigned am = __activemask();
+    const unsigned m = __ballot_sync(am, take);
+    if (!m) return;
+    const int lane = (int)lane_id();
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
+    base = __shfl_sync(am, base, leader);
+    if (take) list[base + __popc(m & ((1u << lane) - 1u))] = q;
+}
 
 // The 64-byte record in two 256-bit loads (sm_100 LDG.E.ENL2.256): kNN 8.30 vs
 // 8.48 ms and radius 2P 6.09 vs 7.01 ms against four 128-bit loads (C2).
@@ -206,6 +225,12 @@ __device__ __forceinline__ void spatial_query(const lbvh_tree &t,
     }
     if (fail) atomicOr(status, fail);
     if (MODE != kFill) counts[q] = cnt;
+    if (MODE == kCountBuf && pool.over_list) {
+        const bool over = cnt > cap32;
+        const bool spilled = over && pool.pool && spill_cur > 0;
+        append_active(over && !spilled, (uint32_t)q, pool.over_list, pool.over_n);
+        if (pool.spill_list) append_active(spilled, (uint32_t)q, pool.spill_list, pool.spill_n);
+    }
 }
 
 template <int MODE>
@@ -710,15 +735,27 @@ int launch_spatial(const lbvh_tree *t, const float *centers, const float *radii,
 int spatial_count(const lbvh_tree *t, const float *centers, const float *radii, float radius,
                   const uint32_t *order, int64_t nq, int32_t *counts, int32_t *buf, int64_t cap,
                   uint32_t *status, cudaStream_t stream, int32_t *spill_heads,
-                  int32_t *spill_pool, int64_t spill_chunks) {
+                  int32_t *spill_pool, int64_t spill_chunks, uint32_t *over_list,
+                  uint32_t *over_n, uint32_t *spill_list, uint32_t *spill_n) {
     if (buf) {
         if (cap < 1) return LBVH_ERR_INVALID_ARG;
         SpillPool sp = {};
         if (spill_pool && spill_heads && spill_chunks > 1) {
-            sp = SpillPool{spill_heads, spill_pool,
-                           (uint32_t)(spill_chunks < (int64_t)1 << 31 ? spill_chunks
-                                                                      : (int64_t)1 << 31)};
+            sp.heads = spill_heads;
+            sp.pool = spill_pool;
+            sp.chunks = (uint32_t)(spill_chunks < (int64_t)1 << 31 ? spill_chunks
+                                                                   : (int64_t)1 << 31);
             cudaMemsetAsync(spill_pool, 0, sizeof(uint32_t), stream);  // allocation counter
+            if (spill_list && spill_n) {
+                sp.spill_list = spill_list;
+                sp.spill_n = spill_n;
+                cudaMemsetAsync(spill_n, 0, sizeof(uint32_t), stream);
+            }
+        }
+        if (over_list && over_n) {
+            sp.over_list = over_list;
+            sp.over_n = over_n;
+            cudaMemsetAsync(over_n, 0, sizeof(uint32_t), stream);
         }
         return launch_spatial<kCountBuf>(t, centers, radii, radius, order, nq, counts, nullptr,
                                          buf, cap, nullptr, status, stream, sp);
