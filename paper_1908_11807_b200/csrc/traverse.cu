@@ -997,52 +997,39 @@ select_overflow_kernel(const uint32_t *__restrict__ order, const int32_t *__rest
 }
 
 // Spilled queries' spans: the row (first `cap` hits) then the pool chunks,
-// one warp per query, consecutive lanes on consecutive output words; each
-// lane has all of its loads of a chunk in flight before it stores, and the
-// next chunk's index is read with them.
+// one half-warp per query (two queries' chunk chains in flight per warp),
+// consecutive lanes on consecutive output words; each lane has all of its
+// loads of a chunk in flight before it stores, the next chunk's index among them.
 __global__ void __launch_bounds__(256)
 spill_copy_kernel(const int32_t *__restrict__ buf, int64_t cap,
                   const int32_t *__restrict__ counts, const int64_t *__restrict__ offsets,
                   const int32_t *__restrict__ heads, const int32_t *__restrict__ pool,
                   const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_len,
                   int32_t *__restrict__ out) {
-    constexpr int kPer = (kSpillChunk + 31) / 32;  // words per lane per chunk
-    const int lane = threadIdx.x & 31;
+    constexpr int kG = 16;                           // lanes per query
+    constexpr int kPer = (kSpillChunk + kG - 1) / kG;  // words per lane per chunk
+    const int g = threadIdx.x & (kG - 1);
+    const unsigned gmask = 0xFFFFu << (threadIdx.x & 16);  // this half-warp
     const int64_t n = (int64_t)*list_len;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += warps) {
+    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / kG;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG; w < n; w += groups) {
         const int64_t q = __ldg(list + w);
         const int64_t cnt = __ldg(counts + q);
         int32_t *dst = out + __ldg(offsets + q);
         int64_t c = __ldg(heads + q);
         const int32_t *row = buf + q * cap;
-        for (int64_t j0 = 0; j0 < cap; j0 += 32 * kPer) {
-            int32_t v[kPer];
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int64_t j = j0 + u * 32 + lane;
-                v[u] = j < cap ? __ldcs(row + j) : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int64_t j = j0 + u * 32 + lane;
-                if (j < cap) dst[j] = v[u];
-            }
-        }
+        for (int64_t j = g; j < cap; j += kG) dst[j] = __ldcs(row + j);
         int64_t done = cap;
         while (done < cnt) {
             const int64_t take = cnt - done < kSpillChunk - 1 ? cnt - done : kSpillChunk - 1;
             const int32_t *ch = pool + c * kSpillChunk;
             int32_t v[kPer];
 #pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int j = u * 32 + lane;
-                v[u] = j < kSpillChunk ? __ldcs(ch + j) : 0;  // slot 127: the next chunk
-            }
-            const int64_t next = __shfl_sync(0xFFFFFFFFu, v[kPer - 1], 31);
+            for (int u = 0; u < kPer; ++u) v[u] = __ldcs(ch + u * kG + g);  // slot 127: the link
+            const int64_t next = __shfl_sync(gmask, v[kPer - 1], kG - 1, kG);
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
-                const int j = u * 32 + lane;
+                const int j = u * kG + g;
                 if (j < take) dst[done + j] = v[u];
             }
             done += take;
@@ -1073,7 +1060,7 @@ int spill_copy(const int32_t *buf, int64_t cap, const int32_t *counts, const int
     if (max_list == 0) return LBVH_OK;
     if (!buf || !counts || !offsets || !heads || !pool || !list || !list_len || !out)
         return LBVH_ERR_INVALID_ARG;
-    int64_t ctas = (max_list + 7) / 8;
+    int64_t ctas = (max_list + 15) / 16;  // 16 queries per 256-thread CTA
     const int64_t lim = (int64_t)kNumSMs * 8;
     spill_copy_kernel<<<(unsigned)(ctas < lim ? ctas : lim), 256, 0, stream>>>(
         buf, cap, counts, offsets, heads, pool, list, list_len, out);
