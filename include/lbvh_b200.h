@@ -293,7 +293,7 @@ int lbvh_knn(const lbvh_tree *tree, const float *centers, const uint32_t *order,
  * listed in spill_list / spill_n (copy them with lbvh_spill_copy); only the
  * rest go to over_list (fill pass).  Hit order is the fill order either way.
  * ev_before / ev_after (optional) bracket the count kernel. */
-#define LBVH_SPILL_CHUNK 128
+#define LBVH_SPILL_CHUNK 256
 size_t lbvh_spatial_count_batch_workspace_bytes(int64_t nq);
 int lbvh_spatial_count_batch(const lbvh_tree *tree, const float *centers, const float *radii,
                              float radius, int64_t nq, int order_bits, int64_t rows,

@@ -52,7 +52,7 @@ class CTree(ctypes.Structure):
 TREE_POINT_LEAVES = 0x1
 TREE_CODES30 = 0x2
 TREE_BUILT = 0x4
-SPILL_CHUNK = 128
+SPILL_CHUNK = 256
 
 
 _SIGS = {

@@ -110,7 +110,7 @@ const char *lbvh_strerror(int code) {
 
 const char *lbvh_last_cuda_error(void) { return g_cuda_err; }
 
-int lbvh_abi_version(void) { return 4; }
+int lbvh_abi_version(void) { return 5; }
 
 uint64_t lbvh_launch_count(void) { return launch_count(); }
 

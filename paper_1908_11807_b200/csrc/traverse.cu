@@ -47,7 +47,7 @@ enum SpatialMode {
 // count pass keeps EVERY hit, in fill order, and heavy queries (C3: 3.6 % of
 // the queries hold 99 % of the hits) need no second traversal; only queries
 // that find the pool exhausted are traversed again by the fill pass.
-constexpr int kSpillChunk = 128;
+constexpr int kSpillChunk = LBVH_SPILL_CHUNK;
 struct SpillPool {
     int32_t *heads;   // per query, written when its count exceeds the row:
                       // first chunk, or -1 = pool exhausted (fill pass)

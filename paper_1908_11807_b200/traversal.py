@@ -332,7 +332,7 @@ def _finish(host: bool, status: dv.Status, *arrays):
 # buffer is skipped when it would exceed _ROW_BUDGET bytes.
 _ROW_HITS = 48
 _ROW_BUDGET = 8 << 30
-# Hits beyond the row are kept by the count pass in a pool of 128-int chunks
+# Hits beyond the row are kept by the count pass in a pool of LBVH_SPILL_CHUNK-int chunks
 # (lbvh_spatial_count_batch's spill pool), so heavy queries are traversed
 # once; sized at _SPILL_INTS ints per query (C3 needs ~8.2), a query that
 # finds it exhausted falls back to the fill pass.

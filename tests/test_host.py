@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     lib = _lib.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.lbvh_abi_version() == 4
+    assert lib.lbvh_abi_version() == 5
     assert set(_lib.exported_symbols()) == set(header_functions())
 
 
