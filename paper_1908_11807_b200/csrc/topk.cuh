@@ -68,4 +68,65 @@ struct TopK {
     }
 };
 
+
+// The same list held as separate 32-bit fields (distance bits, ordinal + 1),
+// for the kNN traversal: unless a candidate's distance equals a kept one,
+// the distance words alone order it -- one 32-bit compare per slot, where
+// the 64-bit key costs ptxas a >= and a > pair per slot; exact ties take the
+// lexicographic path.  Same order, same results as TopK.
+template <int K>
+struct TopKSplit {
+    uint32_t d[K], o[K];
+#ifdef LBVH_KNN_COUNT_VISITS
+    int kept = 0;
+#endif
+    __device__ __forceinline__ void init(int kk, float bound) {
+        const bool none = isnan(bound);
+        const uint32_t ed = none ? 0xFFFFFFFFu : __float_as_uint(bound);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            d[j] = (j < K - kk) ? 0u : ed;
+            o[j] = (j < K - kk) ? 0u : 0xFFFFFFFFu;
+        }
+    }
+    __device__ __forceinline__ float worst() const { return __uint_as_float(d[K - 1]); }
+    __device__ __forceinline__ float dist(int j) const { return __uint_as_float(d[j]); }
+    __device__ __forceinline__ int32_t ordinal(int j) const { return (int32_t)o[j] - 1; }
+
+    __device__ __forceinline__ void offer(float cd, int32_t obj) {
+        const uint32_t cdu = __float_as_uint(cd), cou = (uint32_t)(obj + 1);
+        // keep iff (cd, obj) beats the k-th best (_kernels.py:387-395)
+        if (!(cdu < d[K - 1] || (cdu == d[K - 1] && cou < o[K - 1]))) return;
+#ifdef LBVH_KNN_COUNT_VISITS
+        ++kept;
+#endif
+        bool tie = false;
+#pragma unroll
+        for (int j = 0; j < K; ++j) tie |= d[j] == cdu;
+        if (!tie) {
+            bool lt[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) lt[j] = d[j] < cdu;
+#pragma unroll
+            for (int j = K - 1; j > 0; --j) {
+                d[j] = lt[j] ? d[j] : (lt[j - 1] ? cdu : d[j - 1]);
+                o[j] = lt[j] ? o[j] : (lt[j - 1] ? cou : o[j - 1]);
+            }
+            d[0] = lt[0] ? d[0] : cdu;
+            o[0] = lt[0] ? o[0] : cou;
+        } else {
+            bool lt[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) lt[j] = d[j] < cdu || (d[j] == cdu && o[j] < cou);
+#pragma unroll
+            for (int j = K - 1; j > 0; --j) {
+                d[j] = lt[j] ? d[j] : (lt[j - 1] ? cdu : d[j - 1]);
+                o[j] = lt[j] ? o[j] : (lt[j - 1] ? cou : o[j - 1]);
+            }
+            d[0] = lt[0] ? d[0] : cdu;
+            o[0] = lt[0] ? o[0] : cou;
+        }
+    }
+};
+
 }  // namespace lbvh

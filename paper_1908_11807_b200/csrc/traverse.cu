@@ -278,6 +278,9 @@ spatial_list_kernel(const lbvh_tree t, const float *__restrict__ centers,
 #ifndef LBVH_KNN_MINBLOCKS
 #define LBVH_KNN_MINBLOCKS 5
 #endif
+#ifndef LBVH_KNN_SPLIT
+#define LBVH_KNN_SPLIT 1  // k-best list as split 32-bit fields (TopKSplit)
+#endif
 #ifndef LBVH_KNN_SMEMSTACK
 #define LBVH_KNN_SMEMSTACK 12
 #endif
@@ -325,7 +328,11 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         return;
     }
     const PackedNode *__restrict__ nodes = reinterpret_cast<const PackedNode *>(t.nodes);
+#if LBVH_KNN_SPLIT
+    TopKSplit<K> top;
+#else
     TopK<K> top;
+#endif
 #ifdef LBVH_KNN_BOUND_FROM_KTH  // instrumentation: start from a given bound (e.g. the exact k-th)
     const float bound = kth ? __ldg(kth + q) : __int_as_float(0x7FFFFFFF);
     kth = nullptr;
@@ -407,10 +414,15 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
     }
     if (fail) atomicOr(status, fail);
 #ifdef LBVH_KNN_COUNT_VISITS  // node visits / kept offers in place of the two nearest distances
+#if LBVH_KNN_SPLIT
+    top.d[0] = __float_as_uint((float)visits * (float)visits);
+    top.d[1] = __float_as_uint((float)top.kept * (float)top.kept);
+#else
     top.key[0] = ((uint64_t)__float_as_uint((float)visits * (float)visits) << 32) |
                  (top.key[0] & 0xFFFFFFFFull);
     top.key[1] = ((uint64_t)__float_as_uint((float)top.kept * (float)top.kept) << 32) |
                  (top.key[1] & 0xFFFFFFFFull);
+#endif
 #endif
     // the k-th squared distance (exact; the sharded search's forwarding bound)
     if (kth) kth[q] = top.dist(K - 1);
