@@ -70,10 +70,9 @@ struct TopK {
 
 
 // The same list held as separate 32-bit fields (distance bits, ordinal + 1),
-// for the kNN traversal: unless a candidate's distance equals a kept one,
-// the distance words alone order it -- one 32-bit compare per slot, where
-// the 64-bit key costs ptxas a >= and a > pair per slot; exact ties take the
-// lexicographic path.  Same order, same results as TopK.
+// for the kNN traversal: the shifts move 32-bit words (the 64-bit key costs
+// ptxas a >= and a > pair plus two SELs per slot), and the distance shift
+// needs no select.  Same order, same results as TopK.
 template <int K>
 struct TopKSplit {
     uint32_t d[K], o[K];
@@ -100,32 +99,22 @@ struct TopKSplit {
 #ifdef LBVH_KNN_COUNT_VISITS
         ++kept;
 #endif
-        bool tie = false;
+        // lexicographic (d, o) < (cd, obj+1): one 64-bit compare of the
+        // register pair per slot (ISETP + ISETP.EX)
+        bool lt[K];
+        const uint64_t c = ((uint64_t)cdu << 32) | cou;
 #pragma unroll
-        for (int j = 0; j < K; ++j) tie |= d[j] == cdu;
-        if (!tie) {
-            bool lt[K];
+        for (int j = 0; j < K; ++j) lt[j] = (((uint64_t)d[j] << 32) | o[j]) < c;
+        // a slot that moves takes the candidate or its predecessor; with lt
+        // lexicographic, that distance is max(d[j-1], cd): one predicated
+        // VIMNMX per slot, one predicated SEL for the ordinal
 #pragma unroll
-            for (int j = 0; j < K; ++j) lt[j] = d[j] < cdu;
-#pragma unroll
-            for (int j = K - 1; j > 0; --j) {
-                d[j] = lt[j] ? d[j] : (lt[j - 1] ? cdu : d[j - 1]);
-                o[j] = lt[j] ? o[j] : (lt[j - 1] ? cou : o[j - 1]);
-            }
-            d[0] = lt[0] ? d[0] : cdu;
-            o[0] = lt[0] ? o[0] : cou;
-        } else {
-            bool lt[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) lt[j] = d[j] < cdu || (d[j] == cdu && o[j] < cou);
-#pragma unroll
-            for (int j = K - 1; j > 0; --j) {
-                d[j] = lt[j] ? d[j] : (lt[j - 1] ? cdu : d[j - 1]);
-                o[j] = lt[j] ? o[j] : (lt[j - 1] ? cou : o[j - 1]);
-            }
-            d[0] = lt[0] ? d[0] : cdu;
-            o[0] = lt[0] ? o[0] : cou;
+        for (int j = K - 1; j > 0; --j) {
+            d[j] = lt[j] ? d[j] : max(d[j - 1], cdu);
+            o[j] = lt[j] ? o[j] : (lt[j - 1] ? cou : o[j - 1]);
         }
+        d[0] = lt[0] ? d[0] : cdu;
+        o[0] = lt[0] ? o[0] : cou;
     }
 };
 
