@@ -210,9 +210,11 @@ __device__ __forceinline__ void store_box(float *mins, float *maxs, int64_t id, 
 __device__ __forceinline__ void store_packed(PackedNode *nodes, int64_t id, const Box &L,
                                              const Box &R, int32_t lc, int32_t rc) {
     PackedNode *p = nodes + id;
-    __stcg(&p->a, make_float4(L.lo[0], L.lo[1], L.lo[2], L.hi[0]));
-    __stcg(&p->b, make_float4(L.hi[1], L.hi[2], R.lo[0], R.lo[1]));
-    __stcg(&p->c, make_float4(R.lo[2], R.hi[0], R.hi[1], R.hi[2]));
+    float4 a, b, c;
+    pack_boxes(L, R, a, b, c);
+    __stcg(&p->a, a);
+    __stcg(&p->b, b);
+    __stcg(&p->c, c);
     __stcg(&p->d, make_int4(lc, rc, 0, 0));
 }
 
@@ -537,11 +539,13 @@ __device__ __forceinline__ void frontier_box(const PackedNode *nodes, const floa
                                              int64_t internal, int64_t id, Box &b) {
     if (id < internal) {
         const PackedNode *pn = nodes + id;
-        const float4 a = ld_rlx<CTA>(&pn->a), c = ld_rlx<CTA>(&pn->b), e = ld_rlx<CTA>(&pn->c);
-        b.lo[0] = min_left(a.x, c.z); b.lo[1] = min_left(a.y, c.w);
-        b.lo[2] = min_left(a.z, e.x);
-        b.hi[0] = max_left(a.w, e.y); b.hi[1] = max_left(c.x, e.z);
-        b.hi[2] = max_left(c.y, e.w);
+        Box L, R;
+        unpack_boxes(ld_rlx<CTA>(&pn->a), ld_rlx<CTA>(&pn->b), ld_rlx<CTA>(&pn->c), L, R);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            b.lo[k] = min_left(L.lo[k], R.lo[k]);
+            b.hi[k] = max_left(L.hi[k], R.hi[k]);
+        }
     } else {
         const float *hi = leaf_maxs_rows ? node_maxs : node_mins;  // point leaves: hi == lo
 #pragma unroll
@@ -668,13 +672,13 @@ finish_rows_kernel(const PackedNode *__restrict__ nodes, int64_t n, bool copy_le
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_internal; i += stride) {
         const PackedNode *p = nodes + i;
-        const float4 a = __ldcs(&p->a), b = __ldcs(&p->b), c = __ldcs(&p->c);
-        node_mins[3 * i] = min_left(a.x, b.z);
-        node_mins[3 * i + 1] = min_left(a.y, b.w);
-        node_mins[3 * i + 2] = min_left(a.z, c.x);
-        node_maxs[3 * i] = max_left(a.w, c.y);
-        node_maxs[3 * i + 1] = max_left(b.x, c.z);
-        node_maxs[3 * i + 2] = max_left(b.y, c.w);
+        Box L, R;
+        unpack_boxes(__ldcs(&p->a), __ldcs(&p->b), __ldcs(&p->c), L, R);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            node_mins[3 * i + k] = min_left(L.lo[k], R.lo[k]);
+            node_maxs[3 * i + k] = max_left(L.hi[k], R.hi[k]);
+        }
     }
     if (copy_leaf_maxs)
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n; i += stride)
@@ -765,12 +769,14 @@ unpack_kernel(const lbvh_tree t, float *__restrict__ node_mins, float *__restric
     }
     if (i >= t.n - 1) return;
     const PackedNode *pn = reinterpret_cast<const PackedNode *>(t.nodes) + i;
-    float4 a = pn->a, b = pn->b, c = pn->c;
+    Box L, R;
+    unpack_boxes(pn->a, pn->b, pn->c, L, R);
     int64_t lc = t.left[i], rc = t.right[i];
-    node_mins[3 * lc] = a.x; node_mins[3 * lc + 1] = a.y; node_mins[3 * lc + 2] = a.z;
-    node_maxs[3 * lc] = a.w; node_maxs[3 * lc + 1] = b.x; node_maxs[3 * lc + 2] = b.y;
-    node_mins[3 * rc] = b.z; node_mins[3 * rc + 1] = b.w; node_mins[3 * rc + 2] = c.x;
-    node_maxs[3 * rc] = c.y; node_maxs[3 * rc + 1] = c.z; node_maxs[3 * rc + 2] = c.w;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        node_mins[3 * lc + k] = L.lo[k]; node_maxs[3 * lc + k] = L.hi[k];
+        node_mins[3 * rc + k] = R.lo[k]; node_maxs[3 * rc + k] = R.hi[k];
+    }
 }
 
 __global__ void morton_f64_kernel(const double *__restrict__ pts, int64_t n, double lo0,

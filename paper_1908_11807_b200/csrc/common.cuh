@@ -13,11 +13,13 @@ constexpr int kStack = LBVH_STACK_CAPACITY;
 constexpr uint32_t kLeafTag = 0x80000000u;
 constexpr int kNumSMs = 148;  // B200
 
-// Traversal layout of one internal node: both child boxes + both links,
-// 64 bytes = four 128-bit loads, 64-byte aligned (half an L2 line).
-//   a = {L.min.x, L.min.y, L.min.z, L.max.x}
-//   b = {L.max.y, L.max.z, R.min.x, R.min.y}
-//   c = {R.min.z, R.max.x, R.max.y, R.max.z}
+// Traversal layout of one internal node: both child boxes, interleaved per
+// coordinate (left, right) so the two children's box distances run as packed
+// f32x2 operations (child_dists), + both links.  64 bytes, 64-byte aligned
+// (half an L2 line), read as two 256-bit loads.
+//   a = {L.min.x, R.min.x, L.min.y, R.min.y}
+//   b = {L.min.z, R.min.z, L.max.x, R.max.x}
+//   c = {L.max.y, R.max.y, L.max.z, R.max.z}
 //   d = {left link, right link, 0, 0}; a leaf link is obj | kLeafTag.
 struct __align__(64) PackedNode {
     float4 a, b, c;
@@ -47,6 +49,69 @@ __device__ __forceinline__ float box_dist_sq(float px, float py, float pz, float
     d = __fadd_rn(d, __fmul_rn(ty, ty));
     d = __fadd_rn(d, __fmul_rn(tz, tz));
     return d;
+}
+
+__device__ __forceinline__ void pack_boxes(const Box &L, const Box &R, float4 &a, float4 &b,
+                                           float4 &c) {
+    a = make_float4(L.lo[0], R.lo[0], L.lo[1], R.lo[1]);
+    b = make_float4(L.lo[2], R.lo[2], L.hi[0], R.hi[0]);
+    c = make_float4(L.hi[1], R.hi[1], L.hi[2], R.hi[2]);
+}
+
+__device__ __forceinline__ void unpack_boxes(const float4 &a, const float4 &b, const float4 &c,
+                                             Box &L, Box &R) {
+    L.lo[0] = a.x; R.lo[0] = a.y; L.lo[1] = a.z; R.lo[1] = a.w;
+    L.lo[2] = b.x; R.lo[2] = b.y; L.hi[0] = b.z; R.hi[0] = b.w;
+    L.hi[1] = c.x; R.hi[1] = c.y; L.hi[2] = c.z; R.hi[2] = c.w;
+}
+
+// Packed fp32 pairs (sm_100 FADD2 / FMUL2): each lane rounds to nearest on
+// its own, so a pair op is bit-identical to the two scalar ops.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t x, uint64_t y) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t x, uint64_t y) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    return r;
+}
+
+// box_dist_sq of both children of a packed record, as pair operations: the
+// same roundings in the same order (per axis lo - v and v - hi, the clamp,
+// then x^2, + y^2, + z^2), so dl / dr equal box_dist_sq bit for bit.
+__device__ __forceinline__ void child_dists(float px, float py, float pz, const float4 &a,
+                                            const float4 &b, const float4 &c, float &dl,
+                                            float &dr) {
+    const uint64_t vx = f2_pack(px, px), vy = f2_pack(py, py), vz = f2_pack(pz, pz);
+    float l0, r0, l1, r1;
+    f2_unpack(f2_sub(f2_pack(a.x, a.y), vx), l0, r0);
+    f2_unpack(f2_sub(vx, f2_pack(b.z, b.w)), l1, r1);
+    const uint64_t gx = f2_pack(fmaxf(fmaxf(l0, l1), 0.0f), fmaxf(fmaxf(r0, r1), 0.0f));
+    f2_unpack(f2_sub(f2_pack(a.z, a.w), vy), l0, r0);
+    f2_unpack(f2_sub(vy, f2_pack(c.x, c.y)), l1, r1);
+    const uint64_t gy = f2_pack(fmaxf(fmaxf(l0, l1), 0.0f), fmaxf(fmaxf(r0, r1), 0.0f));
+    f2_unpack(f2_sub(f2_pack(b.x, b.y), vz), l0, r0);
+    f2_unpack(f2_sub(vz, f2_pack(c.z, c.w)), l1, r1);
+    const uint64_t gz = f2_pack(fmaxf(fmaxf(l0, l1), 0.0f), fmaxf(fmaxf(r0, r1), 0.0f));
+    // Squares as pairs, sums as scalar add.rn: ptxas 12.9 contracts
+    // mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (even with --fmad=false), which
+    // would round once instead of twice; a scalar add.rn is never contracted.
+    float xl, xr, yl, yr, zl, zr;
+    f2_unpack(f2_mul(gx, gx), xl, xr);
+    f2_unpack(f2_mul(gy, gy), yl, yr);
+    f2_unpack(f2_mul(gz, gz), zl, zr);
+    dl = __fadd_rn(__fadd_rn(xl, yl), zl);
+    dr = __fadd_rn(__fadd_rn(xr, yr), zr);
 }
 
 // Refit tie rules of numba's min/max (first argument wins ties,

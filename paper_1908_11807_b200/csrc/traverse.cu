@@ -179,8 +179,8 @@ __device__ __forceinline__ void spatial_query(const lbvh_tree &t,
         float4 a, b, c;
         int4 d;
         load_node(nodes, node, a, b, c, d);
-        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
-        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        float dl, dr;
+        child_dists(px, py, pz, a, b, c, dl, dr);
         int32_t next = -1;
         // left child, then right child (_kernels.py:212-225)
         if (dl <= r2) {
@@ -372,8 +372,8 @@ __device__ __forceinline__ void knn_query(const lbvh_tree &t, const float *__res
         ++visits;
 #endif
         load_node(nodes, node, a, b, c, dd);
-        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
-        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        float dl, dr;
+        child_dists(px, py, pz, a, b, c, dl, dr);
         // farther child first so the nearer one is on top (_kernels.py:373-379)
         const bool left_near = dl <= dr;
         const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
@@ -529,8 +529,8 @@ knn_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
         float4 a, b, c;
         int4 dd;
         load_node(nodes, node, a, b, c, dd);
-        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
-        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        float dl, dr;
+        child_dists(px, py, pz, a, b, c, dl, dr);
         const bool left_near = dl <= dr;
         const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
         const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
@@ -652,8 +652,8 @@ knn_smem_heap_kernel(const lbvh_tree t, const float *__restrict__ centers,
         float4 a, b, c;
         int4 dd;
         load_node(nodes, (int32_t)(uint32_t)e, a, b, c, dd);
-        const float dl = box_dist_sq(px, py, pz, a.x, a.y, a.z, a.w, b.x, b.y);
-        const float dr = box_dist_sq(px, py, pz, b.z, b.w, c.x, c.y, c.z, c.w);
+        float dl, dr;
+        child_dists(px, py, pz, a, b, c, dl, dr);
         const bool left_near = dl <= dr;
         const int32_t fl = left_near ? dd.y : dd.x, nl = left_near ? dd.x : dd.y;
         const float fd = left_near ? dr : dl, ndist = left_near ? dl : dr;
