@@ -183,6 +183,14 @@ __device__ __forceinline__ void ldg256(const void *p, float4 &x, float4 &y) {
         : "l"(p));
 }
 
+// 32-byte store (sm_100 STG.E.ENL2.256): one full L2 sector per store.
+__device__ __forceinline__ void stg256(void *p, float4 x, float4 y) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                 :: "l"(p), "f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w), "f"(y.x), "f"(y.y),
+                    "f"(y.z), "f"(y.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // 16-byte shared-memory store / load the compiler may not move across fences
