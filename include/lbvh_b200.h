@@ -145,7 +145,10 @@ int lbvh_finish_rows(const lbvh_tree *tree, float *node_mins, float *node_maxs, 
 
 /* Leaf directory over the build's sorted 30-bit leaf codes (kNN seed index;
  * no reference counterpart).  lbvh_leaf_directory_bits(n) is the bucket
- * count exponent used by the Python layer (n/8 leaves per bucket, <= 24). */
+ * count exponent used by the Python layer: a multiple of 3 (buckets are
+ * cubic cells, >= 2.5 leaves each on average, <= 24 bits), which lets the kNN
+ * seed scan the 2x2x2 cells around a query; other bit counts fall back to a
+ * Morton-window seed. */
 int lbvh_leaf_directory_bits(int64_t n);
 int lbvh_leaf_directory(const uint32_t *leaf_codes, int64_t n, int bits, uint32_t *dir,
                         void *stream);

@@ -42,8 +42,8 @@ def test_library_strerror_and_workspace_sizes():
 
 def test_leaf_directory_bits():
     lib = _lib.load_library()
-    assert [lib.lbvh_leaf_directory_bits(n) for n in (1, 15, 16, 17, 10**7, 2**40)] == \
-        [0, 0, 1, 1, 20, 24]
+    assert [lib.lbvh_leaf_directory_bits(n) for n in (1, 19, 20, 10**6, 10**7, 10**8, 2**40)] == \
+        [0, 0, 3, 18, 21, 24, 24]
     assert lib.lbvh_leaf_directory(None, 0, 3, None, None) == 1
 
 
