@@ -14,10 +14,10 @@ namespace lbvh {
 // upper bound of the true k-th distance).  Leaves are found by a lower_bound
 // over the build's sorted leaf codes.
 #ifndef LBVH_SEED_BLOCK_MIN_K
-#define LBVH_SEED_BLOCK_MIN_K 12  // smallest k seeded from the 2x2x2 cell block
+#define LBVH_SEED_BLOCK_MIN_K 2  // smallest k seeded from the 2x2x2 cell block
 #endif
-#ifndef LBVH_SEED_BLOCK_CAP
-#define LBVH_SEED_BLOCK_CAP 96  // leaves scanned at most by the block seed
+#ifndef LBVH_SEED_BLOCK_PER_K
+#define LBVH_SEED_BLOCK_PER_K 2  // leaves scanned per k by the block seed, nearest cells first
 #endif
 
 // Distance^2 of the query to the leaf at sorted position p (point leaves:
@@ -62,11 +62,12 @@ __device__ __forceinline__ uint32_t compact_bits(uint32_t v) {
 // Block seed: when the leaf directory's buckets are cubic cells (bits = 3L),
 // the leaves of the 2x2x2 block of level-L cells around the query (the block
 // whose centre is the cell corner nearest to it) are eight contiguous runs of
-// the sorted leaves.  Their kk-th smallest distance bounds the true k-th
-// distance like any kk real leaves do, and the block holds the query's
-// neighbourhood on all sides (a Morton window follows the curve and is
-// one-sided across its jumps): at C2 the bound is 1.03x the exact k-th
-// distance on average against 1.55x for the 2k-leaf window.  Returns +inf
+// the sorted leaves.  The first 2*kk of them, the query's own cell first,
+// then the cells sharing a face, an edge, the corner, give a bound like any
+// kk real leaves do, and it covers the query's neighbourhood on all sides (a
+// Morton window follows the curve and is one-sided across its jumps): at C2
+// the bound is 1.13x the exact k-th distance on average against 1.55x for
+// the 2k-leaf window, for the same number of distance tests.  Returns +inf
 // when the block holds fewer than kk leaves (the caller falls back to the
 // window).
 template <int K>
@@ -91,34 +92,48 @@ __device__ __forceinline__ float seed_bound_block(const lbvh_tree &t, uint32_t q
     const float *__restrict__ mn = t.node_mins + 3 * (n - 1);
     const bool points = (t.flags & LBVH_TREE_POINT_LEAVES) != 0;
     const float *__restrict__ mx = points ? mn : t.node_maxs + 3 * (n - 1);
-    const uint32_t sx = spread_bits(base[0]) << 2, sy = spread_bits(base[1]) << 1,
-                   sz = spread_bits(base[2]);
-    // cells (x, y, z) and (x, y, z + 1) are consecutive codes when z is even:
-    // then each (x, y) column is one run of two cells.  The eight directory
-    // reads are independent of the scan, so all are issued up front.
-    const bool pair = (base[2] & 1u) == 0;
-    const uint32_t sz1 = spread_bits(base[2] + 1);
-    const uint32_t sx1 = spread_bits(base[0] + 1) << 2, sy1 = spread_bits(base[1] + 1) << 1;
+    // the eight cells nearest first: the query's own cell, the three that
+    // share a face with it, the three that share an edge, the opposite corner
+    // (all directory reads issued up front; the scan stops after `cap` leaves)
+    uint32_t sa[3][2];  // spread coordinate of [own, other] cell per axis
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const uint32_t c = compact_bits(qcode >> (2 - a)) >> sh;
+        const uint32_t own = c < base[a] ? base[a] : (c > base[a] + 1 ? base[a] + 1 : c);
+        const uint32_t other = own == base[a] ? base[a] + 1 : base[a];
+        sa[a][0] = spread_bits(own) << (2 - a);
+        sa[a][1] = spread_bits(other) << (2 - a);
+    }
+    constexpr int kOff[8] = {0, 4, 2, 1, 6, 5, 3, 7};  // flip x / y / z bits
     uint32_t lo[8], hi[8];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint32_t cxy = ((c & 2) ? sx1 : sx) | ((c & 1) ? sy1 : sy);
-        const uint32_t c0 = cxy | sz, c1 = cxy | sz1;
-        lo[2 * c] = __ldg(t.leaf_dir + c0);
-        hi[2 * c] = __ldg(t.leaf_dir + c0 + 1);
-        lo[2 * c + 1] = __ldg(t.leaf_dir + c1);
-        hi[2 * c + 1] = __ldg(t.leaf_dir + c1 + 1);
-        if (pair) {  // one run [c0, c1]
-            hi[2 * c] = hi[2 * c + 1];
-            lo[2 * c + 1] = hi[2 * c + 1];
-        }
-    }
-    int scanned = 0;
-#pragma unroll
     for (int r = 0; r < 8; ++r) {
+        const int o = kOff[r];
+        const uint32_t code = sa[0][(o >> 2) & 1] | sa[1][(o >> 1) & 1] | sa[2][o & 1];
+        lo[r] = __ldg(t.leaf_dir + code);
+        hi[r] = __ldg(t.leaf_dir + code + 1);
+    }
+    const int cap = LBVH_SEED_BLOCK_PER_K * kk;
+    int scanned = 0, left = 7;
+    uint32_t p = lo[0], e = hi[0];
+    // one flat loop over the runs: the next run shifts into (p, e)
 #pragma unroll 1
-        for (uint32_t p = lo[r]; p < hi[r] && scanned < LBVH_SEED_BLOCK_CAP; ++p, ++scanned)
+    while (scanned < cap) {
+        if (p < e) {
             seed_insert<K>(best, seed_leaf_dist(mn, mx, points, p, px, py, pz));
+            ++p;
+            ++scanned;
+        } else {
+            if (left == 0) break;
+            --left;
+#pragma unroll
+            for (int r = 0; r < 7; ++r) {
+                lo[r] = lo[r + 1];
+                hi[r] = hi[r + 1];
+            }
+            p = lo[0];
+            e = hi[0];
+        }
     }
     return scanned >= kk ? best[K - 1] : INFINITY;
 }
@@ -132,10 +147,9 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
                                             float px, float py, float pz) {
     const int64_t n = t.n;
 #ifndef LBVH_SEED_BLOCK_OFF
-    // k <= 10: the window's 2k leaves are cheaper than the block's ~40 (C2:
-    // 6.22 vs 6.34 ms at k = 10, 2.28 vs 3.18 ms at k = 1); k = 16: the
-    // block's tighter start pays (10.45 -> 9.87 ms)
-    if (K >= 16 && kk >= LBVH_SEED_BLOCK_MIN_K && t.leaf_dir && t.leaf_dir_bits >= 3 &&
+    // lists of <= 4 (k = 1: 2.28 ms window vs 2.39 block, the eight directory
+    // reads and their registers cost more than the 2k leaves save)
+    if (K >= 8 && kk >= LBVH_SEED_BLOCK_MIN_K && t.leaf_dir && t.leaf_dir_bits >= 3 &&
         t.leaf_dir_bits % 3 == 0) {
         const float b = seed_bound_block<K>(t, qcode, kk, px, py, pz);
         if (b != INFINITY) return b;
