@@ -42,6 +42,7 @@ STACK_CAPACITY = _lib.STACK_CAPACITY
 # overlap on three streams (copy engines both ways + SMs).
 _PIPELINE_MIN = 1 << 20
 _PIPELINE_CHUNK = 1 << 20
+_PIPELINE_RAMP = 2  # kNN pipeline: first chunk = chunk >> 2, doubling up to chunk
 
 # Traversal order = stable sort by the top 24 of the 30 Morton bits (3 radix
 # passes instead of 4); ~0.6 queries share a 24-bit cell at 1e7, so warps
@@ -687,6 +688,17 @@ def knn_with_kth(tree: Bvh, centers: torch.Tensor, k: int):
     return out_idx.reshape(nq, span), out_dist.reshape(nq, span), kth
 
 
+def _ramp_chunks(nq: int, chunk: int):
+    """Chunk bounds of a host pipeline: the first chunks grow from chunk/4 so
+    the first D2H (the pipeline's bound) starts after a short H2D + compute
+    head instead of a full chunk's."""
+    c0, size = 0, max(1, chunk >> _PIPELINE_RAMP)
+    while c0 < nq:
+        c1 = min(nq, c0 + size)
+        yield c0, c1
+        c0, size = c1, min(chunk, size * 2)
+
+
 def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> ResultSet:
     """Host kNN batch as an H2D / compute / D2H pipeline over query chunks.
 
@@ -732,8 +744,7 @@ def _knn_pipelined(tree: Bvh, b: _Batch, sort_queries: bool, flags: int = 0) -> 
     ct = tree.ctree()
     root_box = dv.ptr(tree._device()["root_box"])
     c_ptr, o_ptr = dv.ptr(dev_c), dv.ptr(offsets)
-    for c0 in range(0, nq, chunk):
-        c1 = min(nq, c0 + chunk)
+    for c0, c1 in _ramp_chunks(nq, chunk):
         m = c1 - c0
         e_in = torch.cuda.Event()
         with torch.cuda.stream(s_in):
