@@ -27,6 +27,20 @@ for rep in range(10):
         torch.cuda.synchronize()
         res[r].append((time.perf_counter() - t) * 1e3)
         del rs
+r_rad = lb.default_radius(10)
+rres = {r: [] for r in ramps}
+for rep in range(10):
+    for r in ramps:
+        traversal._RADIUS_RAMP = r
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        rs = lb.query_spatial_2p(tree, (host_q, r_rad))
+        torch.cuda.synchronize()
+        rres[r].append((time.perf_counter() - t) * 1e3)
+        del rs
+for r, v in rres.items():
+    v = sorted(v[2:])
+    print(f"radius ramp={r} median_ms={v[len(v) // 2]:.3f} min_ms={v[0]:.3f}")
 for r, v in res.items():
     v = sorted(v[2:])
     print(f"knn ramp={r} median_ms={v[len(v) // 2]:.3f} min_ms={v[0]:.3f}")
