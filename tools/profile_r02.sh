@@ -21,7 +21,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:spat
     -o $OUT/${TAG}_c2_radius python tools/prof_knn.py 10000000 1 10 cube radius > $OUT/${TAG}_ncu_c2r.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:spatial_kernel -s 0 -c 1 \
     -o $OUT/${TAG}_c3_radius python tools/prof_knn.py 10000000 1 10 sphere radius > $OUT/${TAG}_ncu_c3r.log 2>&1
-for tool in memcheck racecheck synccheck initcheck; do
+# compute-sanitizer is closed on some GPU pools: SANITIZE=0 skips it
+[ "${SANITIZE:-1}" = 1 ] && for tool in memcheck racecheck synccheck initcheck; do
   echo "== $tool" >> $OUT/${TAG}_sanitizer.txt
   timeout 900 compute-sanitizer --tool $tool --print-limit 10 python tools/sanitize_smoke.py \
       >> $OUT/${TAG}_sanitizer.txt 2>&1
