@@ -4,8 +4,8 @@
 //   spatial_kernel<FILL>    spatial_pass(store=True)    _kernels.py:179-228
 //   spatial_kernel<BUFFER>  spatial_pass_buffered       _kernels.py:231-282
 //   compact_warp_kernel     compact_rows                _kernels.py:285-290
-//   knn_kernel<K>           knn_pass, k <= K            _kernels.py:293-414
-//   knn_smem_heap_kernel    knn_pass, 16 < k <= 400 (heap in shared memory)
+//   knn_kernel<K>           knn_pass, k <= K <= 32      _kernels.py:293-414
+//   knn_smem_heap_kernel    knn_pass, 32 < k <= 400 (heap in shared memory)
 //   knn_heap_kernel         knn_pass, any k (heap in the output span)
 //
 // One thread per query slot s; slot s serves query order[s], so Morton-sorted
@@ -291,6 +291,12 @@ spatial_list_kernel(const lbvh_tree t, const float *__restrict__ centers,
 #endif
 #ifndef LBVH_KNN16_MINBLOCKS
 #define LBVH_KNN16_MINBLOCKS 3  // k=16: 14.3 ms vs 14.6 (4) and 15.7 (5, spills)
+#endif
+#ifndef LBVH_KNN_HEAP_MIN
+#define LBVH_KNN_HEAP_MIN 33  // smallest k on the shared-memory heap (below: register lists)
+#endif
+#ifndef LBVH_KNN_K24
+#define LBVH_KNN_K24 1  // a 24-slot register list between the 16- and 32-slot ones
 #endif
 #ifndef LBVH_KNN32_MINBLOCKS
 #define LBVH_KNN32_MINBLOCKS 2
@@ -929,10 +935,14 @@ int knn(const lbvh_tree *t, const float *centers, const uint32_t *order,
     LBVH_KNN_CASE(4)
     LBVH_KNN_CASE(8)
     LBVH_KNN_CASE(10)
-    // smallest k on the shared-memory heap path: k = 24 / 32 run at 23.9 / 31.7 ms there vs
-    // 33.9 / 42.2 ms with 32-slot register lists (C2); k = 16 stays in registers (14.3 vs 18.6)
-    if (max_span <= 16 || kth) {
+    // register lists up to k = 32 (split lists + block seed, round 2): C2 k = 20 / 24 / 32
+    // 14.3 / 15.9 / 27.9 ms with 24- and 32-slot lists vs 21.1 / 23.7 / 31.5 ms on the
+    // shared-memory heap (which round 1 preferred above k = 16: 23.9 vs 33.9 ms at k = 24)
+    if (max_span < LBVH_KNN_HEAP_MIN || kth) {
         LBVH_KNN_CASE(16)
+#if LBVH_KNN_K24
+        LBVH_KNN_CASE(24)
+#endif
         LBVH_KNN_CASE(32)
     }
 #undef LBVH_KNN_CASE
