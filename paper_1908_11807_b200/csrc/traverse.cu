@@ -282,7 +282,7 @@ spatial_list_kernel(const lbvh_tree t, const float *__restrict__ centers,
 #define LBVH_KNN_SPLIT 1  // k-best list as split 32-bit fields (TopKSplit)
 #endif
 #ifndef LBVH_KNN_SMEMSTACK
-#define LBVH_KNN_SMEMSTACK 12
+#define LBVH_KNN_SMEMSTACK 8  // with the block seed: C2 5.71-5.75 vs 5.77 ms (12), 5.72 (6), 5.74 (4), 5.78 (10)
 #endif
 // Threads per CTA of knn_kernel (resident threads per SM stay
 // LBVH_KNN_MINBLOCKS * 256 for K <= 16).
