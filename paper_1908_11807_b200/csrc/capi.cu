@@ -173,15 +173,9 @@ int lbvh_unpack_boxes(const lbvh_tree *tree, float *node_mins, float *node_maxs,
 int lbvh_leaf_directory_bits(int64_t n) {
     // cubic cells (3L bits) of >= 2.5 leaves on average: the kNN block seed
     // scans the 2x2x2 cells around a query (about 20-50 leaves)
-#ifndef LBVH_SEED_BLOCK_OFF
     int L = 0;
     while (L < 8 && 5 * ((int64_t)1 << (3 * (L + 1))) <= 2 * n) ++L;
     return 3 * L;
-#else  // A/B builds: round-2 directory (n/8 leaves per bucket), window seed only
-    int b = 0;
-    while (b < 24 && ((int64_t)8 << (b + 1)) <= n) ++b;
-    return b == 21 ? 20 : b;
-#endif
 }
 
 int lbvh_leaf_directory(const uint32_t *leaf_codes, int64_t n, int bits, uint32_t *dir,

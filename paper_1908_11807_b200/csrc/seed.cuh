@@ -146,7 +146,6 @@ template <int K>
 __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, int kk,
                                             float px, float py, float pz) {
     const int64_t n = t.n;
-#ifndef LBVH_SEED_BLOCK_OFF
     // lists of <= 4 (k = 1: 2.28 ms window vs 2.39 block, the eight directory
     // reads and their registers cost more than the 2k leaves save)
     if (K >= 8 && kk >= LBVH_SEED_BLOCK_MIN_K && t.leaf_dir && t.leaf_dir_bits >= 3 &&
@@ -154,7 +153,6 @@ __device__ __forceinline__ float seed_bound(const lbvh_tree &t, uint32_t qcode, 
         const float b = seed_bound_block<K>(t, qcode, kk, px, py, pz);
         if (b != INFINITY) return b;
     }
-#endif
     const uint32_t *__restrict__ codes = t.leaf_codes;
     int64_t lo = 0, hi = n;
     if (t.leaf_dir) {
