@@ -1,4 +1,10 @@
-// seed.cuh -- exact search-radius seed of the kNN kernels.
+// seed.cuh -- exact search-radius seed of the kNN kernels: the kk-th smallest
+// distance^2 among 2*kk real leaves near the query bounds its true k-th
+// distance from above, so the traversal prunes from the first node on and
+// results cannot change.  Two ways to pick the leaves: the 2x2x2 block of
+// leaf-directory cells around the query (seed_bound_block, lists of K >= 8)
+// and the Morton window around its code (seed_bound, the fallback).
+
 #pragma once
 
 #include "common.cuh"
@@ -8,11 +14,6 @@ namespace lbvh {
 #ifndef LBVH_SEED_WINDOW
 #define LBVH_SEED_WINDOW 2  // leaves per k in the Morton window
 #endif
-
-// Search-radius seed for one query: the kk-th smallest distance^2 among the
-// 2*kk leaves that neighbour the query's Morton code in leaf order (a real
-// upper bound of the true k-th distance).  Leaves are found by a lower_bound
-// over the build's sorted leaf codes.
 #ifndef LBVH_SEED_BLOCK_MIN_K
 #define LBVH_SEED_BLOCK_MIN_K 2  // smallest k seeded from the 2x2x2 cell block
 #endif
