@@ -17,8 +17,8 @@ namespace lbvh {
 #ifndef LBVH_SEED_BLOCK_MIN_K
 #define LBVH_SEED_BLOCK_MIN_K 2  // smallest k seeded from the 2x2x2 cell block
 #endif
-#ifndef LBVH_SEED_BLOCK_PER_K
-#define LBVH_SEED_BLOCK_PER_K 2  // leaves scanned per k by the block seed, nearest cells first
+#ifndef LBVH_SEED_BLOCK_QUARTERS
+#define LBVH_SEED_BLOCK_QUARTERS 8  // leaves scanned by the block seed: kk * QUARTERS / 4, nearest cells first
 #endif
 
 // Distance^2 of the query to the leaf at sorted position p (point leaves:
@@ -114,7 +114,7 @@ __device__ __forceinline__ float seed_bound_block(const lbvh_tree &t, uint32_t q
         lo[r] = __ldg(t.leaf_dir + code);
         hi[r] = __ldg(t.leaf_dir + code + 1);
     }
-    const int cap = LBVH_SEED_BLOCK_PER_K * kk;
+    const int cap = (LBVH_SEED_BLOCK_QUARTERS * kk) >> 2;
     int scanned = 0, left = 7;
     uint32_t p = lo[0], e = hi[0];
     // one flat loop over the runs: the next run shifts into (p, e)
