@@ -147,6 +147,27 @@ def test_c2_against_independent_oracle_tree():
     assert rk.distances.tobytes() == kd.tobytes()
 
 
+def test_knn_5e7_block_seed_level8_against_oracle():
+    """5e7 points: the leaf directory reaches 24 bits (the block seed's
+    level-8 cells); a 100k-query sample of the full 5e7-query device batch
+    must equal the oracle on its own tree."""
+    from paper_1908_11807_b200 import _lib
+
+    n, sample = 50_000_000, 100_000
+    assert _lib.lib().lbvh_leaf_directory_bits(n) == 24
+    pts = datasets.generate(datasets.CloudSpec("cube", "filled", n, 0))
+    q = datasets.generate(datasets.CloudSpec("cube", "filled", n, 1))
+    t = lb.build(torch.from_numpy(pts).cuda())
+    rs = lb.query_knn(t, (torch.from_numpy(q).cuda(), 10))
+    idx = rs.indices.view(n, 10)[:sample].cpu().numpy().reshape(-1)
+    dist = rs.distances.view(n, 10)[:sample].cpu().numpy().reshape(-1)
+    del rs, t
+    ref = oracle.build(pts)
+    ko, ki, kd = oracle.query_knn(ref, q[:sample], 10)
+    assert np.array_equal(idx, ki)
+    assert dist.tobytes() == kd.tobytes()
+
+
 @pytest.mark.parametrize("name", ["c2_filled", "c3_hollow_sphere"])
 def test_large_tree_structure(large, name):
     """Size-independent properties on the full trees: every
